@@ -1,0 +1,44 @@
+# Build for the B200 Store-zechin engine. Everything is built in-tree so the
+# shared objects travel to the GPU box with the gpurun snapshot.
+#
+#   paper_1802_02779_b200/libpermlab_b200.so  CUDA kernels + C ABI (include/permlab_b200.h)
+#   paper_1802_02779_b200/libpermlab.so       C++ host API (include/permlab/*.hpp) over the C ABI
+#   paper_1802_02779_b200/libpermlab_gen.so   seeded config generators (C1..C5)
+#   tests/cpp/test_permanent_device           C++ parity suite over the host API
+#   oracle/liboracle.so (+ oracle/_ref/...)   CPU checkers (test infrastructure)
+NVCC ?= nvcc
+PKG := paper_1802_02779_b200
+CSRC := $(PKG)/csrc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -Xptxas -warn-spills
+CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude
+CUDA_HOME ?= /usr/local/cuda
+
+KERNEL_HDRS := $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh $(wildcard $(CSRC)/*.cuh) include/permlab_b200.h
+
+all: $(PKG)/libpermlab_b200.so $(PKG)/libpermlab_gen.so $(PKG)/libpermlab.so tests/cpp/test_permanent_device oracle
+
+$(PKG)/libpermlab_b200.so: $(CSRC)/capi.cu $(KERNEL_HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/capi.cu -lcudart
+
+$(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c
+	gcc -O2 -fPIC -ffp-contract=off -std=gnu11 -Wall -shared -o $@ $< -lm
+
+$(PKG)/libpermlab.so: $(CSRC)/host/permanent.cpp $(wildcard include/permlab/*.hpp) include/permlab_b200.h $(PKG)/libpermlab_b200.so
+	g++ $(CXXFLAGS) -shared -o $@ $(CSRC)/host/permanent.cpp -L$(PKG) -lpermlab_b200 -Wl,-rpath,'$$ORIGIN'
+
+tests/cpp/test_permanent_device: tests/cpp/test_permanent_device.cpp $(PKG)/libpermlab.so
+	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lpermlab -lpermlab_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+oracle:
+	$(MAKE) -C oracle all
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; fi
+
+sass: $(PKG)/libpermlab_b200.so
+	cuobjdump -sass $< > profiles/sass_dump.txt
+
+clean:
+	rm -f $(PKG)/*.so tests/cpp/test_permanent_device
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean sass

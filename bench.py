@@ -1,0 +1,400 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Store-zechin engine (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference] [--no-suite]
+
+A "step" is one pass of the hot path over one batch of the config's synthetic
+input. The headline workload is BASELINE.json configs[1] = C2 (100,000
+boson-sampling 5x5 complex128 submatrices); the same JSON line carries a
+"suite" object with every config (C1..C5) measured the same way, so the
+layer kernel (C4/C5) numbers are visible next to the batched ones.
+
+  value  device-resident inputs (in HBM before the timed region), device
+         compute only, CUDA events on the launching stream, L2 flushed
+         between steps (inputs are < L2), max over ranks;
+  e2e    the public API call with pinned HOST buffers: H2D of the inputs,
+         compute, D2H of the results, all inside the timed region;
+  roofline  algorithmic bytes per launch of the dominant kernel (DESIGN.md
+         section 4) / its average CUDA-event duration, against the measured
+         HBM copy bandwidth in MEASURED_PEAKS.json;
+  cpu_baseline  the reference engine itself (oracle/_ref, compiled from the
+         reference sources) on a bounded sample, all host threads.
+
+Multi-GPU (torchrun): batches shard by matrix with no collective, each rank a
+full batch (weak scaling); C4/C5 in the suite use the per-layer all-gather
+schedule (sharded.py, strong scaling).
+
+--impl reference times the reference's own CPU path (oracle/_ref; the oracle
+port for C5, which the reference cannot run) on this config with all host
+threads; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# Algorithmic bytes / ops per unit.
+ELEM = {"int64": 8, "float64": 8, "complex128": 16}
+DT_SHORT = {"int64": "int64", "float64": "f64", "complex128": "c128"}
+
+
+def layer_dp_bytes(n: int, s: int) -> int:
+    """Compulsory traffic of the layer DP: every stored layer 2..n-1 written once
+    and read once (C(n,2) + sum_{k=3}^{n-1} (C(n,k-1) + C(n,k)) + C(n,n-1))."""
+    b = math.comb(n, 2)
+    for k in range(3, n):
+        b += math.comb(n, k - 1) + math.comb(n, k)
+    b += math.comb(n, n - 1)
+    return b * s
+
+
+def algorithmic_bytes_per_perm(n: int, s: int) -> int:
+    if n <= 16:  # batched kernels: the matrix in, one value out
+        return n * n * s + s
+    return layer_dp_bytes(n, s)
+
+
+def flops_per_perm(n: int, dtype: str) -> int:
+    if n == 1:
+        return 0
+    if n == 2:
+        m, a = 2, 1
+    else:
+        m, a = n * 2 ** (n - 1) - n, n * 2 ** (n - 1) - 2 ** n + 1
+    return 6 * m + 2 * a if dtype == "complex128" else m + a
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return {}
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling through NVML."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- workloads
+
+def workload(name: str):
+    from paper_1802_02779_b200 import configs
+
+    spec = configs.CONFIGS[name]
+    a = configs.generate(name)
+    return spec, a
+
+
+def cpu_reference_time(name: str, a: np.ndarray, budget_s: float, threads: int):
+    """Time the reference's own CPU path on a bounded sample: returns
+    (permanents/s, sample description, kind, cores)."""
+    from oracle import oracle as O
+
+    n = a.shape[1]
+    if name == "c5" or not O.ref_available():
+        # order 32 is beyond the reference (mask cap 31, 128 GiB memo): the
+        # oracle port (restated layer DP, all threads) stands in.
+        t = time.perf_counter()
+        O.sz_batch(a[:1], nthreads=threads)
+        dt = time.perf_counter() - t
+        return 1.0 / dt, f"1 matrix n={n} via oracle port ({threads} threads)", "port", threads
+    if n >= 20:  # single large matrix: the reference engine is single-threaded
+        t = time.perf_counter()
+        O.ref_sz_batch(a[:1], nthreads=1, memo_budget_bytes=8 << 30)
+        dt = time.perf_counter() - t
+        return 1.0 / dt, f"1 matrix n={n}, reference engine (single-threaded by design)", "reference", 1
+    done, t0 = 0, time.perf_counter()
+    chunk = a
+    while True:
+        O.ref_sz_batch(chunk, nthreads=threads)
+        done += chunk.shape[0]
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return done / el, f"{done} matrices n={n} ({el:.1f} s wall, {threads} threads, contiguous chunks)", \
+        "reference", threads
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    name = args.config
+    spec, a = workload(name)
+    threads = os.cpu_count() or 1
+    n, count = spec["n"], spec["count"]
+    per_step = []
+    kind, cores, sample = None, None, None
+    for i in range(args.warmup + args.steps):
+        budget = 2.0 if i >= args.warmup else 0.5
+        v, sample, kind, cores = cpu_reference_time(name, a, budget, threads)
+        if i >= args.warmup:
+            per_step.append(v)
+    value = statistics.mean(per_step)
+    line = {
+        "impl": "reference",
+        "metric": f"permanents/s ({name.upper()}: {spec['desc']})",
+        "value": value, "unit": "permanents/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * count / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DT_SHORT[spec["dtype"]], "data": "synthetic (seeded generator, BASELINE.json recipe)",
+        "config": {"workload": f"{name}: {spec['desc']}", "n": n, "count": count},
+        "cpu_baseline": {"value": value, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "permanents/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- device measurement
+
+def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=False):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_02779_b200 as pl
+
+    spec, a = workload(name)
+    n, count = spec["n"], spec["count"]
+    s = ELEM[spec["dtype"]]
+    stream = torch.cuda.current_stream(device)
+    a_host = torch.from_numpy(a).pin_memory()
+    a_dev = a_host.to(device)
+    status = torch.zeros(1, dtype=torch.int32, device=device)
+    out = torch.empty(count, dtype=a_dev.dtype, device=device)
+    sharded = world > 1 and n >= 20
+    launches_per_step = 1 if n <= 16 else (n - 1)
+
+    def step():
+        if sharded:
+            from paper_1802_02779_b200.sharded import sharded_permanent
+
+            return sharded_permanent(a_dev[0], fma=fma)
+        return pl.store_zechin_permanent_batch(a_dev, out=out, fma=fma, status=status, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    for _ in range(warmup):
+        step()
+    barrier()
+    times = []
+    for _ in range(steps):
+        flush_buf.add_(1)  # evict the (< L2) inputs between timed steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    barrier()
+    if int(status.item()) != 0:
+        raise RuntimeError(f"{name}: device status {int(status.item())}")
+    t_local = sum(times) / 1000.0
+    t = torch.tensor([t_local], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    units = count * steps * (world if not sharded else 1)
+    value = units / t_max
+    ms_step = 1000.0 * t_max / steps
+
+    # e2e through the public API with pinned host buffers (H2D + compute + D2H inside)
+    out_host = torch.empty(count, dtype=a_dev.dtype).pin_memory()
+    e2e_steps = max(1, min(steps, 5 if n >= 26 else steps))
+    barrier()
+    e2e_times = []
+    for _ in range(e2e_steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if sharded:
+            from paper_1802_02779_b200.sharded import sharded_permanent
+
+            ad = a_host.to(device, non_blocking=True)
+            v = sharded_permanent(ad[0], fma=fma)
+            out_host[0] = v
+        else:
+            pl.store_zechin_permanent_batch(a_host, out=out_host, fma=fma, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    te = torch.tensor([sum(e2e_times) / 1000.0], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = count * e2e_steps * (world if not sharded else 1) / float(te.item())
+
+    bytes_per_launch = algorithmic_bytes_per_perm(n, s) * count
+    per_launch_s = t_local / steps
+    return {
+        "name": name, "spec": spec, "value": value, "ms_per_step": ms_step, "t_max": t_max,
+        "e2e": {"value": e2e_value, "unit": "permanents/s", "h2d_bytes_per_step": count * n * n * s,
+                "d2h_bytes_per_step": count * s},
+        "algorithmic_bytes_per_step": bytes_per_launch, "per_step_s": per_launch_s,
+        "launches_per_step": launches_per_step, "flops_per_step": flops_per_perm(n, spec["dtype"]) * count,
+        "sharded": sharded,
+    }
+
+
+def roofline_of(res, peak, peak_src, traffic):
+    achieved = res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9
+    tr = traffic.get(res["name"])
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": tr, "peak_source": peak_src,
+            "kernel": "sz_batch_regs_kernel" if res["spec"]["n"] <= 6 else (
+                "sz_batch_smem_kernel" if res["spec"]["n"] <= 16 else "sz_layer_kernel (all layers of one step)"),
+            "fp_rate_tflops": res["flops_per_step"] / res["per_step_s"] / 1e12}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fma", action="store_true", help="allow FMA contraction (not the reference rounding order)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    flush_buf = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB > 126 MB L2
+    peak, peak_src = load_peaks()
+    traffic = load_traffic()
+
+    with ClockSampler(local) as clocks:
+        head = measure_config(args.config, args.steps, args.warmup, rank, world, device, flush_buf, args.fma)
+        suite = {}
+        if not args.no_suite:
+            for name in ("c1", "c2", "c3", "c4", "c5"):
+                k = {"c1": 10, "c2": 10, "c3": 10, "c4": 5, "c5": 2}[name]
+                r = head if name == args.config else measure_config(name, k, 3, rank, world, device, flush_buf,
+                                                                    args.fma)
+                suite[name] = {"value": r["value"], "unit": "permanents/s", "ms_per_step": r["ms_per_step"],
+                               "steps": args.steps if name == args.config else k,
+                               "time_to_permanent_ms": r["ms_per_step"] if r["spec"]["count"] == 1 else None,
+                               "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"],
+                               "sharded_allgather": r["sharded"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        _, a = workload(args.config)
+        v, sample, kind, cores = cpu_reference_time(args.config, a, 10.0, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        spec = head["spec"]
+        line = {
+            "metric": f"permanents/s ({args.config.upper()}: {spec['desc']})",
+            "value": head["value"], "unit": "permanents/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak" if not head["sharded"] else "strong", "vs_baseline": None,
+            "dtype": DT_SHORT[spec["dtype"]],
+            "data": "synthetic (seeded generators following BASELINE.json recipes; no public dataset)",
+            "config": {"workload": f"{args.config}: {spec['desc']}", "n": spec["n"], "count": spec["count"],
+                       "per_rank_count": spec["count"], "l2": "flushed between timed steps (256 MiB write)",
+                       "arith": "fma" if args.fma else "reference rounding order (no FMA)",
+                       "parallelism": f"dp{world} (batch by matrix, no collective)"},
+            "roofline": roofline_of(head, peak, peak_src, traffic),
+            "cpu_baseline": cpu,
+            "e2e": head["e2e"],
+            "clocks": clocks.summary(),
+            "gpu_launches": head["launches_per_step"] * args.steps,
+            "suite": suite,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,212 @@
+// permlab C++ host API, device-backed.
+//
+// Drop-in for the reference's Store-zechin entry points (reference
+// proj/include/permlab/permanent.hpp:34-96) with the same names, argument
+// meaning and error type; every call runs on the B200 through the C ABI in
+// include/permlab_b200.h. Deviations, all documented in DESIGN.md:
+//   * Int is int64_t with a guard (DomainError when an intermediate could
+//     reach 2^63) instead of arbitrary precision (reference ring.hpp:31);
+//   * a Real (double) ring is added; Rational is not offered on the device;
+//   * Limits.subset_order_limit defaults to the device cap 34 (reference 30)
+//     and memo_budget_bytes caps device layer scratch (0 = uncapped);
+//   * StoreZechinRun.attribution is computed by a host-side replay of the
+//     reference's DFS visiting order (counting only), not by instrumenting
+//     the device arithmetic.
+#ifndef PERMLAB_B200_PERMANENT_HPP
+#define PERMLAB_B200_PERMANENT_HPP
+
+#include <complex>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <variant>
+#include <vector>
+
+namespace permlab {
+
+/// Contract violations and exceeded limits (reference errors.hpp:24-27).
+class DomainError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+/// Resource guards (reference limits.hpp:23-40); PERMLAB_LIMITS overrides
+/// with the reference's key=value syntax (reference limits.cpp:43-76).
+struct Limits {
+    int naive_order_limit = 12;
+    int subset_order_limit = 34;
+    std::uint64_t enumeration_cap = 100000;
+    std::uint64_t memo_budget_bytes = 0;
+    static Limits from_env();
+};
+
+/// Ring-operation tally (reference op_count.hpp:27-42).
+struct OpCount {
+    std::uint64_t multiplications = 0;
+    std::uint64_t additions = 0;
+    OpCount& operator+=(const OpCount& o) {
+        multiplications += o.multiplications;
+        additions += o.additions;
+        return *this;
+    }
+    friend OpCount operator+(OpCount a, const OpCount& b) { return a += b; }
+    bool operator==(const OpCount&) const = default;
+};
+
+using Int = std::int64_t;
+using Real = double;
+using Cplx = std::complex<double>;
+
+enum class RingTag { Int, Real, Complex };
+using RingElement = std::variant<Int, Real, Cplx>;
+
+std::string_view ring_name(RingTag tag);  // "int" | "real" | "complex"
+RingTag ring_of(const RingElement& v);
+
+inline constexpr double kComplexRelTol = 1e-9;  // reference ring.hpp:49-50
+inline constexpr double kComplexAbsTol = 1e-12;
+bool approx_equal(const Cplx& a, const Cplx& b);
+bool approx_equal(const RingElement& a, const RingElement& b);
+std::string to_string(const RingElement& v);  // %.17g rendering (reference ring.cpp:95-120)
+
+/// Dense row-major n x n matrix over one ring (reference matrix.hpp:50-189).
+template <typename T>
+class Matrix {
+  public:
+    Matrix(int order, std::vector<T> entries) : order_(order), entries_(std::move(entries)) {
+        if (order_ < 1) throw DomainError("matrix order must be >= 1");
+        if (entries_.size() != static_cast<std::size_t>(order_) * static_cast<std::size_t>(order_)) {
+            throw DomainError("entry count does not match order^2");
+        }
+    }
+    static Matrix filled(int order, const T& v) {
+        if (order < 1) throw DomainError("matrix order must be >= 1");
+        return Matrix(order, std::vector<T>(static_cast<std::size_t>(order) * order, v));
+    }
+    static Matrix identity(int order) {
+        Matrix m = filled(order, T(0));
+        for (int i = 0; i < order; ++i) m.entries_[static_cast<std::size_t>(i) * order + i] = T(1);
+        return m;
+    }
+    int order() const { return order_; }
+    const std::vector<T>& entries() const { return entries_; }
+    const T& operator()(int i, int j) const { return entries_[static_cast<std::size_t>(i) * order_ + j]; }
+    Matrix transpose() const {
+        std::vector<T> out(entries_.size());
+        for (int i = 0; i < order_; ++i)
+            for (int j = 0; j < order_; ++j) out[static_cast<std::size_t>(j) * order_ + i] = (*this)(i, j);
+        return Matrix(order_, std::move(out));
+    }
+    /// Entry (i, j) of the result is entry (row_perm[i], col_perm[j]).
+    Matrix permute(const std::vector<int>& row_perm, const std::vector<int>& col_perm) const {
+        std::vector<T> out;
+        out.reserve(entries_.size());
+        for (int i = 0; i < order_; ++i)
+            for (int j = 0; j < order_; ++j) out.push_back((*this)(row_perm.at(i), col_perm.at(j)));
+        return Matrix(order_, std::move(out));
+    }
+    Matrix scale_row(int row, const T& s) const {
+        if (row < 0 || row >= order_) throw DomainError("row index out of range");
+        std::vector<T> out = entries_;
+        for (int j = 0; j < order_; ++j) out[static_cast<std::size_t>(row) * order_ + j] = (*this)(row, j) * s;
+        return Matrix(order_, std::move(out));
+    }
+    /// Minor with the listed rows and columns removed (|rows| == |cols| < order).
+    Matrix remove_rows_cols(const std::vector<int>& rows, const std::vector<int>& cols) const {
+        if (rows.size() != cols.size()) throw DomainError("row and column removal sets must have equal size");
+        if (static_cast<int>(rows.size()) >= order_) throw DomainError("cannot remove all rows of a matrix");
+        std::vector<char> dr(order_, 0), dc(order_, 0);
+        for (int r : rows) dr.at(r) = 1;
+        for (int c : cols) dc.at(c) = 1;
+        const int k = order_ - static_cast<int>(rows.size());
+        std::vector<T> out;
+        for (int i = 0; i < order_; ++i)
+            for (int j = 0; j < order_ && !dr[i]; ++j)
+                if (!dc[j]) out.push_back((*this)(i, j));
+        return Matrix(k, std::move(out));
+    }
+    bool operator==(const Matrix&) const = default;
+
+  private:
+    int order_;
+    std::vector<T> entries_;
+};
+
+/// Ring-erased square matrix (reference matrix.hpp:192-258).
+class SquareMatrix {
+  public:
+    using Variant = std::variant<Matrix<Int>, Matrix<Real>, Matrix<Cplx>>;
+    explicit SquareMatrix(Matrix<Int> m) : m_(std::move(m)) {}
+    explicit SquareMatrix(Matrix<Real> m) : m_(std::move(m)) {}
+    explicit SquareMatrix(Matrix<Cplx> m) : m_(std::move(m)) {}
+    RingTag ring() const { return static_cast<RingTag>(m_.index()); }
+    int order() const {
+        return std::visit([](const auto& m) { return m.order(); }, m_);
+    }
+    template <typename T>
+    const Matrix<T>& as() const {
+        if (const auto* p = std::get_if<Matrix<T>>(&m_)) return *p;
+        throw DomainError("matrix ring mismatch");
+    }
+    const Variant& inner() const { return m_; }
+    /// Pointer to the contiguous entries (int64 / double / interleaved complex).
+    const void* data() const {
+        return std::visit([](const auto& m) -> const void* { return m.entries().data(); }, m_);
+    }
+
+  private:
+    Variant m_;
+};
+
+enum class Algorithm { Naive, Ryser, StoreZechin };
+std::string_view algorithm_name(Algorithm a);
+Algorithm algorithm_from_name(std::string_view name);
+
+struct PermanentResult {
+    RingElement value;
+    OpCount counts;  // the Store-zechin counts n*2^(n-1)-n, n*2^(n-1)-2^n+1
+    Algorithm algorithm;
+};
+
+/// Per-term cost split of the reference's DFS order (reference permanent.hpp:44-48).
+struct AttributionReport {
+    std::vector<OpCount> per_term;
+    std::uint64_t final_combination_adds = 0;
+    OpCount totals;
+};
+
+struct StoreZechinRun {
+    PermanentResult result;
+    AttributionReport attribution;
+    std::uint64_t cache_misses = 0;
+    std::uint64_t distinct_subsets = 0;
+};
+
+/// Options of the zero-copy batch overload.
+struct BatchOptions {
+    bool device_pointers = false;  // entries/out are CUDA device pointers
+    bool allow_fma = false;        // contract products into FMAs (not the reference's rounding order)
+    void* stream = nullptr;        // cudaStream_t
+};
+
+PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limits = {});
+StoreZechinRun store_zechin_run(const SquareMatrix& a, const Limits& limits = {});
+AttributionReport store_zechin_attributed(const SquareMatrix& a, const Limits& limits = {});
+
+/// Batch over matrices of one ring and one order (the reference's callers loop
+/// over store_zechin_permanent, e.g. boson.cpp:262-265).
+std::vector<PermanentResult> store_zechin_permanent_batch(const std::vector<SquareMatrix>& batch,
+                                                          const Limits& limits = {});
+
+/// Zero-copy batch over a contiguous buffer of `count` row-major n x n
+/// matrices; `out` receives `count` values of the ring's element type.
+void store_zechin_permanent_batch(RingTag ring, int n, std::int64_t count, const void* entries, void* out,
+                                  const Limits& limits = {}, const BatchOptions& options = {});
+
+/// Closed-form Store-zechin operation counts (reference cost_model.cpp:176-181).
+OpCount store_zechin_counts(int n);
+
+}  // namespace permlab
+
+#endif  // PERMLAB_B200_PERMANENT_HPP

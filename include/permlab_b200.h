@@ -1,0 +1,146 @@
+/*
+ * permlab-b200 C ABI: the drop-in boundary for the Store-zechin hot path.
+ *
+ * The reference ("permlab", arXiv 1802.02779) has no FFI layer; the path sits
+ * behind free C++ functions in namespace permlab (reference
+ * proj/include/permlab/permanent.hpp:77-100, proj/src/permanent.cpp:414-427).
+ * This header is the thin C layer the B200 engine exports underneath the C++
+ * host API in include/permlab/ (which keeps those signatures); plain pointers
+ * and sizes only, no torch or CUDA types. Every entry point says which
+ * reference interface it replaces.
+ *
+ * Data layout (all entry points):
+ *   - a matrix is n*n entries, row-major (reference Matrix<T>::operator(),
+ *     proj/include/permlab/matrix.hpp:80-82); a batch is `count` matrices
+ *     stored contiguously;
+ *   - PL_I64  entries are int64_t (the reference's exact Int ring,
+ *     ring.hpp:31, restricted to values whose every intermediate fits int64 —
+ *     guarded, never wrapped);
+ *     PL_F64  entries are double (a real ring the reference lacks; it matches
+ *     the reference's Complex ring with imag = 0 bit for bit);
+ *     PL_C128 entries are interleaved (re, im) doubles, the layout of
+ *     std::complex<double> (the reference's Cplx, ring.hpp:35).
+ *
+ * Errors: every call returns a pl_status and sets a thread-local message
+ * readable with pl_last_error(). The C++ layer maps PL_ERR_LIMIT /
+ * PL_ERR_OVERFLOW / PL_ERR_ARG to permlab::DomainError, the reference's error
+ * type (proj/include/permlab/errors.hpp:24-27). There is no CPU fallback: with
+ * no usable CUDA device every compute entry point returns PL_ERR_NODEVICE.
+ */
+#ifndef PERMLAB_B200_H
+#define PERMLAB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pl_status {
+    PL_OK = 0,
+    PL_ERR_ARG = 1,      /* malformed argument (null pointer, n < 1, ...)            */
+    PL_ERR_LIMIT = 2,    /* order or scratch budget exceeds pl_limits               */
+    PL_ERR_OVERFLOW = 3, /* an int64 intermediate would overflow (exact ring guard) */
+    PL_ERR_NOMEM = 4,    /* device allocation failed                                 */
+    PL_ERR_CUDA = 5,     /* CUDA runtime error                                       */
+    PL_ERR_NODEVICE = 6  /* no CUDA device: the engine has no CPU fallback          */
+} pl_status;
+
+typedef enum pl_dtype { PL_I64 = 0, PL_F64 = 1, PL_C128 = 2 } pl_dtype;
+
+/* Resource guards (reference proj/include/permlab/limits.hpp:23-33).
+ * subset_order_limit: reference default 30 with a hard mask cap of 31
+ *   (permanent.cpp:155-157); the device engine uses 64-bit masks and uint32
+ *   colex ranks, so its hard cap is PL_MAX_ORDER (C(34,17) < 2^32) and its
+ *   default is PL_MAX_ORDER.
+ * memo_budget_bytes: the reference caps its 2^n-slot memo table
+ *   (permanent.cpp:247-251); the device engine caps its layer scratch
+ *   (2 * max_k C(n,k) entries) instead. 0 = no cap beyond free device memory. */
+typedef struct pl_limits {
+    int32_t subset_order_limit;
+    uint64_t memo_budget_bytes;
+} pl_limits;
+
+#define PL_MAX_ORDER 34
+
+/* flags */
+#define PL_FLAG_DEVICE_PTRS 0x1u /* `a` and `out` are device pointers (else host)           */
+#define PL_FLAG_FMA 0x2u         /* allow fused multiply-add: faster, not the reference's   */
+                                 /* bitwise rounding sequence (still <= 1e-9 relative)      */
+#define PL_FLAG_ASYNC 0x4u       /* device pointers only: enqueue on `stream` and return;   */
+                                 /* int64 overflow is reported into *status_dev instead     */
+
+/* Bits OR-ed into a caller-owned device status word by PL_FLAG_ASYNC calls. */
+#define PL_STATUS_BIT_OVERFLOW 0x1
+
+const char* pl_version(void);
+const char* pl_last_error(void);
+void pl_limits_default(pl_limits* out);
+/* Number of CUDA devices visible (0 if none or the driver is unusable). */
+int32_t pl_device_count(void);
+
+/* Single permanent. Replaces permlab::store_zechin_permanent
+ * (reference permanent.hpp:90, permanent.cpp:418-420). `out` receives one
+ * entry of `dtype`. `stream` is a cudaStream_t (NULL = the calling thread's
+ * default stream). Synchronous unless PL_FLAG_ASYNC. */
+pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, uint32_t flags,
+                          const pl_limits* limits, void* stream);
+
+/* Batch of `count` permanents of order n. The reference has no batch entry
+ * point: this replaces its callers' loops over store_zechin_permanent
+ * (reference boson.cpp:262-265 via outcome_probability boson.cpp:229-240).
+ * With PL_FLAG_ASYNC, `status_dev` (device int32, caller-zeroed) receives
+ * PL_STATUS_BIT_* bits; otherwise it may be NULL. */
+pl_status pl_sz_permanent_batch(pl_dtype dtype, int32_t n, int64_t count, const void* a, void* out,
+                                uint32_t flags, const pl_limits* limits, void* stream, int32_t* status_dev);
+
+/* Operation counts of the Store-zechin recurrence (reference measures them
+ * through Counted<T>, op_count.hpp:52-70; closed form cost_model.cpp:176-181):
+ * n = 1 -> (0, 0); n = 2 -> (2, 1); n >= 3 -> (n*2^(n-1) - n, n*2^(n-1) - 2^n + 1). */
+pl_status pl_sz_counts(int32_t n, uint64_t* multiplications, uint64_t* additions);
+
+/* Memo diagnostics of permlab::store_zechin_run (reference permanent.hpp:66-73):
+ * every subset of size 2..n-1 is evaluated exactly once, so
+ * cache_misses = distinct_subsets = 2^n - n - 2 for n >= 3, 1 for n = 2, 0 for n = 1. */
+pl_status pl_sz_diagnostics(int32_t n, uint64_t* cache_misses, uint64_t* distinct_subsets);
+
+/* ---- layer primitives (sharded multi-GPU driver, tests) -------------------
+ * Layer k (2 <= k <= n-1) holds per(S) for every k-subset S of the columns
+ * over the leading k rows, stored at its colex rank
+ * rank(S) = sum_i C(s_i, i), s_1 < ... < s_k. */
+
+/* Binomial coefficient C(s, k) (0 outside the table, s <= 64). */
+uint64_t pl_binom(int32_t s, int32_t k);
+/* Colex rank of a k-subset bitmask and its inverse. */
+uint64_t pl_colex_rank(uint64_t mask);
+uint64_t pl_colex_unrank(int32_t k, uint64_t rank);
+
+/* Compute entries [rank_begin, rank_end) of layer k into cur_dev[rank] from
+ * layer k-1 in prev_dev (ignored for k = 2). All pointers are device
+ * pointers; `a_dev` is the n*n matrix. Asynchronous on `stream`. For PL_I64
+ * the caller must have run pl_sz_guard_i64 on the same matrix first (its
+ * device flag selects the checked path) and passes that flag in guard_dev. */
+pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,
+                      void* cur_dev, uint64_t rank_begin, uint64_t rank_end, uint32_t flags,
+                      const int32_t* guard_dev, int32_t* status_dev, void* stream);
+
+/* Top level: out_dev[0] = sum_j a[n-1][j] * layer_{n-1}[n-1-j], j ascending
+ * (reference permanent.cpp:288-302). n >= 3. Asynchronous. */
+pl_status pl_sz_top(pl_dtype dtype, int32_t n, const void* a_dev, const void* last_layer_dev, void* out_dev,
+                    uint32_t flags, const int32_t* guard_dev, int32_t* status_dev, void* stream);
+
+/* int64 overflow guard for one matrix: guard_dev[0] = 1 when
+ * prod_i max(1, sum_j |a_ij|) >= 2^63 (then kernels use checked arithmetic
+ * and report PL_STATUS_BIT_OVERFLOW on an actual overflow). Asynchronous. */
+pl_status pl_sz_guard_i64(int32_t n, const int64_t* a_dev, int32_t* guard_dev, void* stream);
+
+/* Device scratch bytes a single-matrix run of order n needs (two layer
+ * buffers of max_k C(n,k) entries). */
+uint64_t pl_sz_scratch_bytes(pl_dtype dtype, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERMLAB_B200_H */

@@ -1,0 +1,207 @@
+// TEST INFRASTRUCTURE ONLY (oracle/_ref). A C-callable wrapper around the
+// reference engine compiled UNMODIFIED from /root/reference/proj/src
+// (permanent.cpp, limits.cpp, ring.cpp, matrix.cpp, boson.cpp) against the
+// Boost shim in oracle/shim. It exists so tests can pin the oracle
+// restatement (sz_oracle.c) and the config generators against the
+// reference itself, and so bench.py can time the reference's own CPU path
+// ("cpu_baseline.kind = reference"). Nothing in the product links it.
+//
+// Entry points wrap the reference's public API:
+//   permlab::store_zechin_permanent / store_zechin_run
+//       (reference include/permlab/permanent.hpp:90,96)
+//   permlab::naive_permanent / ryser_permanent   (permanent.hpp:77,84)
+//   permlab::haar_unitary                         (include/permlab/boson.hpp)
+// Status codes: 0 ok, 1 DomainError (message via ref_last_error), 2 the value
+// (or an intermediate) left the shim's 128-bit range, 3 other exception.
+#include <algorithm>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "permlab/boson.hpp"
+#include "permlab/permanent.hpp"
+
+using namespace permlab;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+Limits make_limits(int subset_order_limit, std::uint64_t memo_budget_bytes) {
+    Limits l;
+    if (subset_order_limit > 0) l.subset_order_limit = subset_order_limit;
+    if (memo_budget_bytes > 0) l.memo_budget_bytes = memo_budget_bytes;
+    l.naive_order_limit = 12;
+    return l;
+}
+
+SquareMatrix int_matrix(int n, const std::int64_t* a) {
+    std::vector<Int> e(static_cast<std::size_t>(n) * n);
+    for (std::size_t i = 0; i < e.size(); ++i) e[i] = Int(static_cast<long long>(a[i]));
+    return SquareMatrix(Matrix<Int>(n, std::move(e)));
+}
+
+SquareMatrix cplx_matrix(int n, const double* a, bool real_only) {
+    std::vector<Cplx> e(static_cast<std::size_t>(n) * n);
+    for (std::size_t i = 0; i < e.size(); ++i) {
+        e[i] = real_only ? Cplx(a[i], 0.0) : Cplx(a[2 * i], a[2 * i + 1]);
+    }
+    return SquareMatrix(Matrix<Cplx>(n, std::move(e)));
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const DomainError& e) {
+        g_last_error = e.what();
+        return 1;
+    } catch (const std::overflow_error& e) {
+        g_last_error = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return 3;
+    }
+}
+
+void put_int(const RingElement& v, std::int64_t* lo, std::int64_t* hi) {
+    const __int128 w = std::get<Int>(v).raw();
+    *lo = static_cast<std::int64_t>(static_cast<std::uint64_t>(w));
+    *hi = static_cast<std::int64_t>(w >> 64);
+}
+
+void put_cplx(const RingElement& v, double* out) {
+    const Cplx z = std::get<Cplx>(v);
+    out[0] = z.real();
+    out[1] = z.imag();
+}
+
+template <typename Body>
+int run_chunks(std::int64_t count, int nthreads, Body&& body) {
+    nthreads = std::max(1, nthreads);
+    std::vector<int> status(static_cast<std::size_t>(nthreads), 0);
+    std::vector<std::thread> pool;
+    const std::int64_t per = (count + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        const std::int64_t b0 = t * per;
+        const std::int64_t b1 = std::min<std::int64_t>(count, b0 + per);
+        pool.emplace_back([&, t, b0, b1] {
+            for (std::int64_t b = b0; b < b1 && status[t] == 0; ++b) status[t] = body(b);
+        });
+    }
+    for (auto& th : pool) th.join();
+    for (int s : status) {
+        if (s != 0) return s;
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_last_error.c_str(); }
+
+int ref_sz_i64(int n, const std::int64_t* a, std::int64_t* lo, std::int64_t* hi, std::uint64_t* mults,
+               std::uint64_t* adds, int subset_order_limit, std::uint64_t memo_budget_bytes) {
+    return guarded([&] {
+        const PermanentResult r =
+            store_zechin_permanent(int_matrix(n, a), make_limits(subset_order_limit, memo_budget_bytes));
+        put_int(r.value, lo, hi);
+        if (mults) *mults = r.counts.multiplications;
+        if (adds) *adds = r.counts.additions;
+    });
+}
+
+int ref_sz_c128(int n, const double* a, double* out, std::uint64_t* mults, std::uint64_t* adds,
+                int subset_order_limit, std::uint64_t memo_budget_bytes) {
+    return guarded([&] {
+        const PermanentResult r =
+            store_zechin_permanent(cplx_matrix(n, a, false), make_limits(subset_order_limit, memo_budget_bytes));
+        put_cplx(r.value, out);
+        if (mults) *mults = r.counts.multiplications;
+        if (adds) *adds = r.counts.additions;
+    });
+}
+
+// Real matrices go through Matrix<Cplx> with imag = 0: the reference has no
+// real-double ring (reference include/permlab/ring.hpp:43).
+int ref_sz_f64(int n, const double* a, double* out, int subset_order_limit, std::uint64_t memo_budget_bytes) {
+    return guarded([&] {
+        const PermanentResult r =
+            store_zechin_permanent(cplx_matrix(n, a, true), make_limits(subset_order_limit, memo_budget_bytes));
+        double z[2];
+        put_cplx(r.value, z);
+        out[0] = z[0];
+    });
+}
+
+// store_zechin_run diagnostics: cache_misses, distinct_subsets and the
+// per-term attribution table (2*n entries: mults, adds per term).
+int ref_sz_run_i64(int n, const std::int64_t* a, std::int64_t* lo, std::int64_t* hi, std::uint64_t* misses,
+                   std::uint64_t* distinct, std::uint64_t* per_term, std::uint64_t* final_adds) {
+    return guarded([&] {
+        const StoreZechinRun run = store_zechin_run(int_matrix(n, a), make_limits(0, 0));
+        put_int(run.result.value, lo, hi);
+        *misses = run.cache_misses;
+        *distinct = run.distinct_subsets;
+        for (std::size_t t = 0; t < run.attribution.per_term.size(); ++t) {
+            per_term[2 * t] = run.attribution.per_term[t].multiplications;
+            per_term[2 * t + 1] = run.attribution.per_term[t].additions;
+        }
+        *final_adds = run.attribution.final_combination_adds;
+    });
+}
+
+int ref_naive_i64(int n, const std::int64_t* a, std::int64_t* lo, std::int64_t* hi) {
+    return guarded([&] { put_int(naive_permanent(int_matrix(n, a), make_limits(0, 0)).value, lo, hi); });
+}
+
+int ref_ryser_i64(int n, const std::int64_t* a, std::int64_t* lo, std::int64_t* hi) {
+    return guarded([&] { put_int(ryser_permanent(int_matrix(n, a), make_limits(0, 0)).value, lo, hi); });
+}
+
+int ref_ryser_c128(int n, const double* a, double* out) {
+    return guarded([&] { put_cplx(ryser_permanent(cplx_matrix(n, a, false), make_limits(0, 0)).value, out); });
+}
+
+// Batches through the reference's public single-matrix API (the reference has
+// no batch entry point; its own batch loop is boson.cpp:262-265). Contiguous
+// per-thread chunks; the API is reentrant (reference SPEC.md:191-192).
+int ref_sz_batch_i64(int n, std::int64_t count, const std::int64_t* a, std::int64_t* out_lohi, int nthreads) {
+    return run_chunks(count, nthreads, [&](std::int64_t b) {
+        return ref_sz_i64(n, a + b * n * n, &out_lohi[2 * b], &out_lohi[2 * b + 1], nullptr, nullptr, 0, 0);
+    });
+}
+
+int ref_sz_batch_c128(int n, std::int64_t count, const double* a, double* out, int nthreads) {
+    return run_chunks(count, nthreads, [&](std::int64_t b) {
+        return ref_sz_c128(n, a + 2 * b * n * n, out + 2 * b, nullptr, nullptr, 0, 0);
+    });
+}
+
+int ref_sz_batch_f64(int n, std::int64_t count, const double* a, double* out, int nthreads,
+                     std::uint64_t memo_budget_bytes) {
+    return run_chunks(count, nthreads, [&](std::int64_t b) {
+        return ref_sz_f64(n, a + b * n * n, out + b, 0, memo_budget_bytes);
+    });
+}
+
+int ref_haar(int m, std::uint64_t seed, double* u) {
+    return guarded([&] {
+        const Interferometer itf = haar_unitary(m, seed);
+        const auto& e = itf.unitary().entries();
+        for (std::size_t i = 0; i < e.size(); ++i) {
+            u[2 * i] = e[i].real();
+            u[2 * i + 1] = e[i].imag();
+        }
+    });
+}
+
+}  // extern "C"

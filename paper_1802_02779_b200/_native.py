@@ -1,0 +1,134 @@
+"""ctypes binding of the C ABI in ``include/permlab_b200.h``.
+
+The shared object is built in-tree (``make``, or ``__graft_entry__.build()``)
+and loaded from this package directory. There is no fallback: importing the
+package without the built library raises immediately, and every compute entry
+point fails with ``PL_ERR_NODEVICE`` when no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libpermlab_b200.so"
+GEN_PATH = PKG_DIR / "libpermlab_gen.so"
+
+PL_OK, PL_ERR_ARG, PL_ERR_LIMIT, PL_ERR_OVERFLOW, PL_ERR_NOMEM, PL_ERR_CUDA, PL_ERR_NODEVICE = range(7)
+PL_I64, PL_F64, PL_C128 = 0, 1, 2
+PL_FLAG_DEVICE_PTRS = 0x1
+PL_FLAG_FMA = 0x2
+PL_FLAG_ASYNC = 0x4
+PL_STATUS_BIT_OVERFLOW = 0x1
+PL_MAX_ORDER = 34
+
+STATUS_NAMES = {
+    PL_OK: "PL_OK",
+    PL_ERR_ARG: "PL_ERR_ARG",
+    PL_ERR_LIMIT: "PL_ERR_LIMIT",
+    PL_ERR_OVERFLOW: "PL_ERR_OVERFLOW",
+    PL_ERR_NOMEM: "PL_ERR_NOMEM",
+    PL_ERR_CUDA: "PL_ERR_CUDA",
+    PL_ERR_NODEVICE: "PL_ERR_NODEVICE",
+}
+
+# Every symbol include/permlab_b200.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = (
+    "pl_version",
+    "pl_last_error",
+    "pl_limits_default",
+    "pl_device_count",
+    "pl_sz_permanent",
+    "pl_sz_permanent_batch",
+    "pl_sz_counts",
+    "pl_sz_diagnostics",
+    "pl_binom",
+    "pl_colex_rank",
+    "pl_colex_unrank",
+    "pl_sz_layer",
+    "pl_sz_top",
+    "pl_sz_guard_i64",
+    "pl_sz_scratch_bytes",
+)
+
+
+class pl_limits(C.Structure):
+    _fields_ = [("subset_order_limit", C.c_int32), ("memo_budget_bytes", C.c_uint64)]
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: the B200 engine has no CPU fallback. Build it with "
+            "`make` at the repo root (or __graft_entry__.build())."
+        )
+    L = C.CDLL(str(LIB_PATH))
+    vp, i32, i64, u32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
+    L.pl_version.restype = C.c_char_p
+    L.pl_last_error.restype = C.c_char_p
+    L.pl_limits_default.argtypes = [C.POINTER(pl_limits)]
+    L.pl_limits_default.restype = None
+    L.pl_device_count.restype = i32
+    L.pl_sz_permanent.argtypes = [C.c_int, i32, vp, vp, u32, C.POINTER(pl_limits), vp]
+    L.pl_sz_permanent.restype = C.c_int
+    L.pl_sz_permanent_batch.argtypes = [C.c_int, i32, i64, vp, vp, u32, C.POINTER(pl_limits), vp, vp]
+    L.pl_sz_permanent_batch.restype = C.c_int
+    L.pl_sz_counts.argtypes = [i32, C.POINTER(u64), C.POINTER(u64)]
+    L.pl_sz_counts.restype = C.c_int
+    L.pl_sz_diagnostics.argtypes = [i32, C.POINTER(u64), C.POINTER(u64)]
+    L.pl_sz_diagnostics.restype = C.c_int
+    L.pl_binom.argtypes = [i32, i32]
+    L.pl_binom.restype = u64
+    L.pl_colex_rank.argtypes = [u64]
+    L.pl_colex_rank.restype = u64
+    L.pl_colex_unrank.argtypes = [i32, u64]
+    L.pl_colex_unrank.restype = u64
+    L.pl_sz_layer.argtypes = [C.c_int, i32, vp, i32, vp, vp, u64, u64, u32, vp, vp, vp]
+    L.pl_sz_layer.restype = C.c_int
+    L.pl_sz_top.argtypes = [C.c_int, i32, vp, vp, vp, u32, vp, vp, vp]
+    L.pl_sz_top.restype = C.c_int
+    L.pl_sz_guard_i64.argtypes = [i32, vp, vp, vp]
+    L.pl_sz_guard_i64.restype = C.c_int
+    L.pl_sz_scratch_bytes.argtypes = [C.c_int, i32]
+    L.pl_sz_scratch_bytes.restype = u64
+    return L
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return lib.pl_last_error().decode()
+
+
+_gen = None
+
+
+def gen():
+    """Seeded config generators (``csrc/gen/configs.c``)."""
+    global _gen
+    if _gen is None:
+        if not GEN_PATH.exists():
+            raise ImportError(f"{GEN_PATH} is missing: run `make` at the repo root")
+        G = C.CDLL(str(GEN_PATH))
+        vp, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
+        G.pl_gen_haar.argtypes = [i32, u64, i32, vp]
+        G.pl_gen_haar.restype = C.c_int
+        G.pl_gen_c1.argtypes = [i64, u64, vp]
+        G.pl_gen_c1.restype = None
+        G.pl_gen_c2.argtypes = [i64, u64, vp]
+        G.pl_gen_c2.restype = C.c_int
+        G.pl_gen_c3.argtypes = [i64, u64, vp]
+        G.pl_gen_c3.restype = None
+        G.pl_gen_c4.argtypes = [i32, u64, vp]
+        G.pl_gen_c4.restype = None
+        G.pl_gen_c5.argtypes = [i32, i32, u64, vp]
+        G.pl_gen_c5.restype = C.c_int
+        G.pl_gen_int_matrices.argtypes = [i32, i64, u64, i64, i64, vp]
+        G.pl_gen_int_matrices.restype = None
+        G.pl_gen_uniform.argtypes = [i64, u64, C.c_double, C.c_double, vp]
+        G.pl_gen_uniform.restype = None
+        G.pl_gen_mt64_stream.argtypes = [u64, i64, vp]
+        G.pl_gen_mt64_stream.restype = None
+        _gen = G
+    return _gen

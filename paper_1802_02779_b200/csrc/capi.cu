@@ -1,0 +1,447 @@
+// C ABI of the B200 Store-zechin engine (include/permlab_b200.h).
+//
+// Host-side orchestration only: argument checks mirroring the reference's
+// guards (reference proj/src/permanent.cpp:336-344, :247-251), device
+// scratch from the stream-ordered allocator, kernel selection by order, and
+// error mapping. No CPU arithmetic path exists: without a device every
+// compute call fails with PL_ERR_NODEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/permlab_b200.h"
+#include "sz_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+pl_status fail(pl_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+pl_status cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(PL_ERR_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+    }
+    return fail(PL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define PL_CUDA(expr)                                        \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+    } while (0)
+
+size_t elem_size(pl_dtype d) { return d == PL_C128 ? 16 : 8; }
+
+bool valid_dtype(pl_dtype d) { return d == PL_I64 || d == PL_F64 || d == PL_C128; }
+
+uint64_t max_layer(int n) {
+    uint64_t m = 0;
+    for (int k = 2; k <= n - 1; ++k) m = std::max<uint64_t>(m, pl::binom_u64(n, k));
+    return m;
+}
+
+pl_status have_device() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(PL_ERR_NODEVICE, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    return PL_OK;
+}
+
+pl_status check_order(int n, const pl_limits* lim) {
+    pl_limits d;
+    pl_limits_default(&d);
+    const pl_limits& L = lim ? *lim : d;
+    if (n < 1) return fail(PL_ERR_ARG, "matrix order must be >= 1");
+    if (n > L.subset_order_limit) {
+        return fail(PL_ERR_LIMIT, "matrix order exceeds subset_order_limit (%d)", L.subset_order_limit);
+    }
+    if (n > PL_MAX_ORDER) return fail(PL_ERR_LIMIT, "column-subset algorithms support order <= %d", PL_MAX_ORDER);
+    return PL_OK;
+}
+
+pl_status check_budget(pl_dtype dt, int n, const pl_limits* lim) {
+    if (!lim || lim->memo_budget_bytes == 0) return PL_OK;
+    if (pl_sz_scratch_bytes(dt, n) > lim->memo_budget_bytes) {
+        return fail(PL_ERR_LIMIT, "store-zechin memo table exceeds the configured memory budget");
+    }
+    return PL_OK;
+}
+
+// ---------------------------------------------------------------- dispatch helpers
+
+template <class F>
+pl_status with_ring(pl_dtype dt, bool fma, F&& f) {
+    switch (dt) {
+        case PL_I64:
+            return f(pl::RI64<true>{});
+        case PL_F64:
+            return fma ? f(pl::RF64<true>{}) : f(pl::RF64<false>{});
+        case PL_C128:
+            return fma ? f(pl::RC128<true>{}) : f(pl::RC128<false>{});
+    }
+    return fail(PL_ERR_ARG, "unknown dtype");
+}
+
+constexpr int kRegsThreads = 128;
+constexpr int kRegsMaxOrder = 6;
+
+template <class R, int N>
+pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
+    using T = typename R::T;
+    const size_t smem = (size_t)kRegsThreads * N * N * sizeof(T);
+    auto kern = pl::sz_batch_regs_kernel<R, N, kRegsThreads>;
+    if (smem > 48 * 1024) PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = (count + kRegsThreads - 1) / kRegsThreads;
+    kern<<<(unsigned)blocks, kRegsThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+template <class R>
+pl_status launch_regs(int n, const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
+    switch (n) {
+        case 1: return launch_regs_n<R, 1>(a, out, count, status, st);
+        case 2: return launch_regs_n<R, 2>(a, out, count, status, st);
+        case 3: return launch_regs_n<R, 3>(a, out, count, status, st);
+        case 4: return launch_regs_n<R, 4>(a, out, count, status, st);
+        case 5: return launch_regs_n<R, 5>(a, out, count, status, st);
+        case 6: return launch_regs_n<R, 6>(a, out, count, status, st);
+    }
+    return fail(PL_ERR_ARG, "register kernel order out of range");
+}
+
+size_t smem_binom_bytes() { return ((pl::kBinomDim * pl::kBinomDim * 4 + 15) / 16) * 16; }
+
+size_t smem_per_warp(pl_dtype dt, int n) {
+    return ((size_t)n * n + 2 * (size_t)max_layer(n)) * elem_size(dt);
+}
+
+constexpr size_t kSmemCap = 200 * 1024;
+
+bool smem_fits(pl_dtype dt, int n) { return smem_binom_bytes() + smem_per_warp(dt, n) <= kSmemCap; }
+
+int num_sms() {
+    static int sms = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    });
+    return sms;
+}
+
+template <class R>
+pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t count, int32_t* status,
+                      cudaStream_t st) {
+    using T = typename R::T;
+    const size_t pw = smem_per_warp(dt, n);
+    int warps = (int)std::min<size_t>(8, (kSmemCap - smem_binom_bytes()) / pw);
+    warps = std::max(1, warps);
+    const size_t smem = smem_binom_bytes() + warps * pw;
+    auto kern = pl::sz_batch_smem_kernel<R>;
+    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t need = (count + warps - 1) / warps;
+    const int64_t blocks = std::min<int64_t>(need, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, warps * 32, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, n,
+                                                     (int)max_layer(n), status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+template <class R>
+pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur, uint64_t r0, uint64_t r1,
+                       const int32_t* guard, int32_t* status, cudaStream_t st) {
+    using T = typename R::T;
+    if (r1 <= r0) return PL_OK;
+    const uint64_t cnt = r1 - r0;
+    const int threads = 256;
+    const uint64_t want = (cnt + threads - 1) / threads;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(want, cap);
+    pl::sz_layer_kernel<R><<<blocks, threads, 0, st>>>(static_cast<const T*>(a), n, k, static_cast<const T*>(prev),
+                                                       static_cast<T*>(cur), r0, r1, guard, status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+template <class R>
+pl_status launch_top(int n, const void* a, const void* last, void* out, const int32_t* guard, int32_t* status,
+                     cudaStream_t st) {
+    using T = typename R::T;
+    pl::sz_top_kernel<R><<<1, 32, 0, st>>>(static_cast<const T*>(a), n, static_cast<const T*>(last),
+                                           static_cast<T*>(out), guard, status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+// Full single-matrix layer DP for one device-resident matrix (n >= 3).
+template <class R>
+pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* buf1, const int32_t* guard,
+                     int32_t* status, cudaStream_t st) {
+    void* prev = buf0;
+    void* cur = buf1;
+    pl_status s = launch_layer<R>(n, a_dev, 2, nullptr, prev, 0, pl::binom_u64(n, 2), guard, status, st);
+    if (s != PL_OK) return s;
+    for (int k = 3; k <= n - 1; ++k) {
+        s = launch_layer<R>(n, a_dev, k, prev, cur, 0, pl::binom_u64(n, k), guard, status, st);
+        if (s != PL_OK) return s;
+        std::swap(prev, cur);
+    }
+    return launch_top<R>(n, a_dev, prev, out_dev, guard, status, st);
+}
+
+// Device-side batch compute: a_dev/out_dev device pointers, enqueue only.
+pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
+                        int32_t* status_dev, cudaStream_t st) {
+    if (count == 0) return PL_OK;
+    if (n <= kRegsMaxOrder && !(dt == PL_C128 && n == kRegsMaxOrder)) {
+        return with_ring(dt, fma, [&](auto r) { return launch_regs<decltype(r)>(n, a_dev, out_dev, count, status_dev, st); });
+    }
+    if (smem_fits(dt, n)) {
+        return with_ring(dt, fma,
+                         [&](auto r) { return launch_smem<decltype(r)>(dt, n, a_dev, out_dev, count, status_dev, st); });
+    }
+    // Large orders: one layer DP per matrix through global scratch.
+    const size_t es = elem_size(dt);
+    const uint64_t ml = max_layer(n);
+    void* bufs = nullptr;
+    int32_t* guards = nullptr;
+    PL_CUDA(cudaMallocAsync(&bufs, 2 * ml * es, st));
+    PL_CUDA(cudaMallocAsync((void**)&guards, sizeof(int32_t), st));
+    PL_CUDA(cudaMemsetAsync(guards, 0, sizeof(int32_t), st));
+    pl_status s = PL_OK;
+    for (int64_t b = 0; b < count && s == PL_OK; ++b) {
+        const char* ab = static_cast<const char*>(a_dev) + (size_t)b * n * n * es;
+        char* ob = static_cast<char*>(out_dev) + (size_t)b * es;
+        if (dt == PL_I64) {
+            pl::sz_guard_i64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(ab), n, guards);
+        }
+        s = with_ring(dt, fma, [&](auto r) {
+            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + ml * es, guards, status_dev, st);
+        });
+    }
+    cudaFreeAsync(bufs, st);
+    cudaFreeAsync(guards, st);
+    return s;
+}
+
+// Synchronous wrapper: owns device copies for host pointers and a status
+// word; waits and maps the status word to PL_ERR_OVERFLOW.
+pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,
+                    int32_t* status_dev_user, cudaStream_t st) {
+    const bool dev_ptrs = flags & PL_FLAG_DEVICE_PTRS;
+    const bool fma = flags & PL_FLAG_FMA;
+    const bool async = flags & PL_FLAG_ASYNC;
+    if (async) {
+        if (!dev_ptrs) return fail(PL_ERR_ARG, "PL_FLAG_ASYNC requires PL_FLAG_DEVICE_PTRS");
+        if (!status_dev_user) return fail(PL_ERR_ARG, "PL_FLAG_ASYNC requires a device status word");
+        return enqueue_batch(dt, n, count, a, out, fma, status_dev_user, st);
+    }
+    const size_t es = elem_size(dt);
+    const size_t in_bytes = (size_t)count * n * n * es;
+    const size_t out_bytes = (size_t)count * es;
+    void* a_dev = const_cast<void*>(a);
+    void* out_dev = out;
+    int32_t* status_dev = nullptr;
+    PL_CUDA(cudaMallocAsync((void**)&status_dev, sizeof(int32_t), st));
+    PL_CUDA(cudaMemsetAsync(status_dev, 0, sizeof(int32_t), st));
+    if (!dev_ptrs) {
+        PL_CUDA(cudaMallocAsync(&a_dev, std::max<size_t>(in_bytes, 16), st));
+        PL_CUDA(cudaMallocAsync(&out_dev, std::max<size_t>(out_bytes, 16), st));
+        PL_CUDA(cudaMemcpyAsync(a_dev, a, in_bytes, cudaMemcpyHostToDevice, st));
+    }
+    pl_status s = enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
+    int32_t status_host = 0;
+    if (s == PL_OK) {
+        if (!dev_ptrs) {
+            const cudaError_t e = cudaMemcpyAsync(out, out_dev, out_bytes, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(out)");
+        }
+        const cudaError_t e2 = cudaMemcpyAsync(&status_host, status_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (s == PL_OK && e2 != cudaSuccess) s = cuda_fail(e2, "cudaMemcpyAsync(status)");
+    }
+    if (!dev_ptrs) {
+        cudaFreeAsync(a_dev, st);
+        cudaFreeAsync(out_dev, st);
+    }
+    cudaFreeAsync(status_dev, st);
+    const cudaError_t e3 = cudaStreamSynchronize(st);
+    if (s == PL_OK && e3 != cudaSuccess) s = cuda_fail(e3, "cudaStreamSynchronize");
+    if (s == PL_OK && (status_host & PL_STATUS_BIT_OVERFLOW)) {
+        s = fail(PL_ERR_OVERFLOW,
+                 "int64 overflow: an intermediate sub-permanent does not fit the exact int64 ring");
+    }
+    return s;
+}
+
+pl_status common_checks(pl_dtype dt, int n, int64_t count, const void* a, void* out, const pl_limits* lim) {
+    if (!valid_dtype(dt)) return fail(PL_ERR_ARG, "unknown dtype %d", (int)dt);
+    if (count < 0) return fail(PL_ERR_ARG, "negative batch count");
+    if (count > 0 && (!a || !out)) return fail(PL_ERR_ARG, "null matrix or output pointer");
+    pl_status s = check_order(n, lim);
+    if (s != PL_OK) return s;
+    s = check_budget(dt, n, lim);
+    if (s != PL_OK) return s;
+    return have_device();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pl_version(void) { return "permlab-b200 0.1.0 (sm_100a)"; }
+
+const char* pl_last_error(void) { return g_err.c_str(); }
+
+void pl_limits_default(pl_limits* out) {
+    if (!out) return;
+    out->subset_order_limit = PL_MAX_ORDER;
+    out->memo_budget_bytes = 0;
+}
+
+int32_t pl_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+
+uint64_t pl_binom(int32_t s, int32_t k) {
+    if (s < 0 || k < 0 || k > s || s > 64) return 0;
+    return pl::binom_u64(s, k);
+}
+
+uint64_t pl_colex_rank(uint64_t mask) {
+    uint64_t r = 0;
+    int i = 1;
+    while (mask) {
+        const int s = __builtin_ctzll(mask);
+        r += pl::binom_u64(s, i++);
+        mask &= mask - 1;
+    }
+    return r;
+}
+
+uint64_t pl_colex_unrank(int32_t k, uint64_t rank) {
+    uint64_t mask = 0;
+    int s = 63;
+    for (int i = k; i >= 1; --i) {
+        while (s >= 0 && pl::binom_u64(s, i) > rank) --s;
+        if (s < 0) return 0;
+        mask |= 1ull << s;
+        rank -= pl::binom_u64(s, i);
+        --s;
+    }
+    return mask;
+}
+
+uint64_t pl_sz_scratch_bytes(pl_dtype dtype, int32_t n) {
+    if (n < 3 || n > 64) return 0;
+    return 2 * max_layer(n) * elem_size(dtype);
+}
+
+pl_status pl_sz_counts(int32_t n, uint64_t* mults, uint64_t* adds) {
+    if (n < 1 || n > 63 || !mults || !adds) return fail(PL_ERR_ARG, "bad arguments to pl_sz_counts");
+    if (n == 1) {
+        *mults = 0;
+        *adds = 0;
+    } else if (n == 2) {
+        *mults = 2;
+        *adds = 1;
+    } else {
+        const uint64_t half = 1ull << (n - 1);
+        *mults = (uint64_t)n * half - (uint64_t)n;
+        *adds = (uint64_t)n * half - 2 * half + 1;
+    }
+    return PL_OK;
+}
+
+pl_status pl_sz_diagnostics(int32_t n, uint64_t* misses, uint64_t* distinct) {
+    if (n < 1 || n > 63 || !misses || !distinct) return fail(PL_ERR_ARG, "bad arguments to pl_sz_diagnostics");
+    const uint64_t v = n == 1 ? 0 : n == 2 ? 1 : (1ull << n) - (uint64_t)n - 2;
+    *misses = v;
+    *distinct = v;
+    return PL_OK;
+}
+
+pl_status pl_sz_permanent_batch(pl_dtype dtype, int32_t n, int64_t count, const void* a, void* out, uint32_t flags,
+                                const pl_limits* limits, void* stream, int32_t* status_dev) {
+    pl_status s = common_checks(dtype, n, count, a, out, limits);
+    if (s != PL_OK) return s;
+    return run_batch(dtype, n, count, a, out, flags, status_dev, static_cast<cudaStream_t>(stream));
+}
+
+pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, uint32_t flags,
+                          const pl_limits* limits, void* stream) {
+    if (flags & PL_FLAG_ASYNC) return fail(PL_ERR_ARG, "pl_sz_permanent is synchronous; use the batch entry point");
+    pl_status s = common_checks(dtype, n, 1, a, out, limits);
+    if (s != PL_OK) return s;
+    return run_batch(dtype, n, 1, a, out, flags, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev, void* cur_dev,
+                      uint64_t r0, uint64_t r1, uint32_t flags, const int32_t* guard_dev, int32_t* status_dev,
+                      void* stream) {
+    if (!valid_dtype(dtype)) return fail(PL_ERR_ARG, "unknown dtype");
+    if (n < 3 || n > PL_MAX_ORDER) return fail(PL_ERR_ARG, "layer order out of range");
+    if (k < 2 || k > n - 1) return fail(PL_ERR_ARG, "layer index k must be in [2, n-1]");
+    if (r1 > pl::binom_u64(n, k) || r0 > r1) return fail(PL_ERR_ARG, "rank range outside the layer");
+    if (!a_dev || !cur_dev || (k > 2 && !prev_dev) || !status_dev) return fail(PL_ERR_ARG, "null device pointer");
+    if (dtype == PL_I64 && !guard_dev) return fail(PL_ERR_ARG, "int64 layers need the guard flag");
+    pl_status s = have_device();
+    if (s != PL_OK) return s;
+    return with_ring(dtype, flags & PL_FLAG_FMA, [&](auto r) {
+        return launch_layer<decltype(r)>(n, a_dev, k, prev_dev, cur_dev, r0, r1, guard_dev, status_dev,
+                                         static_cast<cudaStream_t>(stream));
+    });
+}
+
+pl_status pl_sz_top(pl_dtype dtype, int32_t n, const void* a_dev, const void* last_dev, void* out_dev,
+                    uint32_t flags, const int32_t* guard_dev, int32_t* status_dev, void* stream) {
+    if (!valid_dtype(dtype)) return fail(PL_ERR_ARG, "unknown dtype");
+    if (n < 3 || n > PL_MAX_ORDER) return fail(PL_ERR_ARG, "order out of range");
+    if (!a_dev || !last_dev || !out_dev || !status_dev) return fail(PL_ERR_ARG, "null device pointer");
+    pl_status s = have_device();
+    if (s != PL_OK) return s;
+    return with_ring(dtype, flags & PL_FLAG_FMA, [&](auto r) {
+        return launch_top<decltype(r)>(n, a_dev, last_dev, out_dev, guard_dev, status_dev,
+                                       static_cast<cudaStream_t>(stream));
+    });
+}
+
+pl_status pl_sz_guard_i64(int32_t n, const int64_t* a_dev, int32_t* guard_dev, void* stream) {
+    if (n < 1 || n > PL_MAX_ORDER || !a_dev || !guard_dev) return fail(PL_ERR_ARG, "bad guard arguments");
+    pl_status s = have_device();
+    if (s != PL_OK) return s;
+    pl::sz_guard_i64_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const long long*>(a_dev), n, guard_dev);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,375 @@
+// Store-zechin device kernels (sm_100a).
+//
+// The reference evaluates per(S) for column subsets S by a memoised recursion
+// (reference proj/src/permanent.cpp:244-322):
+//     per(S) = sum_{j in S, ascending} a(|S|-1, j) * per(S \ {j})       (:268-279)
+//     per({j1<j2}) = a(0,j1) a(1,j2) + a(0,j2) a(1,j1)                    (:262-266)
+//     per(A) = sum_{j=0..n-1} a(n-1, j) * per(full \ {j}), left to right  (:288-302)
+// The device engine evaluates the same recurrence bottom-up, one layer
+// (subset size k) at a time, every layer stored densely in colex order:
+//     rank(S) = sum_{i=1..k} C(s_i, i),  s_1 < ... < s_k,
+// so a layer is a flat array of C(n,k) entries with no hashing, no memo
+// probes and no pointer chasing. Removing s_i gives the predecessor rank
+//     rank(S \ {s_i}) = P_i + Q_i,  P_i = sum_{l<i} C(s_l, l),  Q_i = sum_{l>i} C(s_l, l-1),
+// which the kernels update incrementally as i ascends (two table lookups per
+// term), visiting the terms in the reference's ascending-j order.
+//
+// Kernels here:
+//   sz_batch_regs_kernel  n <= 6: one thread per matrix, the whole DP in
+//                         registers (compile-time subset masks), inputs staged
+//                         through shared memory with coalesced loads.
+//   sz_batch_smem_kernel  7 <= n <= ~15: one warp per matrix, ping-pong
+//                         layers and the matrix in shared memory.
+//   sz_layer_kernel       one layer of a single large matrix in global memory
+//                         (the per-layer gather-MAC kernel).
+//   sz_top_kernel         the final n-term development.
+#pragma once
+
+#include <cstdint>
+
+#include "ring.cuh"
+
+namespace pl {
+
+struct DevStatus {
+    int32_t* status;       // OR-ed PL_STATUS_BIT_* bits (device)
+};
+
+// Shared-memory binomial table, row-major [s][l], kBinomDim x kBinomDim.
+__device__ __forceinline__ void load_binom_smem(uint32_t* sb) {
+    for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) {
+        const int s = e / kBinomDim, l = e % kBinomDim;
+        uint32_t v = 0;
+        if (l <= s) {
+            uint64_t r = 1;
+            for (int i = 1; i <= l; ++i) r = r * (uint64_t)(s - l + i) / (uint64_t)i;
+            v = (uint32_t)r;
+        }
+        sb[e] = v;
+    }
+}
+
+// Colex unrank of `r` among k-subsets of {0..n-1}: returns the bitmask and
+// qsum = sum_{l=2..k} C(s_l, l-1) (= Q_1, the suffix part of the first
+// predecessor rank).
+__device__ __forceinline__ uint64_t colex_unrank(uint32_t r, int k, int n, const uint32_t* sb, uint32_t& qsum) {
+    uint64_t mask = 0;
+    uint32_t q = 0;
+    int s = n - 1;
+    for (int i = k; i >= 1; --i) {
+        uint32_t c = sb[s * kBinomDim + i];
+        while (c > r) {
+            --s;
+            c = sb[s * kBinomDim + i];
+        }
+        mask |= 1ull << s;
+        r -= c;
+        if (i >= 2) q += sb[s * kBinomDim + i - 1];
+        --s;
+    }
+    qsum = q;
+    return mask;
+}
+
+// One output of layer k >= 3: sum over the k elements of `mask` ascending of
+// row[s] * prev[rank(mask \ {s})].
+template <class R>
+__device__ __forceinline__ typename R::T eval_subset(uint64_t mask, uint32_t qsum, int k,
+                                                     const typename R::T* row,
+                                                     const typename R::T* prev, const uint32_t* sb,
+                                                     bool& ov) {
+    using T = typename R::T;
+    uint32_t P = 0, Q = qsum;
+    int s = __ffsll((long long)mask) - 1;
+    mask &= mask - 1;
+    T acc = R::mul(row[s], prev[P + Q], ov);
+    P += sb[s * kBinomDim + 1];
+    for (int i = 2; i <= k; ++i) {
+        const int s2 = __ffsll((long long)mask) - 1;
+        mask &= mask - 1;
+        Q -= sb[s2 * kBinomDim + i - 1];
+        acc = R::mac(acc, row[s2], prev[P + Q], ov);
+        P += sb[s2 * kBinomDim + i];
+    }
+    return acc;
+}
+
+// Order-2 base case for the subset {j1 < j2}: a(0,j1) a(1,j2) + a(0,j2) a(1,j1).
+template <class R>
+__device__ __forceinline__ typename R::T base_pair(const typename R::T* a, int n, int j1, int j2, bool& ov) {
+    return R::add(R::mul(a[j1], a[n + j2], ov), R::mul(a[j2], a[n + j1], ov), ov);
+}
+
+// ---------------------------------------------------------------- n <= 6
+
+__host__ __device__ constexpr int popc_c(int x) { return x == 0 ? 0 : (x & 1) + popc_c(x >> 1); }
+
+template <class R, int N>
+__device__ __forceinline__ typename R::T perm_in_registers(const typename R::T* a, bool& ov) {
+    using T = typename R::T;
+    if constexpr (N == 1) {
+        return a[0];
+    } else {
+        T memo[1 << N];
+#pragma unroll
+        for (int m = 0; m < (1 << N); ++m) {
+            if (popc_c(m) == 2) {
+                const int j1 = __ffs(m) - 1;
+                const int j2 = 31 - __clz(m);
+                memo[m] = base_pair<R>(a, N, j1, j2, ov);
+            }
+        }
+        if constexpr (N == 2) {
+            return memo[3];
+        } else {
+#pragma unroll
+            for (int k = 3; k < N; ++k) {
+#pragma unroll
+                for (int m = 0; m < (1 << N); ++m) {
+                    if (popc_c(m) == k) {
+                        T acc = R::zero();
+                        bool first = true;
+#pragma unroll
+                        for (int j = 0; j < N; ++j) {
+                            if ((m >> j) & 1) {
+                                const T c = a[(k - 1) * N + j];
+                                const T v = memo[m & ~(1 << j)];
+                                acc = first ? R::mul(c, v, ov) : R::mac(acc, c, v, ov);
+                                first = false;
+                            }
+                        }
+                        memo[m] = acc;
+                    }
+                }
+            }
+            constexpr int full = (1 << N) - 1;
+            T total = R::mul(a[(N - 1) * N], memo[full & ~1], ov);
+#pragma unroll
+            for (int j = 1; j < N; ++j) total = R::mac(total, a[(N - 1) * N + j], memo[full & ~(1 << j)], ov);
+            return total;
+        }
+    }
+}
+
+// Guard for the exact int64 ring: true when prod_i max(1, sum_j |a_ij|) < 2^63,
+// which bounds |per| of every sub-permanent over leading rows and every
+// partial sum of the development (|per(S)| <= prod_{i<|S|} sum_{j in S} |a_ij|).
+__device__ __forceinline__ bool i64_guard_ok(const long long* a, int n, int stride_row = -1) {
+    if (stride_row < 0) stride_row = n;
+    unsigned long long prod = 1;
+    bool ok = true;
+    for (int i = 0; i < n; ++i) {
+        unsigned long long rs = 0;
+        for (int j = 0; j < n; ++j) {
+            const long long v = a[i * stride_row + j];
+            if (v == (long long)0x8000000000000000ULL) ok = false;
+            const unsigned long long m = v < 0 ? (unsigned long long)(-v) : (unsigned long long)v;
+            const unsigned long long t = rs + m;
+            if (t < rs) ok = false;
+            rs = t;
+        }
+        if (rs == 0) rs = 1;
+        if (__umul64hi(prod, rs) != 0) ok = false;
+        prod *= rs;
+        if (prod >= 0x8000000000000000ULL) ok = false;
+    }
+    return ok;
+}
+
+template <class R, int N, int THREADS>
+__global__ void __launch_bounds__(THREADS) sz_batch_regs_kernel(const typename R::T* __restrict__ a,
+                                                                typename R::T* __restrict__ out, int64_t count,
+                                                                int32_t* __restrict__ status) {
+    using T = typename R::T;
+    constexpr int kEnt = N * N;
+    constexpr int kWordsPerEnt = sizeof(T) / 8;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+
+    const int64_t first = (int64_t)blockIdx.x * THREADS;
+    const int64_t left = count - first;
+    const int nvalid = left < THREADS ? (int)left : THREADS;
+    // Coalesced 8-byte staging of this CTA's contiguous run of matrices.
+    {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a + first * kEnt);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(sm);
+        const int words = nvalid * kEnt * kWordsPerEnt;
+        for (int w = threadIdx.x; w < words; w += THREADS) dst[w] = __ldg(src + w);
+    }
+    __syncthreads();
+    if (threadIdx.x >= nvalid) return;
+    const T* local = sm + threadIdx.x * kEnt;
+
+    bool ov = false;
+    T v;
+    if constexpr (R::kChecked) {
+        // int64: the unchecked (fast) instantiation is taken per warp when every
+        // lane's matrix passes the guard; otherwise checked arithmetic.
+        const bool ok = i64_guard_ok(local, N);
+        if (__all_sync(__activemask(), ok)) {
+            v = perm_in_registers<RI64<false>, N>(local, ov);
+        } else {
+            v = perm_in_registers<R, N>(local, ov);
+        }
+    } else {
+        v = perm_in_registers<R, N>(local, ov);
+    }
+    if (ov) {
+        atomicOr(status, 1);
+        v = R::zero();
+    }
+    out[first + threadIdx.x] = v;
+}
+
+// ---------------------------------------------------------------- 7 <= n <= ~15
+
+// One warp per matrix; layers and matrix in shared memory. `maxc` is
+// max_k C(n,k). Warps stride over the batch (persistent CTAs).
+template <class R>
+__global__ void __launch_bounds__(256) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
+                                                            typename R::T* __restrict__ out, int64_t count,
+                                                            int n, int maxc, int32_t* __restrict__ status) {
+    using T = typename R::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* sb = reinterpret_cast<uint32_t*>(smem_raw);
+    const int warps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t binom_bytes = ((kBinomDim * kBinomDim * 4 + 15) / 16) * 16;
+    const size_t per_warp = ((size_t)n * n + 2 * (size_t)maxc) * sizeof(T);
+    T* mat = reinterpret_cast<T*>(smem_raw + binom_bytes + warp * per_warp);
+    T* buf0 = mat + n * n;
+    T* buf1 = buf0 + maxc;
+    load_binom_smem(sb);
+    __syncthreads();
+
+    for (int64_t b = (int64_t)blockIdx.x * warps + warp; b < count; b += (int64_t)gridDim.x * warps) {
+        const T* g = a + b * n * n;
+        for (int e = lane; e < n * n; e += 32) mat[e] = g[e];
+        __syncwarp();
+        bool ov = false;
+        bool use_checked = false;
+        if constexpr (R::kChecked) {
+            bool ok = true;
+            if (lane == 0) ok = i64_guard_ok(reinterpret_cast<const long long*>(mat), n);
+            use_checked = !__shfl_sync(0xffffffffu, ok, 0);
+        }
+        // layer 2
+        const int c2 = n * (n - 1) / 2;
+        for (int r = lane; r < c2; r += 32) {
+            uint32_t q;
+            const uint64_t m = colex_unrank((uint32_t)r, 2, n, sb, q);
+            const int j1 = __ffsll((long long)m) - 1;
+            const int j2 = 63 - __clzll((long long)m);
+            buf0[r] = base_pair<R>(mat, n, j1, j2, ov);
+        }
+        __syncwarp();
+        T* prev = buf0;
+        T* cur = buf1;
+        for (int k = 3; k < n; ++k) {
+            const int ck = (int)sb[n * kBinomDim + k];
+            const T* row = mat + (k - 1) * n;
+            for (int r = lane; r < ck; r += 32) {
+                uint32_t q;
+                const uint64_t m = colex_unrank((uint32_t)r, k, n, sb, q);
+                T v;
+                if constexpr (R::kChecked) {
+                    if (use_checked) {
+                        v = eval_subset<R>(m, q, k, row, prev, sb, ov);
+                    } else {
+                        v = eval_subset<RI64<false>>(m, q, k, row, prev, sb, ov);
+                    }
+                } else {
+                    v = eval_subset<R>(m, q, k, row, prev, sb, ov);
+                }
+                cur[r] = v;
+            }
+            __syncwarp();
+            T* t = prev;
+            prev = cur;
+            cur = t;
+        }
+        if (__any_sync(0xffffffffu, ov)) {
+            if (lane == 0) {
+                atomicOr(status, 1);
+                out[b] = R::zero();
+            }
+        } else if (lane == 0) {
+            const T* last = mat + (n - 1) * n;
+            T total = R::mul(last[0], prev[n - 1], ov);
+            for (int j = 1; j < n; ++j) total = R::mac(total, last[j], prev[n - 1 - j], ov);
+            if (ov) {
+                atomicOr(status, 1);
+                total = R::zero();
+            }
+            out[b] = total;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- layer kernel
+
+// Entries [r0, r1) of layer k (k >= 2) of one matrix. `guard` (int64 only):
+// nonzero selects checked arithmetic.
+template <class R>
+__global__ void __launch_bounds__(256) sz_layer_kernel(const typename R::T* __restrict__ a, int n, int k,
+                                                       const typename R::T* __restrict__ prev,
+                                                       typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1,
+                                                       const int32_t* __restrict__ guard,
+                                                       int32_t* __restrict__ status) {
+    using T = typename R::T;
+    __shared__ uint32_t sb[kBinomDim * kBinomDim];
+    __shared__ T row[kMaxOrder];
+    __shared__ T row0[kMaxOrder];
+    load_binom_smem(sb);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        row[j] = a[(k - 1) * n + j];
+        row0[j] = a[j];
+    }
+    __syncthreads();
+    bool use_checked = false;
+    if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
+    bool ov = false;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += stride) {
+        uint32_t q;
+        const uint64_t m = colex_unrank((uint32_t)r, k, n, sb, q);
+        T v;
+        if (k == 2) {
+            const int j1 = __ffsll((long long)m) - 1;
+            const int j2 = 63 - __clzll((long long)m);
+            v = R::add(R::mul(row0[j1], row[j2], ov), R::mul(row0[j2], row[j1], ov), ov);
+        } else if constexpr (R::kChecked) {
+            v = use_checked ? eval_subset<R>(m, q, k, row, prev, sb, ov)
+                            : eval_subset<RI64<false>>(m, q, k, row, prev, sb, ov);
+        } else {
+            v = eval_subset<R>(m, q, k, row, prev, sb, ov);
+        }
+        cur[r] = v;
+    }
+    if (ov) atomicOr(status, 1);
+}
+
+template <class R>
+__global__ void sz_top_kernel(const typename R::T* __restrict__ a, int n, const typename R::T* __restrict__ last,
+                              typename R::T* __restrict__ out, const int32_t* __restrict__ guard,
+                              int32_t* __restrict__ status) {
+    using T = typename R::T;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    bool ov = false;
+    const T* row = a + (size_t)(n - 1) * n;
+    T total = R::mul(row[0], last[n - 1], ov);
+    for (int j = 1; j < n; ++j) total = R::mac(total, row[j], last[n - 1 - j], ov);
+    if (ov) {
+        atomicOr(status, 1);
+        total = R::zero();
+    }
+    out[0] = total;
+}
+
+__global__ void sz_guard_i64_kernel(const long long* __restrict__ a, int n, int32_t* __restrict__ guard) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) guard[0] = i64_guard_ok(a, n) ? 0 : 1;
+}
+
+// n == 1 and n == 2 single-matrix cases (and any order <= 6 single matrix).
+}  // namespace pl

@@ -1,0 +1,275 @@
+// C++ parity suite for the device-backed permlab host API. It mirrors the
+// reference's own unit tests for the Store-zechin path (reference
+// proj/tests/test_permanent.cpp) case by case, with the same goldens, so a
+// maintainer can read the two side by side. Device results are additionally
+// compared with the CPU oracle restatement (oracle/liboracle.so, loaded with
+// dlopen so the product library never links it).
+//
+// Usage: test_permanent_device [--host-only]
+//   --host-only runs only the checks that need no GPU (closed forms, limits,
+//   error mapping when no device is present).
+#include <dlfcn.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "permlab/permanent.hpp"
+
+using namespace permlab;
+
+namespace {
+
+int g_checks = 0, g_failures = 0;
+
+#define CHECK(cond)                                                                  \
+    do {                                                                             \
+        ++g_checks;                                                                  \
+        if (!(cond)) {                                                               \
+            ++g_failures;                                                            \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);     \
+        }                                                                            \
+    } while (0)
+
+#define CHECK_THROWS_AS(expr, Exc)                  \
+    do {                                            \
+        bool _thrown = false;                       \
+        try {                                       \
+            (void)(expr);                           \
+        } catch (const Exc&) {                      \
+            _thrown = true;                         \
+        } catch (...) {                             \
+        }                                           \
+        CHECK(_thrown);                             \
+    } while (0)
+
+Matrix<Int> int_matrix(int n, const std::vector<long long>& v) { return {n, std::vector<Int>(v.begin(), v.end())}; }
+
+Int value_of(const PermanentResult& r) { return std::get<Int>(r.value); }
+
+// Reference fixture (reference tests/test_permanent.cpp:37-40).
+const Matrix<Int> kDev4 = int_matrix(4, {7, 0, 1, 2, 5, 3, 4, 5, 3, 5, 6, 7, 1, 7, 8, 9});
+
+Matrix<Int> random_int_matrix(int n, std::mt19937_64& g, int lo = -9, int hi = 9) {
+    std::vector<Int> e(static_cast<std::size_t>(n) * n);
+    for (auto& x : e) x = lo + static_cast<Int>(g() % static_cast<std::uint64_t>(hi - lo + 1));
+    return {n, std::move(e)};
+}
+
+Matrix<Cplx> random_cplx_matrix(int n, std::mt19937_64& g) {
+    std::vector<Cplx> e(static_cast<std::size_t>(n) * n);
+    auto u = [&] { return 2.0 * static_cast<double>(g() >> 11) * 0x1.0p-53 - 1.0; };
+    for (auto& x : e) {
+        const double re = u();
+        x = Cplx(re, u());
+    }
+    return {n, std::move(e)};
+}
+
+std::vector<int> random_permutation(int n, std::mt19937_64& g) {
+    std::vector<int> p(n);
+    for (int i = 0; i < n; ++i) p[i] = i;
+    for (int i = n - 1; i > 0; --i) std::swap(p[i], p[g() % static_cast<std::uint64_t>(i + 1)]);
+    return p;
+}
+
+// ---- oracle (CPU restatement), test-only
+using orc_i64_fn = int (*)(int, const std::int64_t*, std::int64_t*, std::int64_t*, int);
+using orc_c128_fn = int (*)(int, const double*, double*, int);
+orc_i64_fn orc_i64 = nullptr;
+orc_c128_fn orc_c128 = nullptr;
+
+bool load_oracle(const char* self) {
+    std::string dir(self);
+    dir = dir.substr(0, dir.find_last_of('/') + 1);
+    void* h = dlopen((dir + "../../oracle/liboracle.so").c_str(), RTLD_NOW);
+    if (!h) return false;
+    orc_i64 = reinterpret_cast<orc_i64_fn>(dlsym(h, "orc_sz_i64"));
+    orc_c128 = reinterpret_cast<orc_c128_fn>(dlsym(h, "orc_sz_c128"));
+    return orc_i64 && orc_c128;
+}
+
+Int oracle_int(const Matrix<Int>& m) {
+    std::int64_t lo = 0, hi = 0;
+    CHECK(orc_i64(m.order(), m.entries().data(), &lo, &hi, 1) == 0);
+    CHECK(hi == (lo < 0 ? -1 : 0));
+    return lo;
+}
+
+Cplx oracle_cplx(const Matrix<Cplx>& m) {
+    double out[2];
+    CHECK(orc_c128(m.order(), reinterpret_cast<const double*>(m.entries().data()), out, 1) == 0);
+    return {out[0], out[1]};
+}
+
+// ---------------------------------------------------------------- host-only
+
+void host_closed_forms() {
+    // reference tests/test_permanent.cpp:131-147 (counts) and :149-168 (tables)
+    for (int n = 2; n <= 20; ++n) {
+        const std::uint64_t pow2 = std::uint64_t{1} << n;
+        CHECK((store_zechin_counts(n) == OpCount{static_cast<std::uint64_t>(n) * (pow2 / 2) - n,
+                                                 static_cast<std::uint64_t>(n) * (pow2 / 2) - pow2 + 1}));
+    }
+    CHECK((store_zechin_counts(1) == OpCount{0, 0}));
+    CHECK((store_zechin_counts(2) == OpCount{2, 1}));
+    auto report_for = [](int n) { return store_zechin_attributed(SquareMatrix(Matrix<Int>::filled(n, 1))); };
+    const AttributionReport r3 = report_for(3);
+    CHECK((r3.per_term == std::vector<OpCount>{{3, 1}, {3, 1}, {3, 1}}));
+    CHECK(r3.final_combination_adds == 2);
+    CHECK((r3.totals == OpCount{9, 5}));
+    const AttributionReport r4 = report_for(4);
+    CHECK((r4.per_term == std::vector<OpCount>{{10, 5}, {8, 4}, {6, 3}, {4, 2}}));
+    CHECK((r4.totals == OpCount{28, 17}));
+    const AttributionReport r5 = report_for(5);
+    CHECK((r5.per_term == std::vector<OpCount>{{29, 17}, {20, 12}, {13, 8}, {8, 5}, {5, 3}}));
+    CHECK(r5.final_combination_adds == 4);
+    CHECK((r5.totals == OpCount{75, 49}));
+    for (int n = 3; n <= 24; ++n) {
+        const AttributionReport r = report_for(n);
+        CHECK(r.totals == store_zechin_counts(n));
+    }
+    CHECK_THROWS_AS(store_zechin_attributed(SquareMatrix(Matrix<Int>::identity(2))), DomainError);
+    for (Algorithm a : {Algorithm::Naive, Algorithm::Ryser, Algorithm::StoreZechin}) {
+        CHECK(algorithm_from_name(algorithm_name(a)) == a);
+    }
+    CHECK_THROWS_AS(algorithm_from_name("glynn"), DomainError);
+    // limits (reference tests/test_permanent.cpp:280-294): rejected before any device work
+    Limits limits;
+    limits.subset_order_limit = 4;
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(5, 1)), limits), DomainError);
+    limits = Limits{};
+    limits.memo_budget_bytes = 16;
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(5, 1)), limits), DomainError);
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(35, 1))), DomainError);
+    setenv("PERMLAB_LIMITS", "subset_order_limit=24,memo_budget_bytes=1024", 1);
+    const Limits env = Limits::from_env();
+    CHECK(env.subset_order_limit == 24);
+    CHECK(env.memo_budget_bytes == 1024);
+    setenv("PERMLAB_LIMITS", "bogus=1", 1);
+    CHECK_THROWS_AS(Limits::from_env(), DomainError);
+    unsetenv("PERMLAB_LIMITS");
+}
+
+// ---------------------------------------------------------------- device
+
+void device_goldens() {
+    // reference tests/test_permanent.cpp:48-92
+    CHECK(value_of(store_zechin_permanent(SquareMatrix(int_matrix(2, {1, 2, 3, 4})))) == 10);
+    CHECK(value_of(store_zechin_permanent(SquareMatrix(int_matrix(3, {1, 2, 3, 4, 5, 6, 7, 8, 9})))) == 450);
+    const auto dev = store_zechin_permanent(SquareMatrix(kDev4));
+    CHECK(value_of(dev) == 9722);
+    CHECK((dev.counts == OpCount{28, 17}));
+    CHECK(dev.algorithm == Algorithm::StoreZechin);
+    const SquareMatrix a5(int_matrix(5, {1, 1, 0, 2, 3, 2, 0, 1, 1, 4, 3, 1, 2, 0, 1, 0, 2, 1, 3, 2, 1, 0, 4, 1, 2}));
+    const auto r5 = store_zechin_permanent(a5);
+    CHECK(value_of(r5) == 988);
+    CHECK((r5.counts == OpCount{75, 49}));
+    const auto one = store_zechin_permanent(SquareMatrix(int_matrix(1, {42})));
+    CHECK(value_of(one) == 42);
+    CHECK((one.counts == OpCount{0, 0}));
+    const auto two = store_zechin_permanent(SquareMatrix(int_matrix(2, {2, 3, 5, 7})));
+    CHECK(value_of(two) == 29);
+    CHECK((two.counts == OpCount{2, 1}));
+    CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(3, 1)))) == 6);
+    CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::identity(7)))) == 1);
+    // first-column development of the order-4 example (reference :246-255)
+    const std::vector<Int> minors{1116, 258, 166, 122};
+    Int sum = 0;
+    for (int i = 0; i < 4; ++i) {
+        const auto minor = kDev4.remove_rows_cols({i}, {0});
+        CHECK(value_of(store_zechin_permanent(SquareMatrix(minor))) == minors[i]);
+        sum += kDev4(i, 0) * minors[i];
+    }
+    CHECK(sum == 9722);
+}
+
+void device_oracle_agreement() {
+    // reference tests/test_permanent.cpp:94-106 (n = 1..6, 20 each), widened to n = 1..16
+    std::mt19937_64 g(41);
+    for (int n = 1; n <= 16; ++n) {
+        for (int rep = 0; rep < (n <= 8 ? 20 : 3); ++rep) {
+            const auto m = random_int_matrix(n, g, n <= 10 ? -9 : -2, n <= 10 ? 9 : 2);
+            CHECK(value_of(store_zechin_permanent(SquareMatrix(m))) == oracle_int(m));
+        }
+    }
+    // complex: bitwise equal to the oracle (which is bitwise the reference)
+    std::mt19937_64 gc(47);
+    for (int n = 1; n <= 14; ++n) {
+        const auto m = random_cplx_matrix(n, gc);
+        const Cplx d = std::get<Cplx>(store_zechin_permanent(SquareMatrix(m)).value);
+        const Cplx o = oracle_cplx(m);
+        CHECK(d == o);
+        CHECK(approx_equal(d, o));
+    }
+}
+
+void device_identities() {
+    // reference tests/test_permanent.cpp:196-244
+    std::mt19937_64 g(67);
+    for (int rep = 0; rep < 25; ++rep) {
+        const int n = 2 + static_cast<int>(g() % 4);
+        const auto m = random_int_matrix(n, g);
+        const Int expected = value_of(store_zechin_permanent(SquareMatrix(m)));
+        const auto p = m.permute(random_permutation(n, g), random_permutation(n, g));
+        CHECK(value_of(store_zechin_permanent(SquareMatrix(p))) == expected);
+        CHECK(value_of(store_zechin_permanent(SquareMatrix(m.transpose()))) == expected);
+        const Int s = Int(rep) - 12;
+        CHECK(value_of(store_zechin_permanent(SquareMatrix(m.scale_row(rep % n, s)))) == s * expected);
+        if (n > 2) {
+            Int sum = 0;
+            for (int j = 0; j < n; ++j) {
+                sum += m(0, j) * value_of(store_zechin_permanent(SquareMatrix(m.remove_rows_cols({0}, {j}))));
+            }
+            CHECK(sum == expected);
+        }
+    }
+}
+
+void device_run_and_batch() {
+    // reference tests/test_permanent.cpp:184-194
+    std::mt19937_64 g(61);
+    for (int n : {3, 4, 6, 8}) {
+        const StoreZechinRun run = store_zechin_run(SquareMatrix(random_int_matrix(n, g)));
+        const std::uint64_t expected = (std::uint64_t{1} << n) - 2 - static_cast<std::uint64_t>(n);
+        CHECK(run.cache_misses == expected);
+        CHECK(run.distinct_subsets == expected);
+    }
+    // vector batch == singles
+    std::vector<SquareMatrix> batch;
+    for (int b = 0; b < 40; ++b) batch.emplace_back(random_int_matrix(5, g));
+    const auto res = store_zechin_permanent_batch(batch);
+    CHECK(res.size() == batch.size());
+    for (std::size_t b = 0; b < batch.size(); ++b) {
+        CHECK(value_of(res[b]) == value_of(store_zechin_permanent(batch[b])));
+    }
+    CHECK_THROWS_AS(store_zechin_permanent_batch(std::vector<SquareMatrix>{SquareMatrix(Matrix<Int>::filled(3, 1)),
+                                                                           SquareMatrix(Matrix<Int>::filled(4, 1))}),
+                    DomainError);
+    // int64 guard: an exact value beyond int64 is a DomainError, never a wrap
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(22, 1000))), DomainError);
+    // the guard is conservative but the checked path still computes what fits
+    CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(20, 1)))) == 2432902008176640000LL);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const bool host_only = argc > 1 && std::string(argv[1]) == "--host-only";
+    host_closed_forms();
+    if (!host_only) {
+        if (!load_oracle(argv[0])) {
+            std::fprintf(stderr, "cannot load oracle/liboracle.so\n");
+            return 2;
+        }
+        device_goldens();
+        device_oracle_agreement();
+        device_identities();
+        device_run_and_batch();
+    }
+    std::printf("%d checks, %d failures\n", g_checks, g_failures);
+    return g_failures == 0 ? 0 : 1;
+}

@@ -1,0 +1,235 @@
+"""Device parity: the CUDA path (through the C ABI) against the oracle on the
+same seeded inputs, at the BASELINE.json config sizes and at edge cases.
+
+Bars (BASELINE.json north_star): int64 bit-exact; float64 / complex128 within
+relative 1e-9 — and, in the default (non-FMA) mode, bitwise equal to the
+oracle, which is bitwise the reference engine (tests/test_oracle.py)."""
+import math
+import struct
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1802_02779_b200 as pl
+from oracle import oracle as O
+from paper_1802_02779_b200 import configs
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+REL_TOL = 1e-9  # north_star: relative error <= 1e-9 in fp64 / complex128 (no absolute floor)
+
+
+def hexf(x):
+    return struct.pack(">d", x).hex()
+
+
+def rel_err(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_device():
+    if pl.device_count() == 0:
+        pytest.fail("no CUDA device: GPU tests must run on the B200 box")
+
+
+# ---------------------------------------------------------------- configs
+
+def test_c1_bit_exact(goldens):
+    a = configs.c1()
+    out = pl.store_zechin_permanent_batch(a)
+    assert out.dtype == np.int64
+    assert configs.sha256(out) == goldens["c1"]["output_sha256"]
+    assert np.array_equal(out, O.sz_batch(a))
+
+
+@pytest.mark.parametrize("fma", [False, True])
+def test_c2_complex(goldens, fma):
+    a = configs.c2()
+    out = pl.store_zechin_permanent_batch(a, fma=fma)
+    want = O.sz_batch(a)
+    assert rel_err(out, want) <= REL_TOL
+    if not fma:
+        assert configs.sha256(out) == goldens["c2"]["output_sha256"]
+
+
+def test_c3_bit_exact(goldens):
+    a = configs.c3()
+    out = pl.store_zechin_permanent_batch(a)
+    assert configs.sha256(out) == goldens["c3"]["output_sha256"]
+
+
+@pytest.mark.parametrize("fma", [False, True])
+def test_c4_float64(goldens, fma):
+    a = configs.c4()
+    v = pl.store_zechin_permanent(a, fma=fma).value
+    assert rel_err(v, goldens["c4"]["value"]) <= REL_TOL
+    if not fma:
+        assert hexf(v) == goldens["c4"]["value_hex"] == goldens["c4"]["reference_value_hex"]
+
+
+@pytest.mark.parametrize("fma", [False, True])
+def test_c5_complex128(goldens, fma):
+    a = configs.c5()
+    assert configs.sha256(a) == goldens["c5"]["input_sha256"]
+    v = pl.store_zechin_permanent(a, fma=fma).value
+    want = complex(*goldens["c5"]["value"])
+    assert abs(v - want) <= REL_TOL * abs(want)  # pure relative: |per| ~ 3e-32
+    if not fma:
+        assert [hexf(v.real), hexf(v.imag)] == goldens["c5"]["value_hex"]
+
+
+# ---------------------------------------------------------------- orders / rings
+
+@pytest.mark.parametrize("n", list(range(1, 21)))
+def test_int_orders_vs_oracle(n):
+    count = 64 if n <= 12 else (4 if n <= 16 else 1)
+    lo, hi = (-9, 9) if n <= 10 else (-1, 2)
+    a = configs.int_matrices(n, count, seed=1000 + n, lo=lo, hi=hi)
+    out = pl.store_zechin_permanent_batch(a)
+    assert np.array_equal(out, O.sz_batch(a))
+
+
+@pytest.mark.parametrize("n", list(range(1, 21)) + [23, 24])
+def test_complex_orders_bitwise(n):
+    count = 33 if n <= 12 else (3 if n <= 16 else 1)
+    a = configs.complex_uniform((count, n, n), seed=2000 + n)
+    out = pl.store_zechin_permanent_batch(a)
+    want = O.sz_batch(a)
+    assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
+    out_f = pl.store_zechin_permanent_batch(a, fma=True)
+    assert rel_err(out_f, want) <= REL_TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 7, 9, 13, 15, 16, 17, 22])
+def test_float_orders_bitwise(n):
+    count = 17 if n <= 13 else 2
+    a = configs.uniform((count, n, n), seed=3000 + n)
+    out = pl.store_zechin_permanent_batch(a)
+    assert np.array_equal(out.view(np.uint64), O.sz_batch(a).view(np.uint64))
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_empty_and_ragged_batches():
+    for dt in (np.int64, np.float64, np.complex128):
+        assert pl.store_zechin_permanent_batch(np.zeros((0, 5, 5), dtype=dt)).shape == (0,)
+    for count in (1, 31, 127, 129, 1000):  # CTA tails of the batched kernels
+        for n in (5, 8):
+            a = configs.int_matrices(n, count, seed=count + n)
+            assert np.array_equal(pl.store_zechin_permanent_batch(a), O.sz_batch(a))
+
+
+def test_reference_goldens_on_device():
+    dev4 = np.array([7, 0, 1, 2, 5, 3, 4, 5, 3, 5, 6, 7, 1, 7, 8, 9]).reshape(4, 4)
+    assert pl.store_zechin_permanent(dev4).value == 9722
+    assert pl.store_zechin_permanent(np.array([[42]])).value == 42
+    r = pl.store_zechin_permanent(np.array([[2, 3], [5, 7]]))
+    assert (r.value, r.counts) == (29, pl.OpCount(2, 1))
+    run = pl.store_zechin_run(np.ones((8, 8), dtype=np.int64))
+    assert run.result.value == math.factorial(8)
+    assert run.cache_misses == run.distinct_subsets == 2 ** 8 - 8 - 2
+
+
+def test_int64_overflow_guard():
+    # every intermediate fits: the checked path computes it exactly (20! < 2^63)
+    assert pl.store_zechin_permanent(np.ones((20, 20), dtype=np.int64)).value == math.factorial(20)
+    # 21! > 2^63 (layer path), 5! 10^20 (register kernel), 9! 10^27 (shared-memory kernel): never wrap
+    with pytest.raises(pl.DomainError, match="overflow"):
+        pl.store_zechin_permanent(np.ones((21, 21), dtype=np.int64))
+    with pytest.raises(pl.DomainError, match="overflow"):
+        pl.store_zechin_permanent_batch(np.full((3, 5, 5), 10 ** 4, dtype=np.int64))
+    with pytest.raises(pl.DomainError, match="overflow"):
+        pl.store_zechin_permanent_batch(np.full((3, 9, 9), 10 ** 3, dtype=np.int64))
+    # INT64_MIN entry can never be exact-negated: guard -> checked path
+    a = np.zeros((3, 3), dtype=np.int64)
+    a[0, 0] = np.iinfo(np.int64).min
+    a[1, 1] = a[2, 2] = 1
+    assert pl.store_zechin_permanent(a).value == int(np.iinfo(np.int64).min)
+
+
+def test_zero_rows_and_signed_zero():
+    a = configs.uniform((7, 7), seed=9)
+    a[3] = 0.0
+    assert pl.store_zechin_permanent(a).value == O.sz_f64(a)
+    z = -np.zeros((6, 6))
+    assert hexf(pl.store_zechin_permanent(z).value) == hexf(O.sz_f64(z))
+
+
+# ---------------------------------------------------------------- size-independent properties at full size
+
+def test_c4_permutation_and_transpose_invariance():
+    a = configs.c4()
+    base = pl.store_zechin_permanent(a).value
+    rng = np.random.default_rng(4)
+    p = a[rng.permutation(26)][:, rng.permutation(26)]
+    assert rel_err(pl.store_zechin_permanent(p).value, base) <= REL_TOL
+    assert rel_err(pl.store_zechin_permanent(a.T.copy()).value, base) <= REL_TOL
+
+
+def test_c5_row_linearity():
+    a = configs.c5()
+    x = configs.complex_uniform((32,), seed=77) * 1e-2
+    b, c = a.copy(), a.copy()
+    b[31] = x
+    c[31] = a[31] - x
+    pa, pb, pc = (pl.store_zechin_permanent(m, fma=True).value for m in (a, b, c))
+    assert abs(pb + pc - pa) <= 1e-9 * max(abs(pa), abs(pb), abs(pc))
+
+
+# ---------------------------------------------------------------- device pointers / layer primitives
+
+def test_torch_device_batch_and_async_status():
+    import torch
+
+    a = configs.c3(2000)
+    want = O.sz_batch(a)
+    ad = torch.from_numpy(a).cuda()
+    out = pl.store_zechin_permanent_batch(ad)
+    assert np.array_equal(out.cpu().numpy(), want)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out2 = pl.store_zechin_permanent_batch(ad, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0 and np.array_equal(out2.cpu().numpy(), want)
+    bad = torch.full((4, 9, 9), 10 ** 17, dtype=torch.int64, device="cuda")
+    pl.store_zechin_permanent_batch(bad, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) & 1
+    pin = torch.from_numpy(configs.c2(500)).pin_memory()
+    out3 = pl.store_zechin_permanent_batch(pin)
+    assert np.array_equal(out3.numpy().view(np.uint64), O.sz_batch(pin.numpy()).view(np.uint64))
+
+
+def test_layer_primitive_ranges_match_oracle():
+    import torch
+
+    from paper_1802_02779_b200.sharded import device_hooks, layer_slices, sharded_layer_dp
+
+    n = 14
+    a_np = configs.uniform((n, n), seed=123)
+    a = torch.from_numpy(a_np).cuda()
+    layer_fn, top_fn = device_hooks(a)
+    prev = torch.zeros(4000, dtype=a.dtype, device="cuda")
+    cur = torch.zeros_like(prev)
+    for k in range(2, n):
+        full = torch.from_numpy(O.sz_layer_f64(a_np, k)).cuda()
+        if k > 2:
+            src = torch.from_numpy(O.sz_layer_f64(a_np, k - 1)).cuda()
+            prev[: src.numel()] = src
+        for world in (1, 3):
+            _, sl = layer_slices(n, k, world)
+            for r0, r1 in sl:  # every rank's slice, one at a time
+                cur.zero_()
+                layer_fn(k, prev, cur, r0, r1)
+                assert torch.equal(cur[r0:r1], full[r0:r1])
+    v = sharded_layer_dp(a, 0, 1, layer_fn, top_fn)
+    assert hexf(v) == hexf(O.sz_f64(a_np))
+
+
+def test_cpp_device_suite():
+    exe = ROOT / "tests" / "cpp" / "test_permanent_device"
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr

@@ -1,0 +1,135 @@
+"""Multi-rank layer sharding (paper_1802_02779_b200/sharded.py) on CPU.
+
+The schedule that runs over NCCL on GPUs (slice every layer into equal padded
+colex-rank ranges, compute the own slice, all-gather in place) is executed
+here on world_size 2 and 3 gloo process groups, with the CPU oracle's
+single-layer step standing in for the device layer kernel, and must reproduce
+the unsharded oracle bit for bit. A virtual-rank test covers p = 2, 4, 8 in
+one process (memcpy as the all-gather)."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_1802_02779_b200 import configs
+from paper_1802_02779_b200.sharded import layer_slices, max_padded_layer, sharded_layer_dp
+
+_dp = C.POINTER(C.c_double)
+
+
+def _bind():
+    L = O.lib()
+    for name in ("orc_sz_layer_step_f64", "orc_sz_layer_step_c128"):
+        f = getattr(L, name)
+        f.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, C.c_uint64, C.c_uint64]
+        f.restype = C.c_int
+    for name in ("orc_sz_top_f64", "orc_sz_top_c128"):
+        f = getattr(L, name)
+        f.argtypes = [C.c_int, _dp, _dp, _dp]
+        f.restype = C.c_int
+    return L
+
+
+def _dptr(t: torch.Tensor):
+    return C.cast(C.c_void_p(t.data_ptr()), _dp)
+
+
+def cpu_hooks(a: torch.Tensor):
+    L = _bind()
+    n = a.shape[0]
+    cplx = a.is_complex()
+    step = L.orc_sz_layer_step_c128 if cplx else L.orc_sz_layer_step_f64
+    top = L.orc_sz_top_c128 if cplx else L.orc_sz_top_f64
+
+    def layer_fn(k, prev, cur, r0, r1):
+        assert step(n, _dptr(a), k, _dptr(prev), _dptr(cur), r0, r1) == 0
+
+    def top_fn(a_, last):
+        out = torch.zeros(2, dtype=torch.float64)
+        assert top(n, _dptr(a_), _dptr(last), _dptr(out)) == 0
+        return complex(out[0], out[1]) if cplx else float(out[0])
+
+    return layer_fn, top_fn
+
+
+def test_layer_slices_cover_exactly():
+    for n in (5, 9, 26, 32):
+        for world in (1, 2, 3, 4, 8):
+            for k in range(2, n):
+                per, sl = layer_slices(n, k, world)
+                covered = [r for r0, r1 in sl for r in range(r0, r1)] if n <= 9 else None
+                if covered is not None:
+                    assert covered == list(range(len(covered)))
+                assert sl[0][0] == 0 and sl[-1][1] == __import__("math").comb(n, k)
+                assert all(sl[g][1] == sl[g + 1][0] for g in range(world - 1))
+                assert per * world >= sl[-1][1]
+            assert max_padded_layer(n, world) >= max(__import__("math").comb(n, k) for k in range(2, n))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_virtual_ranks_bitwise(world, cplx):
+    n = 11
+    a_np = configs.complex_uniform((n, n), seed=7) if cplx else configs.uniform((n, n), seed=7)
+    a = torch.from_numpy(a_np)
+    layer_fn, top_fn = cpu_hooks(a)
+    size = max_padded_layer(n, world)
+    replicas = [[torch.zeros(size, dtype=a.dtype) for _ in range(2)] for _ in range(world)]
+    for k in range(2, n):
+        per, sl = layer_slices(n, k, world)
+        for g in range(world):
+            prev, cur = replicas[g]
+            layer_fn(k, prev, cur, *sl[g])
+        for g in range(world):  # all-gather by memcpy
+            for h in range(world):
+                replicas[g][1][h * per:(h + 1) * per] = replicas[h][1][h * per:(h + 1) * per]
+        for g in range(world):
+            replicas[g].reverse()
+    values = {top_fn(a, replicas[g][0]) for g in range(world)}
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    assert values == {want}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, cplx, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a_np = configs.complex_uniform((n, n), seed=31) if cplx else configs.uniform((n, n), seed=31)
+        a = torch.from_numpy(a_np)
+        layer_fn, top_fn = cpu_hooks(a)
+        v = sharded_layer_dp(a, rank, world, layer_fn, top_fn)
+        q.put((rank, v))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gloo_sharded_dp_bitwise(world, cplx):
+    n = 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, cplx, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a_np = configs.complex_uniform((n, n), seed=31) if cplx else configs.uniform((n, n), seed=31)
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    assert set(results.values()) == {want}
