@@ -252,16 +252,16 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
     for _ in range(warmup):
         step()
     barrier()
-    times = []
+    evs = []
     for _ in range(steps):
-        flush_buf.add_(1)  # evict the (< L2) inputs between timed steps
+        flush_buf.add_(1)  # evict the (< L2) inputs between timed steps (outside the event pair)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step()
+        step()  # asynchronous: the host runs ahead, the device never waits on it
         e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
+        evs.append((e0, e1))
     barrier()
+    times = [e0.elapsed_time(e1) for e0, e1 in evs]
     if int(status.item()) != 0:
         raise RuntimeError(f"{name}: device status {int(status.item())}")
     t_local = sum(times) / 1000.0

@@ -118,7 +118,9 @@ uint64_t pl_colex_unrank(int32_t k, uint64_t rank);
 
 /* Compute entries [rank_begin, rank_end) of layer k into cur_dev[rank] from
  * layer k-1 in prev_dev (ignored for k = 2). All pointers are device
- * pointers; `a_dev` is the n*n matrix. Asynchronous on `stream`. For PL_I64
+ * pointers; `a_dev` is the n*n matrix; prev_dev must be 16-byte aligned and
+ * readable for 16 bytes past its last entry (the kernel stages 16-byte
+ * aligned spans). Asynchronous on `stream`. For PL_I64
  * the caller must have run pl_sz_guard_i64 on the same matrix first (its
  * device flag selects the checked path) and passes that flag in guard_dev. */
 pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,

@@ -14,8 +14,12 @@
 #include <mutex>
 #include <string>
 
+#include <map>
+#include <vector>
+
 #include "../../include/permlab_b200.h"
 #include "sz_kernels.cuh"
+#include "sz_ws.cuh"
 
 namespace {
 
@@ -171,19 +175,90 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
     return PL_OK;
 }
 
+// Low-window width D of the tiled layer kernel: as wide as one tile source
+// (C(D, D/2) entries) fits in shared memory, but leaving >= 10 high columns so
+// a layer has enough tiles (>= 2^10 high masks) to keep every SM busy.
+int tile_window(size_t elem, int n) {
+    return std::max(1, std::min(pl::ws_window((int)elem), n - 10));
+}
+
+struct Qtab {
+    uint32_t* qtab = nullptr;
+    uint32_t* offs = nullptr;
+};
+
+// qtab[offs[m] + q] for window D on the current device, built once (host
+// enumeration of the 2^D low masks, copied to device memory).
+pl_status get_qtab(int D, Qtab* out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, Qtab> cache;
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, D});
+    if (it != cache.end()) {
+        *out = it->second;
+        return PL_OK;
+    }
+    std::vector<uint32_t> offs(D + 2, 0);
+    for (int m = 0; m <= D; ++m) offs[m + 1] = offs[m] + (uint32_t)pl::binom_u64(D, m);
+    std::vector<uint32_t> tab(1u << D);
+    for (uint32_t mask = 0; mask < (1u << D); ++mask) {
+        uint32_t r = 0, r1 = 0;
+        int i = 1;
+        for (uint32_t mm = mask; mm; mm &= mm - 1, ++i) r += (uint32_t)pl::binom_u64(__builtin_ctz(mm), i);
+        i = 1;
+        for (uint32_t mm = mask & (mask - 1); mm; mm &= mm - 1, ++i) r1 += (uint32_t)pl::binom_u64(__builtin_ctz(mm), i);
+        tab[offs[__builtin_popcount(mask)] + r] = mask | (r1 << pl::kQtabShift);
+    }
+    Qtab q;
+    PL_CUDA(cudaMalloc(&q.qtab, tab.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMalloc(&q.offs, offs.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMemcpy(q.qtab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    PL_CUDA(cudaMemcpy(q.offs, offs.data(), offs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    cache[{dev, D}] = q;
+    *out = q;
+    return PL_OK;
+}
+
+template <class R>
+struct Unchecked {
+    using type = R;
+};
+template <>
+struct Unchecked<pl::RI64<true>> {
+    using type = pl::RI64<false>;
+};
+
 template <class R>
 pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur, uint64_t r0, uint64_t r1,
                        const int32_t* guard, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
     if (r1 <= r0) return PL_OK;
-    const uint64_t cnt = r1 - r0;
-    const int threads = 256;
-    const uint64_t want = (cnt + threads - 1) / threads;
-    const uint64_t cap = (uint64_t)num_sms() * 8;
-    const unsigned blocks = (unsigned)std::min<uint64_t>(want, cap);
-    pl::sz_layer_kernel<R><<<blocks, threads, 0, st>>>(static_cast<const T*>(a), n, k, static_cast<const T*>(prev),
-                                                       static_cast<T*>(cur), r0, r1, guard, status);
+    if (k == 2) {
+        const unsigned blocks = (unsigned)std::min<uint64_t>((r1 - r0 + 255) / 256, 1024);
+        pl::sz_base_layer_kernel<R><<<blocks, 256, 0, st>>>(static_cast<const T*>(a), n, static_cast<T*>(cur), r0, r1,
+                                                            status);
+        PL_CUDA(cudaGetLastError());
+        return PL_OK;
+    }
+    const int D = tile_window(sizeof(T), n);
+    Qtab q;
+    pl_status s = get_qtab(D, &q);
+    if (s != PL_OK) return s;
+    const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
+    const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
+    unsigned int* counter = nullptr;
+    PL_CUDA(cudaMallocAsync((void**)&counter, sizeof(unsigned int), st));
+    PL_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
+    const size_t smem = pl::WsSmem<T>::bytes(D);
+    auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
+    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<num_sms(), pl::kWsThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
+                                                  static_cast<T*>(cur), r0, r1, F0, F1, counter, q.qtab, q.offs,
+                                                  guard, status);
     PL_CUDA(cudaGetLastError());
+    PL_CUDA(cudaFreeAsync(counter, st));
     return PL_OK;
 }
 
@@ -229,7 +304,10 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     const uint64_t ml = max_layer(n);
     void* bufs = nullptr;
     int32_t* guards = nullptr;
-    PL_CUDA(cudaMallocAsync(&bufs, 2 * ml * es, st));
+    // Layer buffers carry 64 bytes of slack: 8-byte rings stage 16-byte aligned
+    // spans that may read one element past a layer's last entry.
+    const size_t slack = 64;
+    PL_CUDA(cudaMallocAsync(&bufs, 2 * (ml * es + slack), st));
     PL_CUDA(cudaMallocAsync((void**)&guards, sizeof(int32_t), st));
     PL_CUDA(cudaMemsetAsync(guards, 0, sizeof(int32_t), st));
     pl_status s = PL_OK;
@@ -240,7 +318,8 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
             pl::sz_guard_i64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(ab), n, guards);
         }
         s = with_ring(dt, fma, [&](auto r) {
-            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + ml * es, guards, status_dev, st);
+            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + ml * es + slack, guards,
+                                           status_dev, st);
         });
     }
     cudaFreeAsync(bufs, st);

@@ -20,8 +20,8 @@
 //                         through shared memory with coalesced loads.
 //   sz_batch_smem_kernel  7 <= n <= ~15: one warp per matrix, ping-pong
 //                         layers and the matrix in shared memory.
-//   sz_layer_kernel       one layer of a single large matrix in global memory
-//                         (the per-layer gather-MAC kernel).
+//   sz_base_layer_kernel  layer 2 (order-2 base case) of a single large matrix;
+//                         layers >= 3 run in the warp-specialised kernel (sz_ws.cuh).
 //   sz_top_kernel         the final n-term development.
 #pragma once
 
@@ -307,45 +307,19 @@ __global__ void __launch_bounds__(256) sz_batch_smem_kernel(const typename R::T*
     }
 }
 
-// ---------------------------------------------------------------- layer kernel
+// ---------------------------------------------------------------- layer 2
 
-// Entries [r0, r1) of layer k (k >= 2) of one matrix. `guard` (int64 only):
-// nonzero selects checked arithmetic.
+// Layer 2 (order-2 base case) for ranks [r0, r1): rank({j1 < j2}) = j1 + C(j2, 2).
 template <class R>
-__global__ void __launch_bounds__(256) sz_layer_kernel(const typename R::T* __restrict__ a, int n, int k,
-                                                       const typename R::T* __restrict__ prev,
-                                                       typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1,
-                                                       const int32_t* __restrict__ guard,
-                                                       int32_t* __restrict__ status) {
-    using T = typename R::T;
-    __shared__ uint32_t sb[kBinomDim * kBinomDim];
-    __shared__ T row[kMaxOrder];
-    __shared__ T row0[kMaxOrder];
-    load_binom_smem(sb);
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        row[j] = a[(k - 1) * n + j];
-        row0[j] = a[j];
-    }
-    __syncthreads();
-    bool use_checked = false;
-    if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
+__global__ void sz_base_layer_kernel(const typename R::T* __restrict__ a, int n, typename R::T* __restrict__ cur,
+                                     uint64_t r0, uint64_t r1, int32_t* __restrict__ status) {
     bool ov = false;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += stride) {
-        uint32_t q;
-        const uint64_t m = colex_unrank((uint32_t)r, k, n, sb, q);
-        T v;
-        if (k == 2) {
-            const int j1 = __ffsll((long long)m) - 1;
-            const int j2 = 63 - __clzll((long long)m);
-            v = R::add(R::mul(row0[j1], row[j2], ov), R::mul(row0[j2], row[j1], ov), ov);
-        } else if constexpr (R::kChecked) {
-            v = use_checked ? eval_subset<R>(m, q, k, row, prev, sb, ov)
-                            : eval_subset<RI64<false>>(m, q, k, row, prev, sb, ov);
-        } else {
-            v = eval_subset<R>(m, q, k, row, prev, sb, ov);
-        }
-        cur[r] = v;
+    for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        int j2 = 1;
+        while (binom_u64(j2 + 1, 2) <= r) ++j2;
+        const int j1 = (int)(r - binom_u64(j2, 2));
+        cur[r] = base_pair<R>(a, n, j1, j2, ov);
     }
     if (ov) atomicOr(status, 1);
 }

@@ -80,7 +80,7 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
     n = a.shape[0]
     if n < 3:
         raise ValueError("sharded DP needs n >= 3")
-    size = max_padded_layer(n, world)
+    size = max_padded_layer(n, world) + 4  # slack: 16-byte aligned ring copies may read one entry past a layer
     bufs = [torch.zeros(size, dtype=a.dtype, device=a.device) for _ in range(2)]
     plan = ShardPlan(n, world, rank)
     prev, cur = bufs
