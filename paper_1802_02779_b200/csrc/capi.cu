@@ -66,6 +66,22 @@ pl_status have_device() {
         cudaGetLastError();
         return fail(PL_ERR_NODEVICE, "no CUDA device available (the engine has no CPU fallback)");
     }
+    // Layer scratch comes from the stream-ordered allocator. Keep freed blocks
+    // cached in the device's default pool (as a caching allocator does): with
+    // the default release threshold of 0 every synchronisation would return
+    // them to the OS and the next call would re-map up to 2 x 9.6 GB.
+    static std::once_flag pool_once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+        std::call_once(pool_once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+        });
+    }
     return PL_OK;
 }
 
@@ -104,16 +120,21 @@ pl_status with_ring(pl_dtype dt, bool fma, F&& f) {
     return fail(PL_ERR_ARG, "unknown dtype");
 }
 
+int num_sms();
+
 constexpr int kRegsThreads = 128;
-constexpr int kRegsMaxOrder = 6;
+constexpr int kRegsMaxOrder = 5;  // n = 6 spills in registers; it runs in the shared-memory kernel
 
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
-    const size_t smem = (size_t)kRegsThreads * N * N * sizeof(T);
+    const size_t smem = 2 * (size_t)kRegsThreads * N * N * sizeof(T);  // double-buffered chunks
     auto kern = pl::sz_batch_regs_kernel<R, N, kRegsThreads>;
-    if (smem > 48 * 1024) PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = (count + kRegsThreads - 1) / kRegsThreads;
+    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegsThreads, smem));
+    const int64_t chunks = (count + kRegsThreads - 1) / kRegsThreads;
+    const int64_t blocks = std::min<int64_t>(chunks, (int64_t)num_sms() * std::max(per_sm, 1));
     kern<<<(unsigned)blocks, kRegsThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
@@ -127,20 +148,66 @@ pl_status launch_regs(int n, const void* a, void* out, int64_t count, int32_t* s
         case 3: return launch_regs_n<R, 3>(a, out, count, status, st);
         case 4: return launch_regs_n<R, 4>(a, out, count, status, st);
         case 5: return launch_regs_n<R, 5>(a, out, count, status, st);
-        case 6: return launch_regs_n<R, 6>(a, out, count, status, st);
     }
     return fail(PL_ERR_ARG, "register kernel order out of range");
 }
 
-size_t smem_binom_bytes() { return ((pl::kBinomDim * pl::kBinomDim * 4 + 15) / 16) * 16; }
-
 size_t smem_per_warp(pl_dtype dt, int n) {
-    return ((size_t)n * n + 2 * (size_t)max_layer(n)) * elem_size(dt);
+    return (((size_t)n * n + 2 * (size_t)max_layer(n)) * elem_size(dt) + 15) & ~size_t(15);
 }
 
 constexpr size_t kSmemCap = 200 * 1024;
+constexpr int kSmemMaxOrder = 14;  // predecessor ranks must fit 12 bits (C(14,7) = 3432)
 
-bool smem_fits(pl_dtype dt, int n) { return smem_binom_bytes() + smem_per_warp(dt, n) <= kSmemCap; }
+bool smem_fits(pl_dtype dt, int n) { return n <= kSmemMaxOrder && smem_per_warp(dt, n) <= kSmemCap; }
+
+struct Ptab {
+    uint16_t* tab = nullptr;
+    uint32_t* off = nullptr;
+};
+
+// Predecessor table of order n (see sz_batch_smem_kernel), built once per
+// (device, n) on the host and cached.
+pl_status get_ptab(int n, Ptab* out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, Ptab> cache;
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, n});
+    if (it != cache.end()) {
+        *out = it->second;
+        return PL_OK;
+    }
+    std::vector<uint32_t> off(n + 2, 0);
+    off[2] = 0;
+    off[3] = (uint32_t)pl::binom_u64(n, 2);
+    for (int k = 3; k <= n; ++k) off[k + 1] = off[k] + (k < n ? (uint32_t)(k * pl::binom_u64(n, k)) : 0u);
+    std::vector<uint16_t> tab(off[n + 1] ? off[n + 1] : 1);
+    for (int j2 = 1; j2 < n; ++j2)
+        for (int j1 = 0; j1 < j2; ++j1) tab[off[2] + j1 + j2 * (j2 - 1) / 2] = (uint16_t)(j1 | (j2 << 8));
+    for (int k = 3; k < n; ++k) {
+        const uint64_t ck = pl::binom_u64(n, k);
+        uint64_t mask = (1ull << k) - 1;
+        for (uint64_t r = 0; r < ck; ++r) {
+            int i = 0;
+            for (uint64_t m = mask; m; m &= m - 1, ++i) {
+                const int s = __builtin_ctzll(m);
+                tab[off[k] + i * ck + r] = (uint16_t)(pl_colex_rank(mask & ~(1ull << s)) | ((uint32_t)s << 12));
+            }
+            const uint64_t c = mask & (~mask + 1), rr = mask + c;  // Gosper: next k-subset in colex order
+            mask = (((rr ^ mask) >> 2) / c) | rr;
+        }
+    }
+    Ptab p;
+    PL_CUDA(cudaMalloc(&p.tab, tab.size() * sizeof(uint16_t)));
+    PL_CUDA(cudaMalloc(&p.off, off.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMemcpy(p.tab, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    PL_CUDA(cudaMemcpy(p.off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    cache[{dev, n}] = p;
+    *out = p;
+    return PL_OK;
+}
 
 int num_sms() {
     static int sms = 0;
@@ -158,10 +225,13 @@ template <class R>
 pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t count, int32_t* status,
                       cudaStream_t st) {
     using T = typename R::T;
+    Ptab pt;
+    pl_status s = get_ptab(n, &pt);
+    if (s != PL_OK) return s;
     const size_t pw = smem_per_warp(dt, n);
-    int warps = (int)std::min<size_t>(8, (kSmemCap - smem_binom_bytes()) / pw);
+    int warps = (int)std::min<size_t>(8, kSmemCap / pw);
     warps = std::max(1, warps);
-    const size_t smem = smem_binom_bytes() + warps * pw;
+    const size_t smem = warps * pw;
     auto kern = pl::sz_batch_smem_kernel<R>;
     PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
@@ -170,7 +240,7 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
     const int64_t need = (count + warps - 1) / warps;
     const int64_t blocks = std::min<int64_t>(need, (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, warps * 32, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, n,
-                                                     (int)max_layer(n), status);
+                                                     (int)max_layer(n), pt.tab, pt.off, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
@@ -248,17 +318,13 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     if (s != PL_OK) return s;
     const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
     const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
-    unsigned int* counter = nullptr;
-    PL_CUDA(cudaMallocAsync((void**)&counter, sizeof(unsigned int), st));
-    PL_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
-    const size_t smem = pl::WsSmem<T>::bytes(D);
+    const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<num_sms(), pl::kWsThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                                                  static_cast<T*>(cur), r0, r1, F0, F1, counter, q.qtab, q.offs,
+                                                  static_cast<T*>(cur), r0, r1, F0, F1, q.qtab, q.offs,
                                                   guard, status);
     PL_CUDA(cudaGetLastError());
-    PL_CUDA(cudaFreeAsync(counter, st));
     return PL_OK;
 }
 
@@ -292,7 +358,7 @@ pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* 
 pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
                         int32_t* status_dev, cudaStream_t st) {
     if (count == 0) return PL_OK;
-    if (n <= kRegsMaxOrder && !(dt == PL_C128 && n == kRegsMaxOrder)) {
+    if (n <= kRegsMaxOrder) {
         return with_ring(dt, fma, [&](auto r) { return launch_regs<decltype(r)>(n, a_dev, out_dev, count, status_dev, st); });
     }
     if (smem_fits(dt, n)) {
@@ -306,8 +372,9 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     int32_t* guards = nullptr;
     // Layer buffers carry 64 bytes of slack: 8-byte rings stage 16-byte aligned
     // spans that may read one element past a layer's last entry.
-    const size_t slack = 64;
-    PL_CUDA(cudaMallocAsync(&bufs, 2 * (ml * es + slack), st));
+    // Each buffer starts 256-byte aligned (TMA bulk copies need 16).
+    const size_t stride = (ml * es + 64 + 255) & ~size_t(255);
+    PL_CUDA(cudaMallocAsync(&bufs, 2 * stride, st));
     PL_CUDA(cudaMallocAsync((void**)&guards, sizeof(int32_t), st));
     PL_CUDA(cudaMemsetAsync(guards, 0, sizeof(int32_t), st));
     pl_status s = PL_OK;
@@ -318,8 +385,7 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
             pl::sz_guard_i64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(ab), n, guards);
         }
         s = with_ring(dt, fma, [&](auto r) {
-            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + ml * es + slack, guards,
-                                           status_dev, st);
+            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + stride, guards, status_dev, st);
         });
     }
     cudaFreeAsync(bufs, st);

@@ -9,34 +9,35 @@
 //     rank(S) = rank_D(V) + sum_{l=1..f} C(F_l, m + l),
 // so the k-subsets sharing F form one contiguous colex range, the tile (F, k),
 // of C(D, m) entries indexed by q = rank_D(V). Output q needs
-//   * low terms  S \ {v_i}: inside the tile (F, k-1) -> staged in shared memory,
+//   * low terms  S \ {v_i}: inside the tile (F, k-1), a small contiguous
+//     region (<= C(D, D/2) entries) gathered through L1 (__ldg);
 //     rank_D(V \ {v_i}) = P_i + Q_i (P_i = sum_{l<i} C(v_l, l),
 //     Q_i = sum_{l>i} C(v_l, l-1)), one paired-binomial lookup per term;
 //   * high terms S \ {F_l}: entry q of the tile (F \ {F_l}, k-1) -> aligned
-//     contiguous streams with a tile-uniform coefficient.
+//     contiguous streams with a tile-uniform coefficient, staged by TMA.
 // Low columns are all below high columns, so "low ascending, then high
 // ascending" is the reference's ascending-j order; the non-FMA rings keep its
 // rounding sequence bit for bit.
 //
-// Roles (one CTA per SM, persistent):
-//   warp 0, producer    claims tiles in increasing F (atomic counter: the GPU
-//                       sweeps each layer front to back, so stream tiles of
-//                       nearby high columns are re-read from L2), writes tile
-//                       descriptors, stages each tile's low source with one
-//                       TMA bulk copy into a double buffer (the next tile's
-//                       source is issued as soon as its buffer frees, while
-//                       the current tile still streams), and streams the
-//                       high-term segments of every chunk of CH outputs into
-//                       the owning group's NSG-stage ring, FS segments per stage, one
-//                       cp.async.bulk per segment, completion by mbarrier
-//                       transaction counts (~100 KB per SM in flight);
-//   warps 1..16         two consumer groups of 8 warps taking alternate chunks
-//                       (one output per thread): low terms from the staged
-//                       source, high terms from the group's ring, coalesced
-//                       store. Each group owns its ring, so every waiter is at
-//                       most one mbarrier phase ahead of the producer (a ring
-//                       shared by groups that run ahead of each other would
-//                       let parity waits pass a phase early).
+// Schedule. One CTA per SM, persistent. CTA b takes the b-th, (b+G)-th, ...
+// valid tile in increasing F (increasing colex order), so the GPU sweeps each
+// layer front to back and stream tiles of nearby high columns are re-read
+// from L2. Every warp walks the same tile sequence and derives each tile's
+// descriptor itself: there is no per-tile synchronisation at all.
+//
+// Roles.
+//   last warp, producer  streams the high-term segments of every chunk of CH
+//                        outputs into the owning consumer group's NSG-stage
+//                        shared-memory ring, FS segments per stage, one
+//                        cp.async.bulk per segment, completion by mbarrier
+//                        transaction counts (~160 KB in flight per SM). It is
+//                        the highest warp id: the issue arbiter favours high
+//                        ids over the consumers.
+//   warps 0..15          two consumer groups of 8 warps taking alternate
+//                        chunks, one output per thread: low terms (L1
+//                        gathers), high terms from the group's ring, coalesced
+//                        store. Each group owns its ring, so every waiter is
+//                        at most one mbarrier phase ahead of the producer.
 #pragma once
 
 #include <cstdint>
@@ -54,75 +55,51 @@ constexpr int kWsFS = 4;                      // stream segments per ring stage
 constexpr int kQtabShift = 17;                // qtab entry: mask(V) | rank(V \ {min V}) << 17
 constexpr int kWsEnd = -1;
 
-// Window width D and ring depth NS per element size (shared memory <= 227 KB).
+// Window width D and ring depth per element size (shared memory <= 227 KB;
+// what the ring leaves is L1 for the low-source gathers).
 __host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 14 : 15; }
 template <int ELEM>
 struct WsGeom {
-    static constexpr int NSG = ELEM == 16 ? 3 : 6;  // stages per group ring
-    static constexpr int NS = NSG * kWsGroups;
-};
-
-template <class T>
-struct WsDesc {
-    int32_t F, m, f, src_pad;
-    uint32_t q0, q1, rounds, pad;
-    uint64_t cur_base;
-    uint64_t sbase[kMaxOrder];  // bases of the stream tiles (F \ {F_l}, k-1) in the previous layer
-    T coef[kMaxOrder];          // a(k-1, F_l)
+    static constexpr int NSG = ELEM == 16 ? 4 : 8;  // stages per group ring (power of two)
 };
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size_t(15); }
 
 template <class T>
 struct WsSmem {
-    static constexpr int NS = WsGeom<(int)sizeof(T)>::NS;
     static constexpr int NSG = WsGeom<(int)sizeof(T)>::NSG;
     static constexpr size_t kSlot = round16(sizeof(T) * kWsChunk + 16) / sizeof(T);  // elements per segment slot
-    uint2* B2;         // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
-    WsDesc<T>* desc;   // [2]
-    uint64_t* full;    // [G][NSG]
-    uint64_t* empty;   // [G][NSG]
-    uint64_t* sfull;   // [2]
-    uint64_t* sempty;  // [2]
-    T* row_low;        // [32]
-    T* src;            // [2][src_stride]
-    T* stage;          // [G][NSG][FS][kSlot]
-    size_t src_stride;
+    uint2* B2;        // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
+    T* row_low;       // [32]   a(k-1, v), v < D
+    T* coef;          // [warps][kMaxOrder]  per-warp a(k-1, F_l) of the warp's current tile
+    uint64_t* full;   // [G][NSG]
+    uint64_t* empty;  // [G][NSG]
+    T* stage;         // [G][NSG][FS][kSlot]
 
-    __host__ __device__ static size_t bytes(int D) {
-        const size_t cap = (size_t)binom_u64(D, D / 2);
-        return round16(sizeof(uint2) * kBinomDim * kBinomDim) + 2 * round16(sizeof(WsDesc<T>)) +
-               round16(8 * (2 * NS + 4)) + round16(sizeof(T) * 32) + 2 * round16(sizeof(T) * cap + 16) +
-               round16((size_t)NS * kWsFS * kSlot * sizeof(T));
+    __host__ __device__ static size_t bytes() {
+        return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) +
+               round16(sizeof(T) * kMaxOrder * (kWsConsumerWarps + 1)) + round16(8 * 2 * kWsGroups * NSG) +
+               round16((size_t)kWsGroups * NSG * kWsFS * kSlot * sizeof(T));
     }
-    __device__ WsSmem(unsigned char* base, int D) {
+    __device__ explicit WsSmem(unsigned char* base) {
         size_t off = 0;
         auto take = [&](size_t b) {
             unsigned char* p = base + off;
             off += round16(b);
             return p;
         };
-        const size_t cap = (size_t)binom_u64(D, D / 2);
         B2 = reinterpret_cast<uint2*>(take(sizeof(uint2) * kBinomDim * kBinomDim));
-        desc = reinterpret_cast<WsDesc<T>*>(take(2 * round16(sizeof(WsDesc<T>))));
-        uint64_t* bars = reinterpret_cast<uint64_t*>(take(8 * (2 * NS + 4)));
-        full = bars;
-        empty = bars + NS;
-        sfull = bars + 2 * NS;
-        sempty = bars + 2 * NS + 2;
         row_low = reinterpret_cast<T*>(take(sizeof(T) * 32));
-        src_stride = round16(sizeof(T) * cap + 16) / sizeof(T);
-        src = reinterpret_cast<T*>(take(2 * round16(sizeof(T) * cap + 16)));
-        stage = reinterpret_cast<T*>(take((size_t)NS * kWsFS * kSlot * sizeof(T)));
+        coef = reinterpret_cast<T*>(take(sizeof(T) * kMaxOrder * (kWsConsumerWarps + 1)));
+        uint64_t* bars = reinterpret_cast<uint64_t*>(take(8 * 2 * kWsGroups * NSG));
+        full = bars;
+        empty = bars + kWsGroups * NSG;
+        stage = reinterpret_cast<T*>(take((size_t)kWsGroups * NSG * kWsFS * kSlot * sizeof(T)));
     }
-    __device__ T* src_buf(int b) const { return src + (size_t)b * src_stride; }
-    // ring slot of group g, stage s, segment li
     __device__ T* slot(int g, int s, int li) const { return stage + (((size_t)g * NSG + s) * kWsFS + li) * kSlot; }
     __device__ uint64_t* full_bar(int g, int s) const { return full + g * NSG + s; }
     __device__ uint64_t* empty_bar(int g, int s) const { return empty + g * NSG + s; }
-    __device__ WsDesc<T>* desc_buf(int b) const {
-        return reinterpret_cast<WsDesc<T>*>(reinterpret_cast<unsigned char*>(desc) + b * round16(sizeof(WsDesc<T>)));
-    }
+    __device__ T* warp_coef(int w) const { return coef + (size_t)w * kMaxOrder; }
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -152,20 +129,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
-}
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
 }
 
 // TMA 1D bulk copy global -> shared, completion counted on `bar` in bytes.
@@ -199,6 +162,67 @@ __device__ __forceinline__ BulkSpan<T> bulk_span(const T* base, uint64_t start, 
     }
 }
 
+// ---------------------------------------------------------------- tiles
+
+struct WsTile {
+    int32_t F, m, f;
+    uint32_t q0, q1, nchunks;
+    uint64_t cur_base, src_base;
+};
+
+// Next valid tile of this CTA's static interleaved share (F with
+// 0 <= k - |F| <= D), or kWsEnd. Every warp walks the same sequence.
+__device__ __forceinline__ int32_t ws_next(uint32_t& cursor, uint32_t F1, int k, int D) {
+    for (;;) {
+        const uint32_t t = cursor;
+        if (t > F1) return kWsEnd;
+        cursor += gridDim.x;
+        const int mm = k - __popc(t);
+        if (mm >= 0 && mm <= D) return (int32_t)t;
+    }
+}
+
+__device__ __forceinline__ WsTile ws_tile(int32_t F, int k, int D, uint64_t r0, uint64_t r1,
+                                          const uint2* __restrict__ B2) {
+    WsTile t;
+    t.F = F;
+    t.f = __popc((uint32_t)F);
+    t.m = k - t.f;
+    t.cur_base = 0;
+    t.src_base = 0;
+    int l = 1;
+    for (uint32_t ff = (uint32_t)F; ff; ff &= ff - 1, ++l) {
+        const int col = D + __ffs(ff) - 1;
+        const uint2 b = B2[(t.m + l) * kBinomDim + col];
+        t.cur_base += b.x;
+        t.src_base += b.y;
+    }
+    const uint32_t len = B2[t.m * kBinomDim + D].x;
+    t.q0 = r0 > t.cur_base ? (uint32_t)(r0 - t.cur_base) : 0u;
+    t.q1 = (r1 - t.cur_base) < len ? (uint32_t)(r1 - t.cur_base) : len;
+    t.nchunks = t.q1 > t.q0 ? (t.q1 - t.q0 + kWsChunk - 1) / kWsChunk : 0u;
+    return t;
+}
+
+// Column of the l-th (0-based) high element of F.
+__device__ __forceinline__ int ws_high_col(uint32_t F, int l, int D) {
+    for (int i = 0; i < l; ++i) F &= F - 1;
+    return D + __ffs(F) - 1;
+}
+
+// Base rank, in the previous layer, of the stream tile (F \ {F_l}, k-1): the
+// remaining high elements keep the low count m and shift down one position.
+__device__ __forceinline__ uint64_t ws_stream_base(uint32_t F, int l, int m, int D, const uint2* __restrict__ B2) {
+    uint64_t b = 0;
+    int i = 0, p = 1;
+    for (uint32_t ff = F; ff; ff &= ff - 1, ++i) {
+        if (i == l) continue;
+        b += B2[(m + p) * kBinomDim + D + __ffs(ff) - 1].x;
+        ++p;
+    }
+    return b;
+}
+
 // ---------------------------------------------------------------- consumer math
 
 template <class RR, int M, class T>
@@ -206,18 +230,24 @@ __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const
                                     const uint2* __restrict__ B2, bool& ov) {
     uint32_t V = e & ((1u << kQtabShift) - 1);
     uint32_t Q = e >> kQtabShift, P = 0;
-    T acc;
+    int sv[M];
+    uint32_t pr[M];
 #pragma unroll
     for (int i = 1; i <= M; ++i) {
         const int s = __ffs(V) - 1;
         V &= V - 1;
         const uint2 b = B2[i * kBinomDim + s];  // (C(s, i), C(s, i-1))
         if (i >= 2) Q -= b.y;
-        const T c = row_low[s];
-        const T x = src[P + Q];
-        acc = i == 1 ? RR::mul(c, x, ov) : RR::mac(acc, c, x, ov);
+        sv[i - 1] = s;
+        pr[i - 1] = P + Q;
         P += b.x;
     }
+    T x[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) x[i] = __ldg(src + pr[i]);
+    T acc = RR::mul(row_low[sv[0]], x[0], ov);
+#pragma unroll
+    for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[sv[i]], x[i], ov);
     return acc;
 }
 
@@ -236,131 +266,68 @@ __device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, co
     return RR::zero();
 }
 
-// One ring stage's high terms for output j.
+// One ring stage's high terms for output j (a full stage needs no predicates).
 template <class RR, class T>
-__device__ __forceinline__ T ws_stage_terms(T acc, const WsSmem<T>& sm, const WsDesc<T>& d, int g, int s, int l0,
-                                            int nl, uint32_t c0, int j, bool init_first, bool& ov) {
+__device__ __forceinline__ T ws_stage_terms(T acc, const WsSmem<T>& sm, const T* __restrict__ coef, int g, int s,
+                                            int l0, int nl, const int* __restrict__ pads, int j, bool init_first,
+                                            bool& ov) {
+    const T* st = sm.slot(g, s, 0) + j;
+    if (nl == kWsFS && !init_first) {
+#pragma unroll
+        for (int li = 0; li < kWsFS; ++li) acc = RR::mac(acc, coef[l0 + li], st[li * WsSmem<T>::kSlot + pads[li]], ov);
+        return acc;
+    }
 #pragma unroll
     for (int li = 0; li < kWsFS; ++li) {
         if (li < nl) {
-            const int pad = sizeof(T) == 16 ? 0 : (int)((d.sbase[l0 + li] + c0) & 1u);
-            const T x = sm.slot(g, s, li)[pad + j];
-            acc = (init_first && li == 0) ? RR::mul(d.coef[l0 + li], x, ov) : RR::mac(acc, d.coef[l0 + li], x, ov);
+            const T x = st[li * WsSmem<T>::kSlot + pads[li]];
+            acc = (init_first && li == 0) ? RR::mul(coef[l0 + li], x, ov) : RR::mac(acc, coef[l0 + li], x, ov);
         }
     }
     return acc;
 }
 
 // Consumer group g's share of one tile: chunks g, g + G, g + 2G, ... Each of
-// its chunks takes `rounds` consecutive stages of the group's own ring; `seq`
-// is the group's running stage counter (stage seq % NSG, use seq / NSG).
+// its chunks takes ceil(f / FS) consecutive stages of the group's own ring;
+// `seq` is the group's running stage counter (stage seq % NSG, use seq / NSG).
 template <class RR, class T>
-__device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsDesc<T>& d, const T* src,
+__device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTile& t, const T* __restrict__ src,
+                                                const T* __restrict__ coef, const uint64_t* __restrict__ sbase_pad,
                                                 const uint32_t* __restrict__ qt, T* __restrict__ cur, int g, int j,
                                                 uint32_t& seq, bool& ov) {
     constexpr int NSG = WsSmem<T>::NSG;
-    const int m = d.m, f = d.f;
-    const uint32_t nchunks = (d.q1 - d.q0 + kWsChunk - 1) / kWsChunk;
-    // qtab prefetch one chunk ahead (its latency is a global load)
+    const int m = t.m, f = t.f;
     uint32_t c = (uint32_t)g;
-    uint32_t e_next = 0;
-    if (m >= 1 && c < nchunks) {
-        const uint32_t q = d.q0 + c * kWsChunk + j;
-        if (q < d.q1) e_next = __ldg(qt + q);
-    }
-    for (; c < nchunks; c += kWsGroups) {
-        const uint32_t c0 = d.q0 + c * kWsChunk;
-        const uint32_t len = min((uint32_t)kWsChunk, d.q1 - c0);
+    uint32_t e_next = 0;  // qtab prefetch one chunk ahead (a global load)
+    if (m >= 1 && c < t.nchunks) e_next = __ldg(qt + min(t.q0 + c * kWsChunk + j, t.q1 - 1));
+    for (; c < t.nchunks; c += kWsGroups) {
+        const uint32_t c0 = t.q0 + c * kWsChunk;
+        const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
+        // Lanes past the tile end compute a duplicate of its last output
+        // (no divergence); only their store and overflow flag are dropped.
         const bool valid = (uint32_t)j < len;
         const uint32_t e = e_next;
-        if (m >= 1 && c + kWsGroups < nchunks) {
-            const uint32_t qn = c0 + kWsGroups * kWsChunk + j;
-            if (qn < d.q1) e_next = __ldg(qt + qn);
-        }
+        if (m >= 1 && c + kWsGroups < t.nchunks) e_next = __ldg(qt + min(c0 + kWsGroups * kWsChunk + j, t.q1 - 1));
+        bool lov = false;
         T acc = RR::zero();
-        if (valid && m >= 1) acc = ws_low_dispatch<RR>(m, e, src, sm.row_low, sm.B2, ov);
+        if (m >= 1) acc = ws_low_dispatch<RR>(m, e, src, sm.row_low, sm.B2, lov);
         for (int l0 = 0; l0 < f; l0 += kWsFS, ++seq) {
             const int nl = min(kWsFS, f - l0);
+            int pads[kWsFS];
+#pragma unroll
+            for (int li = 0; li < kWsFS; ++li) {
+                pads[li] = sizeof(T) == 16 || li >= nl ? 0 : (int)((sbase_pad[l0 + li] + c0) & 1u);
+            }
             const int s = (int)(seq % NSG);
             mbar_wait(sm.full_bar(g, s), (seq / NSG) & 1u);
-            if (valid) acc = ws_stage_terms<RR>(acc, sm, d, g, s, l0, nl, c0, j, m == 0 && l0 == 0, ov);
+            acc = ws_stage_terms<RR>(acc, sm, coef, g, s, l0, nl, pads, j, m == 0 && l0 == 0, lov);
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
         }
-        if (valid) cur[d.cur_base + c0 + j] = acc;
-    }
-}
-
-// ---------------------------------------------------------------- producer helpers
-
-// Claims the next valid tile (F with 0 <= k - |F| <= D) or kWsEnd; lane 0 only.
-__device__ __forceinline__ int32_t ws_claim(unsigned int* counter, uint32_t F0, uint32_t F1, int k, int D) {
-    for (;;) {
-        const uint32_t t = F0 + atomicAdd(counter, 1u);
-        if (t > F1) return kWsEnd;
-        const int mm = k - __popc(t);
-        if (mm >= 0 && mm <= D) return (int32_t)t;
-    }
-}
-
-// Writes the descriptor of tile F into buffer tb and issues its low-source
-// bulk copy (whole warp; the arrive on sfull[tb] releases the descriptor).
-template <class T>
-__device__ __forceinline__ void ws_open_tile(const WsSmem<T>& sm, int tb, int32_t F, int k, int D, uint64_t r0,
-                                             uint64_t r1, const T* __restrict__ prev, const T* __restrict__ row,
-                                             int lane) {
-    WsDesc<T>* d = sm.desc_buf(tb);
-    if (F == kWsEnd) {
-        if (lane == 0) {
-            d->F = kWsEnd;
-            mbar_arrive(&sm.sfull[tb]);
+        if (valid) {
+            cur[t.cur_base + c0 + j] = acc;
+            ov |= lov;
         }
-        return;
-    }
-    const int f = __popc((uint32_t)F), m = k - f;
-    uint64_t cur_base = 0, src_base = 0;
-    {
-        int l = 1;
-        for (uint32_t ff = (uint32_t)F; ff; ff &= ff - 1, ++l) {
-            const int col = D + __ffs(ff) - 1;
-            const uint2 b = sm.B2[(m + l) * kBinomDim + col];
-            cur_base += b.x;
-            src_base += b.y;
-        }
-    }
-    if (lane < f) {
-        uint64_t b = 0;
-        int l = 0, p = 1;
-        for (uint32_t ff = (uint32_t)F; ff; ff &= ff - 1, ++l) {
-            const int col = D + __ffs(ff) - 1;
-            if (l == lane) {
-                d->coef[lane] = row[col];
-                continue;
-            }
-            b += sm.B2[(m + p) * kBinomDim + col].x;
-            ++p;
-        }
-        d->sbase[lane] = b;
-    }
-    const uint32_t tile_len = sm.B2[m * kBinomDim + D].x;
-    const uint32_t q0 = r0 > cur_base ? (uint32_t)(r0 - cur_base) : 0u;
-    const uint32_t q1 = (r1 - cur_base) < tile_len ? (uint32_t)(r1 - cur_base) : tile_len;
-    BulkSpan<T> sp{prev, 0u, 0};
-    if (m >= 1) sp = bulk_span(prev, src_base, sm.B2[(m - 1) * kBinomDim + D].x);
-    if (lane == 0) {
-        d->F = F;
-        d->m = m;
-        d->f = f;
-        d->q0 = q0;
-        d->q1 = q1;
-        d->rounds = (uint32_t)((f + kWsFS - 1) / kWsFS);
-        d->cur_base = cur_base;
-        d->src_pad = sp.pad;
-    }
-    __syncwarp();
-    if (lane == 0) {
-        mbar_arrive_expect_tx(&sm.sfull[tb], sp.bytes);
-        if (sp.bytes) bulk_g2s(sm.src_buf(tb), sp.src, sp.bytes, &sm.sfull[tb]);
     }
 }
 
@@ -370,13 +337,13 @@ template <class R, class RU>
 __global__ void __launch_bounds__(kWsThreads, 1)
     sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, uint32_t F0, uint32_t F1,
-                 unsigned int* __restrict__ counter, const uint32_t* __restrict__ qtab,
-                 const uint32_t* __restrict__ qtab_off, const int32_t* __restrict__ guard,
-                 int32_t* __restrict__ status) {
+                 const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
+                 const int32_t* __restrict__ guard, int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const WsSmem<T> sm(smem_raw, D);
+    __shared__ uint64_t sbase_sh[kWsConsumerWarps + 1][kMaxOrder];  // per-warp stream bases (8-byte pads)
+    const WsSmem<T> sm(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* row = a + (size_t)(k - 1) * n;
 
@@ -390,91 +357,68 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             mbar_init(&sm.full[s], 1);               // producer's arrive.expect_tx
             mbar_init(&sm.empty[s], kWsGroupWarps);  // the owning group's warps
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&sm.sfull[b], 1);
-            mbar_init(&sm.sempty[b], kWsConsumerWarps);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == 0) {
+    uint32_t cursor = F0 + blockIdx.x;
+    if (warp == kWsConsumerWarps) {
         // ------------------------------------------------------------ producer
         uint32_t seqg[kWsGroups] = {};
-        uint32_t tile_u = 0;
-        int32_t F = 0;
-        if (lane == 0) F = ws_claim(counter, F0, F1, k, D);
-        F = __shfl_sync(0xffffffffu, F, 0);
-        ws_open_tile(sm, 0, F, k, D, r0, r1, prev, row, lane);  // buffer 0 starts free
-        while (F != kWsEnd) {
-            const WsDesc<T>* d = sm.desc_buf((int)(tile_u & 1u));
-            int32_t Fn = 0;
-            if (lane == 0) Fn = ws_claim(counter, F0, F1, k, D);
-            Fn = __shfl_sync(0xffffffffu, Fn, 0);
-            const int nb = (int)((tile_u + 1) & 1u);
-            const unsigned npar = (((tile_u + 1) >> 1) & 1u) ^ 1u;
-            bool opened = false;
-            const int f = d->f;
+        for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
+            const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
+            // lane l holds the base of stream tile F \ {F_l}
+            const uint64_t my_base = lane < t.f ? ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2) : 0;
             int g = 0;
-            for (uint32_t c0 = d->q0; c0 < d->q1; c0 += kWsChunk, g = (g + 1) % kWsGroups) {
-                const uint32_t len = min((uint32_t)kWsChunk, d->q1 - c0);
-                for (int l0 = 0; l0 < f; l0 += kWsFS) {
-                    // one lane decides (per-lane test_wait results may differ) and broadcasts
-                    bool ready = false;
-                    if (!opened) ready = __shfl_sync(0xffffffffu, lane == 0 ? mbar_test(&sm.sempty[nb], npar) : false, 0);
-                    if (ready) {
-                        ws_open_tile(sm, nb, Fn, k, D, r0, r1, prev, row, lane);
-                        opened = true;
-                    }
-                    const int nl = min(kWsFS, f - l0);
+            for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == kWsGroups) ? 0 : g + 1) {
+                const uint32_t c0 = t.q0 + c * kWsChunk;
+                const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
+                for (int l0 = 0; l0 < t.f; l0 += kWsFS) {
+                    const int nl = min(kWsFS, t.f - l0);
+                    const uint64_t base = __shfl_sync(0xffffffffu, my_base, (l0 + lane) & 31);
                     const uint32_t sq = seqg[g]++;
                     const int s = (int)(sq % NSG);
                     mbar_wait(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
                     BulkSpan<T> seg{prev, 0u, 0};
-                    if (lane < nl) seg = bulk_span(prev, d->sbase[l0 + lane] + c0, len);
-                    unsigned total = seg.bytes;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+                    if (lane < nl) seg = bulk_span(prev, base + c0, len);
+                    const unsigned total = __reduce_add_sync(0xffffffffu, seg.bytes);
                     if (lane == 0) mbar_arrive_expect_tx(sm.full_bar(g, s), total);
                     __syncwarp();
                     if (lane < nl) bulk_g2s(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s));
                 }
             }
-            if (!opened) {
-                mbar_wait(&sm.sempty[nb], npar);
-                ws_open_tile(sm, nb, Fn, k, D, r0, r1, prev, row, lane);
-            }
-            F = Fn;
-            ++tile_u;
         }
     } else {
         // ------------------------------------------------------------ consumers
-        const int cw = warp - 1;
-        const int g = cw / kWsGroupWarps;
-        const int j = (cw % kWsGroupWarps) * 32 + lane;
+        const int g = warp / kWsGroupWarps;
+        const int j = (warp % kWsGroupWarps) * 32 + lane;
+        T* coef = sm.warp_coef(warp);
+        uint64_t* sb = sbase_sh[warp];
         bool use_checked = false;
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
-        uint32_t seq = 0, tile_u = 0;
-        for (;;) {
-            const int tb = (int)(tile_u & 1u);
-            mbar_wait(&sm.sfull[tb], (tile_u >> 1) & 1u);
-            const WsDesc<T>& d = *sm.desc_buf(tb);
-            if (d.F == kWsEnd) break;
-            const uint32_t* qt = qtab + qtab_off[d.m];
-            const T* src = sm.src_buf(tb) + d.src_pad;
-            if constexpr (R::kChecked) {
-                if (use_checked) {
-                    ws_consume_tile<R>(sm, d, src, qt, cur, g, j, seq, ov);
-                } else {
-                    ws_consume_tile<RU>(sm, d, src, qt, cur, g, j, seq, ov);
-                }
-            } else {
-                ws_consume_tile<R>(sm, d, src, qt, cur, g, j, seq, ov);
+        uint32_t seq = 0;
+        for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
+            const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
+            // skip tiles with no chunk for this group (no stages either)
+            if ((uint32_t)g >= t.nchunks) continue;
+            __syncwarp();
+            if (lane < t.f) {
+                coef[lane] = row[ws_high_col((uint32_t)F, lane, D)];
+                if constexpr (sizeof(T) != 16) sb[lane] = ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.sempty[tb]);
-            ++tile_u;
+            const uint32_t* qt = qtab + qtab_off[t.m];
+            const T* src = prev + t.src_base;
+            if constexpr (R::kChecked) {
+                if (use_checked) {
+                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+                } else {
+                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+                }
+            } else {
+                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+            }
         }
         if (ov) atomicOr(status, 1);
     }
