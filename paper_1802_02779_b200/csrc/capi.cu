@@ -60,12 +60,15 @@ uint64_t max_layer(int n) {
 }
 
 pl_status have_device() {
-    int count = 0;
-    const cudaError_t e = cudaGetDeviceCount(&count);
-    if (e != cudaSuccess || count == 0) {
-        cudaGetLastError();
-        return fail(PL_ERR_NODEVICE, "no CUDA device available (the engine has no CPU fallback)");
-    }
+    static const int count = [] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        return c;
+    }();
+    if (count == 0) return fail(PL_ERR_NODEVICE, "no CUDA device available (the engine has no CPU fallback)");
     // Layer scratch comes from the stream-ordered allocator. Keep freed blocks
     // cached in the device's default pool (as a caching allocator does): with
     // the default release threshold of 0 every synchronisation would return
@@ -122,19 +125,31 @@ pl_status with_ring(pl_dtype dt, bool fma, F&& f) {
 
 int num_sms();
 
+// Raise a kernel's MaxDynamicSharedMemorySize only when a launch needs more
+// than any earlier one (the attribute is a per-kernel maximum: lowering it
+// would invalidate larger launches of the same kernel).
+template <class K>
+cudaError_t set_smem_once(K kern, size_t bytes) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> cur;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = cur[reinterpret_cast<const void*>(kern)];
+    if (bytes <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
 constexpr int kRegsThreads = 128;
 constexpr int kRegsMaxOrder = 5;  // n = 6 spills in registers; it runs in the shared-memory kernel
 
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
-    const size_t smem = 2 * (size_t)kRegsThreads * N * N * sizeof(T);  // double-buffered chunks
+    const size_t smem = (size_t)kRegsThreads * N * N * sizeof(T);
     auto kern = pl::sz_batch_regs_kernel<R, N, kRegsThreads>;
-    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 1;
-    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRegsThreads, smem));
-    const int64_t chunks = (count + kRegsThreads - 1) / kRegsThreads;
-    const int64_t blocks = std::min<int64_t>(chunks, (int64_t)num_sms() * std::max(per_sm, 1));
+    PL_CUDA(set_smem_once(kern, smem));
+    const int64_t blocks = (count + kRegsThreads - 1) / kRegsThreads;
     kern<<<(unsigned)blocks, kRegsThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
@@ -153,7 +168,7 @@ pl_status launch_regs(int n, const void* a, void* out, int64_t count, int32_t* s
 }
 
 size_t smem_per_warp(pl_dtype dt, int n) {
-    return (((size_t)n * n + 2 * (size_t)max_layer(n)) * elem_size(dt) + 15) & ~size_t(15);
+    return ((((size_t)n * n + 1) & ~size_t(1)) + 2 * (((size_t)max_layer(n) + 1) & ~size_t(1))) * elem_size(dt);
 }
 
 constexpr size_t kSmemCap = 200 * 1024;
@@ -228,19 +243,15 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
     Ptab pt;
     pl_status s = get_ptab(n, &pt);
     if (s != PL_OK) return s;
-    const size_t pw = smem_per_warp(dt, n);
-    int warps = (int)std::min<size_t>(8, kSmemCap / pw);
-    warps = std::max(1, warps);
-    const size_t smem = warps * pw;
+    const size_t smem = smem_per_warp(dt, n) + 32;  // one matrix per CTA
     auto kern = pl::sz_batch_smem_kernel<R>;
-    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;
-    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     per_sm = std::max(per_sm, 1);
-    const int64_t need = (count + warps - 1) / warps;
-    const int64_t blocks = std::min<int64_t>(need, (int64_t)num_sms() * per_sm);
-    kern<<<(unsigned)blocks, warps * 32, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, n,
-                                                     (int)max_layer(n), pt.tab, pt.off, status);
+    const int64_t blocks = std::min<int64_t>(count, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, 128, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, n,
+                                              (int)max_layer(n), pt.tab, pt.off, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
@@ -320,7 +331,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
-    PL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PL_CUDA(set_smem_once(kern, smem));
     kern<<<num_sms(), pl::kWsThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                                   static_cast<T*>(cur), r0, r1, F0, F1, q.qtab, q.offs,
                                                   guard, status);

@@ -19,7 +19,7 @@
 //                         registers (compile-time subset masks), inputs staged
 //                         through shared memory by double-buffered TMA bulk
 //                         copies (persistent CTAs).
-//   sz_batch_smem_kernel  6 <= n <= 14: one warp per matrix, ping-pong
+//   sz_batch_smem_kernel  6 <= n <= 14: one CTA per matrix, ping-pong
 //                         layers and the matrix in shared memory, predecessor
 //                         ranks from a host-built table shared by the batch.
 //   sz_base_layer_kernel  layer 2 (order-2 base case) of a single large matrix;
@@ -180,138 +180,123 @@ __device__ __forceinline__ bool i64_guard_ok(const long long* a, int n, int stri
 
 __device__ __forceinline__ unsigned smem_addr_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-// Persistent batched kernel for n <= 6. CTA-sized chunks of THREADS
-// consecutive matrices (one per thread) are staged into shared memory by one
-// TMA bulk copy each, double-buffered: the copy of the next chunk is in
-// flight while the current chunk is evaluated in registers. Chunks that are
-// partial or misaligned fall back to cooperative 8-byte loads.
+// Batched kernel for n <= 5: one thread per matrix, the whole DP in
+// registers. Each CTA stages its chunk of THREADS consecutive matrices into
+// shared memory with one TMA bulk copy (cooperative 8-byte loads for a partial
+// or misaligned chunk); four CTAs per SM overlap one another's copies and
+// arithmetic.
 template <class R, int N, int THREADS>
-__global__ void __launch_bounds__(THREADS) sz_batch_regs_kernel(const typename R::T* __restrict__ a,
-                                                                typename R::T* __restrict__ out, int64_t count,
-                                                                int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(THREADS, 4) sz_batch_regs_kernel(const typename R::T* __restrict__ a,
+                                                                   typename R::T* __restrict__ out, int64_t count,
+                                                                   int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int kEnt = N * N;
     constexpr size_t kChunkBytes = (size_t)THREADS * kEnt * sizeof(T);
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bar[2];
-    T* buf[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw + kChunkBytes)};
-    const int64_t nchunks = (count + THREADS - 1) / THREADS;
-    const bool aligned = (reinterpret_cast<uintptr_t>(a) & 15u) == 0;
-    auto full_bulk = [&](int64_t c) { return aligned && (c + 1) * THREADS <= count && (kChunkBytes % 16) == 0; };
-    auto issue = [&](int64_t c, int b) {  // thread 0 only
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr_u32(&bar[b])),
-                     "r"((unsigned)kChunkBytes)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                smem_addr_u32(buf[b])),
-            "l"(a + c * THREADS * kEnt), "r"((unsigned)kChunkBytes), "r"(smem_addr_u32(&bar[b]))
-            : "memory");
-    };
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr_u32(&bar[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr_u32(&bar[1])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    int64_t c = blockIdx.x;
-    if (threadIdx.x == 0 && c < nchunks && full_bulk(c)) issue(c, 0);
-    unsigned phase[2] = {0u, 0u};
-    for (int b = 0; c < nchunks; c += gridDim.x, b ^= 1) {
-        const int64_t cn = c + gridDim.x;
-        if (threadIdx.x == 0 && cn < nchunks && full_bulk(cn)) issue(cn, b ^ 1);
-        const int64_t first = c * THREADS;
-        const int nvalid = count - first < THREADS ? (int)(count - first) : THREADS;
-        if (full_bulk(c)) {
+    __shared__ __align__(8) uint64_t bar;
+    T* buf = reinterpret_cast<T*>(smem_raw);
+    const int64_t first = (int64_t)blockIdx.x * THREADS;
+    const int nvalid = count - first < THREADS ? (int)(count - first) : THREADS;
+    const bool bulk = (reinterpret_cast<uintptr_t>(a) & 15u) == 0 && nvalid == THREADS && (kChunkBytes % 16) == 0;
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr_u32(&bar)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr_u32(&bar)),
+                         "r"((unsigned)kChunkBytes)
+                         : "memory");
             asm volatile(
-                "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
-                    smem_addr_u32(&bar[b])),
-                "r"(phase[b])
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_addr_u32(buf)),
+                "l"(a + first * kEnt), "r"((unsigned)kChunkBytes), "r"(smem_addr_u32(&bar))
                 : "memory");
-            phase[b] ^= 1u;
-        } else {
-            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a + first * kEnt);
-            unsigned long long* dst = reinterpret_cast<unsigned long long*>(buf[b]);
-            const int words = nvalid * kEnt * (int)(sizeof(T) / 8);
-            for (int w = threadIdx.x; w < words; w += THREADS) dst[w] = __ldg(src + w);
-            __syncthreads();
         }
-        if (threadIdx.x < nvalid) {
-            const T* local = buf[b] + threadIdx.x * kEnt;
-            bool ov = false;
-            T v;
-            if constexpr (R::kChecked) {
-                // int64: the unchecked instantiation when every lane's matrix
-                // passes the guard (warp-uniform), checked arithmetic otherwise.
-                const bool ok = i64_guard_ok(local, N);
-                if (__all_sync(__activemask(), ok)) {
-                    v = perm_in_registers<RI64<false>, N>(local, ov);
-                } else {
-                    v = perm_in_registers<R, N>(local, ov);
-                }
-            } else {
-                v = perm_in_registers<R, N>(local, ov);
-            }
-            if (ov) {
-                atomicOr(status, 1);
-                v = R::zero();
-            }
-            out[first + threadIdx.x] = v;
-        }
-        __syncthreads();  // buffer b is refilled two chunks later
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        asm volatile(
+            "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(
+                smem_addr_u32(&bar))
+            : "memory");
+    } else {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a + first * kEnt);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(buf);
+        const int words = nvalid * kEnt * (int)(sizeof(T) / 8);
+        for (int w = threadIdx.x; w < words; w += THREADS) dst[w] = __ldg(src + w);
+        __syncthreads();
     }
+    if (threadIdx.x >= nvalid) return;
+    const T* local = buf + threadIdx.x * kEnt;
+    bool ov = false;
+    T v;
+    if constexpr (R::kChecked) {
+        // int64: the unchecked instantiation when every lane's matrix passes
+        // the guard (warp-uniform), checked arithmetic otherwise.
+        const bool ok = i64_guard_ok(local, N);
+        if (__all_sync(__activemask(), ok)) {
+            v = perm_in_registers<RI64<false>, N>(local, ov);
+        } else {
+            v = perm_in_registers<R, N>(local, ov);
+        }
+    } else {
+        v = perm_in_registers<R, N>(local, ov);
+    }
+    if (ov) {
+        atomicOr(status, 1);
+        v = R::zero();
+    }
+    out[first + threadIdx.x] = v;
 }
 
 // ---------------------------------------------------------------- 7 <= n <= 14
 
-// One warp per matrix; the matrix and two layer buffers live in the warp's
-// shared-memory slice; warps stride over the batch (persistent CTAs). The
-// predecessor structure is the same for every matrix of order n, so it is
-// read from a table built once on the host (L1-resident, coalesced):
+// One CTA per matrix at a time (persistent CTAs striding over the batch);
+// the matrix and two layer buffers live in the CTA's shared memory (16 KB at
+// n = 12, so ~14 CTAs share an SM). The predecessor structure is the same for
+// every matrix of order n, so it is read from a table built once on the host
+// (L1-resident, coalesced):
 //   layer 2:  ptab[off[2] + r]           = j1 | j2 << 8       (r = j1 + C(j2, 2))
 //   layer k:  ptab[off[k] + i*C(n,k) + r] = rank(S \ {s_i}) | s_i << 12
 // with s_i the i-th element of the r-th k-subset in colex order, ascending.
 template <class R>
-__global__ void __launch_bounds__(256) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
+__global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
                                                             typename R::T* __restrict__ out, int64_t count,
                                                             int n, int maxc, const uint16_t* __restrict__ ptab,
                                                             const uint32_t* __restrict__ poff,
                                                             int32_t* __restrict__ status) {
     using T = typename R::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warps = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t per_warp = (((size_t)n * n + 2 * (size_t)maxc) * sizeof(T) + 15) & ~size_t(15);
-    T* mat = reinterpret_cast<T*>(smem_raw + warp * per_warp);
-    T* buf0 = mat + n * n;
-    T* buf1 = buf0 + maxc;
+    __shared__ int flag;
+    T* mat = reinterpret_cast<T*>(smem_raw);
+    T* buf0 = mat + ((n * n + 1) & ~1);
+    T* buf1 = buf0 + ((maxc + 1) & ~1);
+    const int tid = threadIdx.x, nt = blockDim.x;
 
-    for (int64_t b = (int64_t)blockIdx.x * warps + warp; b < count; b += (int64_t)gridDim.x * warps) {
+    for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
         const T* g = a + b * n * n;
-        for (int e = lane; e < n * n; e += 32) mat[e] = g[e];
-        __syncwarp();
+        for (int e = tid; e < n * n; e += nt) mat[e] = g[e];
+        if (tid == 0) flag = 0;
+        __syncthreads();
         bool ov = false;
         bool use_checked = false;
         if constexpr (R::kChecked) {
-            bool ok = true;
-            if (lane == 0) ok = i64_guard_ok(reinterpret_cast<const long long*>(mat), n);
-            use_checked = !__shfl_sync(0xffffffffu, ok, 0);
+            if (tid == 0) flag = i64_guard_ok(reinterpret_cast<const long long*>(mat), n) ? 0 : 2;
+            __syncthreads();
+            use_checked = flag == 2;
         }
         auto run = [&](auto ring) {
             using RR = decltype(ring);
             const uint32_t c2 = poff[3] - poff[2];
-            for (uint32_t r = lane; r < c2; r += 32) {
+            for (uint32_t r = tid; r < c2; r += nt) {
                 const uint32_t e = __ldg(ptab + poff[2] + r);
                 buf0[r] = base_pair<RR>(mat, n, (int)(e & 0xffu), (int)(e >> 8), ov);
             }
-            __syncwarp();
+            __syncthreads();
             T* prev = buf0;
             T* cur = buf1;
             for (int k = 3; k < n; ++k) {
                 const uint32_t ck = (poff[k + 1] - poff[k]) / (uint32_t)k;
                 const uint16_t* pt = ptab + poff[k];
                 const T* row = mat + (k - 1) * n;
-                for (uint32_t r = lane; r < ck; r += 32) {
+                for (uint32_t r = tid; r < ck; r += nt) {
                     uint32_t e = __ldg(pt + r);
                     T acc = RR::mul(row[e >> 12], prev[e & 0xfffu], ov);
                     int i = 1;
@@ -329,7 +314,7 @@ __global__ void __launch_bounds__(256) sz_batch_smem_kernel(const typename R::T*
                     }
                     cur[r] = acc;
                 }
-                __syncwarp();
+                __syncthreads();
                 T* t = prev;
                 prev = cur;
                 cur = t;
@@ -342,22 +327,22 @@ __global__ void __launch_bounds__(256) sz_batch_smem_kernel(const typename R::T*
         } else {
             last_layer = run(R{});
         }
-        if (__any_sync(0xffffffffu, ov)) {
-            if (lane == 0) {
-                atomicOr(status, 1);
-                out[b] = R::zero();
+        if (ov) atomicOr(&flag, 1);
+        __syncthreads();
+        if (tid == 0) {
+            T total = R::zero();
+            if (!(flag & 1)) {
+                const T* last = mat + (n - 1) * n;
+                total = R::mul(last[0], last_layer[n - 1], ov);
+                for (int j = 1; j < n; ++j) total = R::mac(total, last[j], last_layer[n - 1 - j], ov);
             }
-        } else if (lane == 0) {
-            const T* last = mat + (n - 1) * n;
-            T total = R::mul(last[0], last_layer[n - 1], ov);
-            for (int j = 1; j < n; ++j) total = R::mac(total, last[j], last_layer[n - 1 - j], ov);
-            if (ov) {
+            if ((flag & 1) || ov) {
                 atomicOr(status, 1);
                 total = R::zero();
             }
             out[b] = total;
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 

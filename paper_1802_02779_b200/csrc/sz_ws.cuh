@@ -57,7 +57,7 @@ constexpr int kWsEnd = -1;
 
 // Window width D and ring depth per element size (shared memory <= 227 KB;
 // what the ring leaves is L1 for the low-source gathers).
-__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 14 : 15; }
+__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 17 : 17; }
 template <int ELEM>
 struct WsGeom {
     static constexpr int NSG = ELEM == 16 ? 4 : 8;  // stages per group ring (power of two)
@@ -260,7 +260,7 @@ __device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, co
         return ws_low<RR, M>(e, src, row_low, B2, ov);
         PL_WS_CASE(1) PL_WS_CASE(2) PL_WS_CASE(3) PL_WS_CASE(4) PL_WS_CASE(5) PL_WS_CASE(6) PL_WS_CASE(7)
         PL_WS_CASE(8) PL_WS_CASE(9) PL_WS_CASE(10) PL_WS_CASE(11) PL_WS_CASE(12) PL_WS_CASE(13) PL_WS_CASE(14)
-        PL_WS_CASE(15)
+        PL_WS_CASE(15) PL_WS_CASE(16) PL_WS_CASE(17)
 #undef PL_WS_CASE
     }
     return RR::zero();
@@ -287,17 +287,19 @@ __device__ __forceinline__ T ws_stage_terms(T acc, const WsSmem<T>& sm, const T*
     return acc;
 }
 
-// Consumer group g's share of one tile: chunks g, g + G, g + 2G, ... Each of
+// Consumer group g's share of one tile: chunks c0g, c0g + G, ... (chunks are
+// dealt to groups round-robin over the CTA's whole tile sequence, so tiles of
+// a single chunk alternate between groups). Each of
 // its chunks takes ceil(f / FS) consecutive stages of the group's own ring;
 // `seq` is the group's running stage counter (stage seq % NSG, use seq / NSG).
 template <class RR, class T>
 __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTile& t, const T* __restrict__ src,
                                                 const T* __restrict__ coef, const uint64_t* __restrict__ sbase_pad,
                                                 const uint32_t* __restrict__ qt, T* __restrict__ cur, int g, int j,
-                                                uint32_t& seq, bool& ov) {
+                                                uint32_t c_first, uint32_t& seq, bool& ov) {
     constexpr int NSG = WsSmem<T>::NSG;
     const int m = t.m, f = t.f;
-    uint32_t c = (uint32_t)g;
+    uint32_t c = c_first;
     uint32_t e_next = 0;  // qtab prefetch one chunk ahead (a global load)
     if (m >= 1 && c < t.nchunks) e_next = __ldg(qt + min(t.q0 + c * kWsChunk + j, t.q1 - 1));
     for (; c < t.nchunks; c += kWsGroups) {
@@ -365,11 +367,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (warp == kWsConsumerWarps) {
         // ------------------------------------------------------------ producer
         uint32_t seqg[kWsGroups] = {};
+        uint32_t gchunk = 0;  // running chunk counter over the tile sequence
         for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
             // lane l holds the base of stream tile F \ {F_l}
             const uint64_t my_base = lane < t.f ? ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2) : 0;
-            int g = 0;
+            int g = (int)(gchunk % kWsGroups);
             for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == kWsGroups) ? 0 : g + 1) {
                 const uint32_t c0 = t.q0 + c * kWsChunk;
                 const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     if (lane < nl) bulk_g2s(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s));
                 }
             }
+            gchunk += t.nchunks;
         }
     } else {
         // ------------------------------------------------------------ consumers
@@ -397,11 +401,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         bool use_checked = false;
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
-        uint32_t seq = 0;
+        uint32_t seq = 0, gchunk = 0;
         for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
-            // skip tiles with no chunk for this group (no stages either)
-            if ((uint32_t)g >= t.nchunks) continue;
+            // this group's first chunk of the tile; skip tiles with none (no stages either)
+            const uint32_t c_first = (uint32_t)((g - (int)(gchunk % kWsGroups) + kWsGroups) % kWsGroups);
+            gchunk += t.nchunks;
+            if (c_first >= t.nchunks) continue;
             __syncwarp();
             if (lane < t.f) {
                 coef[lane] = row[ws_high_col((uint32_t)F, lane, D)];
@@ -412,12 +418,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const T* src = prev + t.src_base;
             if constexpr (R::kChecked) {
                 if (use_checked) {
-                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
                 } else {
-                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
                 }
             } else {
-                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, seq, ov);
+                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
             }
         }
         if (ov) atomicOr(status, 1);
