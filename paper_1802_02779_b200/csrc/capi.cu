@@ -146,9 +146,8 @@ constexpr int kRegsMaxOrder = 5;  // n = 6 spills in registers; it runs in the s
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
-    const size_t smem = (size_t)kRegsThreads * N * N * sizeof(T);
     auto kern = pl::sz_batch_regs_kernel<R, N, kRegsThreads>;
-    PL_CUDA(set_smem_once(kern, smem));
+    const size_t smem = 0;
     const int64_t blocks = (count + kRegsThreads - 1) / kRegsThreads;
     kern<<<(unsigned)blocks, kRegsThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, status);
     PL_CUDA(cudaGetLastError());

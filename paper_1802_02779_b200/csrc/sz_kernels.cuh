@@ -104,7 +104,25 @@ __device__ __forceinline__ typename R::T base_pair(const typename R::T* a, int n
 
 // ---------------------------------------------------------------- n <= 6
 
-__host__ __device__ constexpr int popc_c(int x) { return x == 0 ? 0 : (x & 1) + popc_c(x >> 1); }
+// Iterative (inlinable) bit helpers: with the mask loops fully unrolled they
+// fold to constants, so every memo index and matrix index is static and the
+// whole DP stays in registers.
+__host__ __device__ __forceinline__ constexpr int popc_c(int x) {
+    int c = 0;
+    for (int i = 0; i < 16; ++i) c += (x >> i) & 1;
+    return c;
+}
+__host__ __device__ __forceinline__ constexpr int ctz_c(int x) {
+    for (int i = 0; i < 16; ++i)
+        if ((x >> i) & 1) return i;
+    return 16;
+}
+__host__ __device__ __forceinline__ constexpr int msb_c(int x) {
+    int r = 0;
+    for (int i = 0; i < 16; ++i)
+        if ((x >> i) & 1) r = i;
+    return r;
+}
 
 template <class R, int N>
 __device__ __forceinline__ typename R::T perm_in_registers(const typename R::T* a, bool& ov) {
@@ -116,8 +134,8 @@ __device__ __forceinline__ typename R::T perm_in_registers(const typename R::T* 
 #pragma unroll
         for (int m = 0; m < (1 << N); ++m) {
             if (popc_c(m) == 2) {
-                const int j1 = __ffs(m) - 1;
-                const int j2 = 31 - __clz(m);
+                const int j1 = ctz_c(m);
+                const int j2 = msb_c(m);
                 memo[m] = base_pair<R>(a, N, j1, j2, ov);
             }
         }
@@ -181,56 +199,79 @@ __device__ __forceinline__ bool i64_guard_ok(const long long* a, int n, int stri
 __device__ __forceinline__ unsigned smem_addr_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 // Batched kernel for n <= 5: one thread per matrix, the whole DP in
-// registers. Each CTA stages its chunk of THREADS consecutive matrices into
-// shared memory with one TMA bulk copy (cooperative 8-byte loads for a partial
-// or misaligned chunk); four CTAs per SM overlap one another's copies and
-// arithmetic.
+// registers. Each thread loads its own n*n entries with 16-byte vector loads
+// issued back to back (the sectors its neighbours need arrive in the same L1
+// lines), so a resident CTA keeps its whole chunk in flight with no shared-
+// memory staging or barrier; four CTAs per SM overlap loads and arithmetic.
+template <class T, int E>
+struct MatRegs {
+    T v[E];
+};
+
+template <class T, int E>
+__device__ __forceinline__ void load_matrix(const T* __restrict__ p, MatRegs<T, E>& m) {
+    if constexpr (sizeof(T) == 16) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) m.v[e] = __ldg(reinterpret_cast<const double2*>(p) + e);
+    } else {
+        if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {  // pairs of entries per 16-byte load
+#pragma unroll
+            for (int e = 0; e + 1 < E; e += 2) {
+                const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(p + e));
+                m.v[e] = *reinterpret_cast<const T*>(&w.x);
+                m.v[e + 1] = *reinterpret_cast<const T*>(&w.y);
+            }
+            if (E % 2) m.v[E - 1] = __ldg(p + E - 1);
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) m.v[e] = __ldg(p + e);
+        }
+    }
+}
+
+// Compile-time-indexed form of i64_guard_ok (keeps the matrix in registers).
+template <int N>
+__device__ __forceinline__ bool i64_guard_ok_n(const long long* a) {
+    unsigned long long prod = 1;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        unsigned long long rs = 0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const long long v = a[i * N + j];
+            ok &= v != (long long)0x8000000000000000ULL;
+            const unsigned long long mg = v < 0 ? (unsigned long long)(-v) : (unsigned long long)v;
+            const unsigned long long t = rs + mg;
+            ok &= t >= rs;
+            rs = t;
+        }
+        rs = rs == 0 ? 1 : rs;
+        ok &= __umul64hi(prod, rs) == 0;
+        prod *= rs;
+        ok &= prod < 0x8000000000000000ULL;
+    }
+    return ok;
+}
+
 template <class R, int N, int THREADS>
-__global__ void __launch_bounds__(THREADS, 4) sz_batch_regs_kernel(const typename R::T* __restrict__ a,
+__global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
+    sz_batch_regs_kernel(const typename R::T* __restrict__ a,
                                                                    typename R::T* __restrict__ out, int64_t count,
                                                                    int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int kEnt = N * N;
-    constexpr size_t kChunkBytes = (size_t)THREADS * kEnt * sizeof(T);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bar;
-    T* buf = reinterpret_cast<T*>(smem_raw);
-    const int64_t first = (int64_t)blockIdx.x * THREADS;
-    const int nvalid = count - first < THREADS ? (int)(count - first) : THREADS;
-    const bool bulk = (reinterpret_cast<uintptr_t>(a) & 15u) == 0 && nvalid == THREADS && (kChunkBytes % 16) == 0;
-    if (bulk) {
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr_u32(&bar)) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr_u32(&bar)),
-                         "r"((unsigned)kChunkBytes)
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                    smem_addr_u32(buf)),
-                "l"(a + first * kEnt), "r"((unsigned)kChunkBytes), "r"(smem_addr_u32(&bar))
-                : "memory");
-        }
-        __syncthreads();  // the barrier is initialised before anyone waits on it
-        asm volatile(
-            "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(
-                smem_addr_u32(&bar))
-            : "memory");
-    } else {
-        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a + first * kEnt);
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(buf);
-        const int words = nvalid * kEnt * (int)(sizeof(T) / 8);
-        for (int w = threadIdx.x; w < words; w += THREADS) dst[w] = __ldg(src + w);
-        __syncthreads();
-    }
-    if (threadIdx.x >= nvalid) return;
-    const T* local = buf + threadIdx.x * kEnt;
+    const int64_t b = (int64_t)blockIdx.x * THREADS + threadIdx.x;
+    if (b >= count) return;
+    MatRegs<T, kEnt> m;
+    load_matrix<T, kEnt>(a + b * kEnt, m);
+    const T* local = m.v;
     bool ov = false;
     T v;
     if constexpr (R::kChecked) {
         // int64: the unchecked instantiation when every lane's matrix passes
         // the guard (warp-uniform), checked arithmetic otherwise.
-        const bool ok = i64_guard_ok(local, N);
+        const bool ok = i64_guard_ok_n<N>(local);
         if (__all_sync(__activemask(), ok)) {
             v = perm_in_registers<RI64<false>, N>(local, ov);
         } else {
@@ -243,10 +284,10 @@ __global__ void __launch_bounds__(THREADS, 4) sz_batch_regs_kernel(const typenam
         atomicOr(status, 1);
         v = R::zero();
     }
-    out[first + threadIdx.x] = v;
+    out[b] = v;
 }
 
-// ---------------------------------------------------------------- 7 <= n <= 14
+// ---------------------------------------------------------------- 6 <= n <= 14
 
 // One CTA per matrix at a time (persistent CTAs striding over the batch);
 // the matrix and two layer buffers live in the CTA's shared memory (16 KB at
