@@ -254,6 +254,22 @@ __device__ __forceinline__ bool i64_guard_ok_n(const long long* a) {
     return ok;
 }
 
+template <int N>
+__device__ __forceinline__ bool i64_fits_f64_n(const long long* a) {
+    double prod = 1.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double rs = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const long long v = a[i * N + j];
+            rs += v < 0 ? -(double)v : (double)v;
+        }
+        prod *= rs < 1.0 ? 1.0 : rs;
+    }
+    return prod < 9007199254740992.0;
+}
+
 template <class R, int N, int THREADS>
 __global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
     sz_batch_regs_kernel(const typename R::T* __restrict__ a,
@@ -269,10 +285,17 @@ __global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
     bool ov = false;
     T v;
     if constexpr (R::kChecked) {
-        // int64: the unchecked instantiation when every lane's matrix passes
-        // the guard (warp-uniform), checked arithmetic otherwise.
+        // int64, warp-uniform choice: exact doubles with FMA when every lane's
+        // guard bound is below 2^53 (see i64_fits_f64), wrapping int64 below
+        // 2^63, checked int64 otherwise.
         const bool ok = i64_guard_ok_n<N>(local);
-        if (__all_sync(__activemask(), ok)) {
+        const unsigned act = __activemask();
+        if (__all_sync(act, ok && i64_fits_f64_n<N>(local))) {
+            double dv[kEnt];
+#pragma unroll
+            for (int e = 0; e < kEnt; ++e) dv[e] = (double)local[e];
+            v = (T)perm_in_registers<RF64<true>, N>(dv, ov);
+        } else if (__all_sync(act, ok)) {
             v = perm_in_registers<RI64<false>, N>(local, ov);
         } else {
             v = perm_in_registers<R, N>(local, ov);
@@ -289,6 +312,75 @@ __global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
 
 // ---------------------------------------------------------------- 6 <= n <= 14
 
+// Guard bound for the exact-in-double shortcut: every sub-permanent and partial
+// sum of an integer matrix is bounded by prod_i max(1, sum_j |a_ij|); below 2^53
+// all of them are integers representable in a double and an FMA of exact
+// integers is exact, so the FP64 pipe reproduces int64 arithmetic bit for bit.
+__device__ __forceinline__ bool i64_fits_f64(const long long* a, int n) {
+    double prod = 1.0;
+    for (int i = 0; i < n; ++i) {
+        double rs = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const long long v = a[i * n + j];
+            rs += v < 0 ? -(double)v : (double)v;  // |entries| < 2^53 below, so this is exact or already over
+        }
+        prod *= rs < 1.0 ? 1.0 : rs;
+    }
+    return prod < 9007199254740992.0;  // 2^53 (double rounding only ever overestimates here)
+}
+
+// The layer DP of one matrix held in shared memory (see sz_batch_smem_kernel).
+template <class RR, class TT>
+__device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, int n,
+                                             const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff,
+                                             bool& ov) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const uint32_t c2 = poff[3] - poff[2];
+    for (uint32_t r = tid; r < c2; r += nt) {
+        const uint32_t e = __ldg(ptab + poff[2] + r);
+        buf0[r] = base_pair<RR>(mat, n, (int)(e & 0xffu), (int)(e >> 8), ov);
+    }
+    __syncthreads();
+    TT* prev = buf0;
+    TT* cur = buf1;
+    for (int k = 3; k < n; ++k) {
+        const uint32_t ck = (poff[k + 1] - poff[k]) / (uint32_t)k;
+        const uint16_t* pt = ptab + poff[k];
+        const TT* row = mat + (k - 1) * n;
+        for (uint32_t r = tid; r < ck; r += nt) {
+            uint32_t e = __ldg(pt + r);
+            TT acc = RR::mul(row[e >> 12], prev[e & 0xfffu], ov);
+            int i = 1;
+            for (; i + 4 <= k; i += 4) {
+                const uint32_t e0 = __ldg(pt + (i + 0) * ck + r), e1 = __ldg(pt + (i + 1) * ck + r);
+                const uint32_t e2 = __ldg(pt + (i + 2) * ck + r), e3 = __ldg(pt + (i + 3) * ck + r);
+                acc = RR::mac(acc, row[e0 >> 12], prev[e0 & 0xfffu], ov);
+                acc = RR::mac(acc, row[e1 >> 12], prev[e1 & 0xfffu], ov);
+                acc = RR::mac(acc, row[e2 >> 12], prev[e2 & 0xfffu], ov);
+                acc = RR::mac(acc, row[e3 >> 12], prev[e3 & 0xfffu], ov);
+            }
+            for (; i < k; ++i) {
+                e = __ldg(pt + i * ck + r);
+                acc = RR::mac(acc, row[e >> 12], prev[e & 0xfffu], ov);
+            }
+            cur[r] = acc;
+        }
+        __syncthreads();
+        TT* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    return prev;
+}
+
+template <class RR, class TT>
+__device__ __forceinline__ TT smem_top(const TT* mat, const TT* last_layer, int n, bool& ov) {
+    const TT* last = mat + (n - 1) * n;
+    TT total = RR::mul(last[0], last_layer[n - 1], ov);
+    for (int j = 1; j < n; ++j) total = RR::mac(total, last[j], last_layer[n - 1 - j], ov);
+    return total;
+}
+
 // One CTA per matrix at a time (persistent CTAs striding over the batch);
 // the matrix and two layer buffers live in the CTA's shared memory (16 KB at
 // n = 12, so ~14 CTAs share an SM). The predecessor structure is the same for
@@ -297,6 +389,9 @@ __global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
 //   layer 2:  ptab[off[2] + r]           = j1 | j2 << 8       (r = j1 + C(j2, 2))
 //   layer k:  ptab[off[k] + i*C(n,k) + r] = rank(S \ {s_i}) | s_i << 12
 // with s_i the i-th element of the r-th k-subset in colex order, ascending.
+// Integer matrices take one of three exact paths per matrix: doubles with FMA
+// when the guard bound is below 2^53, wrapping int64 below 2^63, checked int64
+// otherwise.
 template <class R>
 __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
                                                             typename R::T* __restrict__ out, int64_t count,
@@ -305,7 +400,7 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
                                                             int32_t* __restrict__ status) {
     using T = typename R::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int flag;
+    __shared__ int flag, mode;
     T* mat = reinterpret_cast<T*>(smem_raw);
     T* buf0 = mat + ((n * n + 1) & ~1);
     T* buf1 = buf0 + ((maxc + 1) & ~1);
@@ -317,66 +412,34 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
         if (tid == 0) flag = 0;
         __syncthreads();
         bool ov = false;
-        bool use_checked = false;
+        T total = R::zero();
         if constexpr (R::kChecked) {
-            if (tid == 0) flag = i64_guard_ok(reinterpret_cast<const long long*>(mat), n) ? 0 : 2;
-            __syncthreads();
-            use_checked = flag == 2;
-        }
-        auto run = [&](auto ring) {
-            using RR = decltype(ring);
-            const uint32_t c2 = poff[3] - poff[2];
-            for (uint32_t r = tid; r < c2; r += nt) {
-                const uint32_t e = __ldg(ptab + poff[2] + r);
-                buf0[r] = base_pair<RR>(mat, n, (int)(e & 0xffu), (int)(e >> 8), ov);
+            if (tid == 0) {
+                const long long* m = reinterpret_cast<const long long*>(mat);
+                mode = i64_fits_f64(m, n) ? 0 : (i64_guard_ok(m, n) ? 1 : 2);
             }
             __syncthreads();
-            T* prev = buf0;
-            T* cur = buf1;
-            for (int k = 3; k < n; ++k) {
-                const uint32_t ck = (poff[k + 1] - poff[k]) / (uint32_t)k;
-                const uint16_t* pt = ptab + poff[k];
-                const T* row = mat + (k - 1) * n;
-                for (uint32_t r = tid; r < ck; r += nt) {
-                    uint32_t e = __ldg(pt + r);
-                    T acc = RR::mul(row[e >> 12], prev[e & 0xfffu], ov);
-                    int i = 1;
-                    for (; i + 4 <= k; i += 4) {
-                        const uint32_t e0 = __ldg(pt + (i + 0) * ck + r), e1 = __ldg(pt + (i + 1) * ck + r);
-                        const uint32_t e2 = __ldg(pt + (i + 2) * ck + r), e3 = __ldg(pt + (i + 3) * ck + r);
-                        acc = RR::mac(acc, row[e0 >> 12], prev[e0 & 0xfffu], ov);
-                        acc = RR::mac(acc, row[e1 >> 12], prev[e1 & 0xfffu], ov);
-                        acc = RR::mac(acc, row[e2 >> 12], prev[e2 & 0xfffu], ov);
-                        acc = RR::mac(acc, row[e3 >> 12], prev[e3 & 0xfffu], ov);
-                    }
-                    for (; i < k; ++i) {
-                        e = __ldg(pt + i * ck + r);
-                        acc = RR::mac(acc, row[e >> 12], prev[e & 0xfffu], ov);
-                    }
-                    cur[r] = acc;
-                }
+            if (mode == 0) {
+                double* dm = reinterpret_cast<double*>(mat);
+                for (int e = tid; e < n * n; e += nt) dm[e] = (double)mat[e];
                 __syncthreads();
-                T* t = prev;
-                prev = cur;
-                cur = t;
+                const double* last = smem_dp<RF64<true>>(dm, reinterpret_cast<double*>(buf0),
+                                                         reinterpret_cast<double*>(buf1), n, ptab, poff, ov);
+                if (tid == 0) total = (T)smem_top<RF64<true>>(dm, last, n, ov);
+            } else if (mode == 1) {
+                const T* last = smem_dp<RI64<false>>(mat, buf0, buf1, n, ptab, poff, ov);
+                if (tid == 0) total = smem_top<RI64<false>>(mat, last, n, ov);
+            } else {
+                const T* last = smem_dp<R>(mat, buf0, buf1, n, ptab, poff, ov);
+                if (ov) atomicOr(&flag, 1);
+                __syncthreads();
+                if (tid == 0 && !(flag & 1)) total = smem_top<R>(mat, last, n, ov);
             }
-            return prev;
-        };
-        const T* last_layer;
-        if constexpr (R::kChecked) {
-            last_layer = use_checked ? run(R{}) : run(RI64<false>{});
         } else {
-            last_layer = run(R{});
+            const T* last = smem_dp<R>(mat, buf0, buf1, n, ptab, poff, ov);
+            if (tid == 0) total = smem_top<R>(mat, last, n, ov);
         }
-        if (ov) atomicOr(&flag, 1);
-        __syncthreads();
         if (tid == 0) {
-            T total = R::zero();
-            if (!(flag & 1)) {
-                const T* last = mat + (n - 1) * n;
-                total = R::mul(last[0], last_layer[n - 1], ov);
-                for (int j = 1; j < n; ++j) total = R::mac(total, last[j], last_layer[n - 1 - j], ov);
-            }
             if ((flag & 1) || ov) {
                 atomicOr(status, 1);
                 total = R::zero();

@@ -225,9 +225,32 @@ __device__ __forceinline__ uint64_t ws_stream_base(uint32_t F, int l, int m, int
 
 // ---------------------------------------------------------------- consumer math
 
+// Low-source gathers: the tile's source region is re-read for the whole life of
+// the tile, so its lines are kept in L2 with an evict-last policy.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+template <class T>
+__device__ __forceinline__ T ldg_keep(const T* p, uint64_t pol) {
+    if constexpr (sizeof(T) == 16) {
+        double2 v;
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n"
+                     : "=d"(v.x), "=d"(v.y)
+                     : "l"(p), "l"(pol));
+        return *reinterpret_cast<T*>(&v);
+    } else {
+        unsigned long long v;
+        asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;\n" : "=l"(v) : "l"(p), "l"(pol));
+        return *reinterpret_cast<T*>(&v);
+    }
+}
+
 template <class RR, int M, class T>
 __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const T* __restrict__ row_low,
-                                    const uint2* __restrict__ B2, bool& ov) {
+                                    const uint2* __restrict__ B2, uint64_t pol, bool& ov) {
     uint32_t V = e & ((1u << kQtabShift) - 1);
     uint32_t Q = e >> kQtabShift, P = 0;
     int sv[M];
@@ -244,7 +267,7 @@ __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const
     }
     T x[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x[i] = __ldg(src + pr[i]);
+    for (int i = 0; i < M; ++i) x[i] = ldg_keep(src + pr[i], pol);
     T acc = RR::mul(row_low[sv[0]], x[0], ov);
 #pragma unroll
     for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[sv[i]], x[i], ov);
@@ -253,11 +276,11 @@ __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const
 
 template <class RR, class T>
 __device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, const T* row_low, const uint2* B2,
-                                             bool& ov) {
+                                             uint64_t pol, bool& ov) {
     switch (m) {
 #define PL_WS_CASE(M) \
     case M:           \
-        return ws_low<RR, M>(e, src, row_low, B2, ov);
+        return ws_low<RR, M>(e, src, row_low, B2, pol, ov);
         PL_WS_CASE(1) PL_WS_CASE(2) PL_WS_CASE(3) PL_WS_CASE(4) PL_WS_CASE(5) PL_WS_CASE(6) PL_WS_CASE(7)
         PL_WS_CASE(8) PL_WS_CASE(9) PL_WS_CASE(10) PL_WS_CASE(11) PL_WS_CASE(12) PL_WS_CASE(13) PL_WS_CASE(14)
         PL_WS_CASE(15) PL_WS_CASE(16) PL_WS_CASE(17)
@@ -299,6 +322,7 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
                                                 uint32_t c_first, uint32_t& seq, bool& ov) {
     constexpr int NSG = WsSmem<T>::NSG;
     const int m = t.m, f = t.f;
+    const uint64_t keep = l2_evict_last_policy();
     uint32_t c = c_first;
     uint32_t e_next = 0;  // qtab prefetch one chunk ahead (a global load)
     if (m >= 1 && c < t.nchunks) e_next = __ldg(qt + min(t.q0 + c * kWsChunk + j, t.q1 - 1));
@@ -312,7 +336,7 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
         if (m >= 1 && c + kWsGroups < t.nchunks) e_next = __ldg(qt + min(c0 + kWsGroups * kWsChunk + j, t.q1 - 1));
         bool lov = false;
         T acc = RR::zero();
-        if (m >= 1) acc = ws_low_dispatch<RR>(m, e, src, sm.row_low, sm.B2, lov);
+        if (m >= 1) acc = ws_low_dispatch<RR>(m, e, src, sm.row_low, sm.B2, keep, lov);
         for (int l0 = 0; l0 < f; l0 += kWsFS, ++seq) {
             const int nl = min(kWsFS, f - l0);
             int pads[kWsFS];
