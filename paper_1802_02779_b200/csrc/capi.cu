@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -259,12 +260,18 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
 // (C(D, D/2) entries) fits in shared memory, but leaving >= 10 high columns so
 // a layer has enough tiles (>= 2^10 high masks) to keep every SM busy.
 int tile_window(size_t elem, int n) {
+    static const int override_d = [] {
+        const char* e = std::getenv("PL_WS_WINDOW");  // tuning/debug override of the window width
+        return e ? std::atoi(e) : 0;
+    }();
+    if (override_d > 0) return std::max(1, std::min({override_d, pl::ws_window((int)elem), n - 1}));
     return std::max(1, std::min(pl::ws_window((int)elem), n - 10));
 }
 
 struct Qtab {
     uint32_t* qtab = nullptr;
     uint32_t* offs = nullptr;
+    uint2* binom_pairs = nullptr;  // [i * 35 + s] = (C(s, i), C(s, i - 1)), shared by every D
 };
 
 // qtab[offs[m] + q] for window D on the current device, built once (host
@@ -292,6 +299,12 @@ pl_status get_qtab(int D, Qtab* out) {
         tab[offs[__builtin_popcount(mask)] + r] = mask | (r1 << pl::kQtabShift);
     }
     Qtab q;
+    std::vector<uint2> bp(pl::kBinomDim * pl::kBinomDim);
+    for (int i = 0; i < pl::kBinomDim; ++i)
+        for (int sc = 0; sc < pl::kBinomDim; ++sc)
+            bp[i * pl::kBinomDim + sc] = make_uint2((uint32_t)pl::binom_u64(sc, i), i >= 1 ? (uint32_t)pl::binom_u64(sc, i - 1) : 0u);
+    PL_CUDA(cudaMalloc(&q.binom_pairs, bp.size() * sizeof(uint2)));
+    PL_CUDA(cudaMemcpy(q.binom_pairs, bp.data(), bp.size() * sizeof(uint2), cudaMemcpyHostToDevice));
     PL_CUDA(cudaMalloc(&q.qtab, tab.size() * sizeof(uint32_t)));
     PL_CUDA(cudaMalloc(&q.offs, offs.size() * sizeof(uint32_t)));
     PL_CUDA(cudaMemcpy(q.qtab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -333,7 +346,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     PL_CUDA(set_smem_once(kern, smem));
     kern<<<num_sms(), pl::kWsThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                                   static_cast<T*>(cur), r0, r1, F0, F1, q.qtab, q.offs,
-                                                  guard, status);
+                                                  q.binom_pairs, guard, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, uint32_t F0, uint32_t F1,
                  const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
-                 const int32_t* __restrict__ guard, int32_t* __restrict__ status) {
+                 const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
+                 int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -373,10 +374,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* row = a + (size_t)(k - 1) * n;
 
-    for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) {
-        const int i = e / kBinomDim, s = e % kBinomDim;
-        sm.B2[e] = make_uint2((uint32_t)binom_u64(s, i), i >= 1 ? (uint32_t)binom_u64(s, i - 1) : 0u);
-    }
+    for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) sm.B2[e] = __ldg(&binom_pairs[e]);
     for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
     if (threadIdx.x == 0) {
         for (int s = 0; s < kWsGroups * NSG; ++s) {
