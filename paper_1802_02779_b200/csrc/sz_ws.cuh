@@ -50,7 +50,9 @@ constexpr int kWsGroupWarps = 8;
 constexpr int kWsGroups = 2;
 constexpr int kWsConsumerWarps = kWsGroupWarps * kWsGroups;
 constexpr int kWsThreads = 32 * (1 + kWsConsumerWarps);
-constexpr int kWsChunk = 32 * kWsGroupWarps;  // CH: outputs per chunk (one per thread of a group)
+constexpr int kWsLanes = 32 * kWsGroupWarps;   // consumer threads per group
+constexpr int kWsPer = 2;                      // outputs per consumer thread per chunk (independent chains)
+constexpr int kWsChunk = kWsLanes * kWsPer;    // CH: outputs per chunk
 constexpr int kWsFS = 4;                      // stream segments per ring stage
 constexpr int kQtabShift = 17;                // qtab entry: mask(V) | rank(V \ {min V}) << 17
 constexpr int kWsEnd = -1;
@@ -60,7 +62,7 @@ constexpr int kWsEnd = -1;
 __host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 17 : 17; }
 template <int ELEM>
 struct WsGeom {
-    static constexpr int NSG = ELEM == 16 ? 4 : 8;  // stages per group ring (power of two)
+    static constexpr int NSG = ELEM == 16 ? 2 : 4;  // stages per group ring (power of two)
 };
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size_t(15); }
@@ -324,19 +326,34 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
     const int m = t.m, f = t.f;
     const uint64_t keep = l2_evict_last_policy();
     uint32_t c = c_first;
-    uint32_t e_next = 0;  // qtab prefetch one chunk ahead (a global load)
-    if (m >= 1 && c < t.nchunks) e_next = __ldg(qt + min(t.q0 + c * kWsChunk + j, t.q1 - 1));
+    // each thread owns outputs j and j + kWsLanes of every chunk: two independent
+    // accumulation chains; qtab entries are prefetched one chunk ahead
+    uint32_t e_next[kWsPer] = {};
+    if (m >= 1 && c < t.nchunks) {
+#pragma unroll
+        for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(t.q0 + c * kWsChunk + j + p * kWsLanes, t.q1 - 1));
+    }
     for (; c < t.nchunks; c += kWsGroups) {
         const uint32_t c0 = t.q0 + c * kWsChunk;
         const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
         // Lanes past the tile end compute a duplicate of its last output
         // (no divergence); only their store and overflow flag are dropped.
-        const bool valid = (uint32_t)j < len;
-        const uint32_t e = e_next;
-        if (m >= 1 && c + kWsGroups < t.nchunks) e_next = __ldg(qt + min(c0 + kWsGroups * kWsChunk + j, t.q1 - 1));
-        bool lov = false;
-        T acc = RR::zero();
-        if (m >= 1) acc = ws_low_dispatch<RR>(m, e, src, sm.row_low, sm.B2, keep, lov);
+        uint32_t e[kWsPer];
+#pragma unroll
+        for (int p = 0; p < kWsPer; ++p) e[p] = e_next[p];
+        if (m >= 1 && c + kWsGroups < t.nchunks) {
+#pragma unroll
+            for (int p = 0; p < kWsPer; ++p)
+                e_next[p] = __ldg(qt + min(c0 + kWsGroups * kWsChunk + j + p * kWsLanes, t.q1 - 1));
+        }
+        bool lov[kWsPer];
+        T acc[kWsPer];
+#pragma unroll
+        for (int p = 0; p < kWsPer; ++p) {
+            lov[p] = false;
+            acc[p] = RR::zero();
+            if (m >= 1) acc[p] = ws_low_dispatch<RR>(m, e[p], src, sm.row_low, sm.B2, keep, lov[p]);
+        }
         for (int l0 = 0; l0 < f; l0 += kWsFS, ++seq) {
             const int nl = min(kWsFS, f - l0);
             int pads[kWsFS];
@@ -346,13 +363,19 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
             }
             const int s = (int)(seq % NSG);
             mbar_wait(sm.full_bar(g, s), (seq / NSG) & 1u);
-            acc = ws_stage_terms<RR>(acc, sm, coef, g, s, l0, nl, pads, j, m == 0 && l0 == 0, lov);
+#pragma unroll
+            for (int p = 0; p < kWsPer; ++p)
+                acc[p] = ws_stage_terms<RR>(acc[p], sm, coef, g, s, l0, nl, pads, j + p * kWsLanes, m == 0 && l0 == 0,
+                                            lov[p]);
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
         }
-        if (valid) {
-            cur[t.cur_base + c0 + j] = acc;
-            ov |= lov;
+#pragma unroll
+        for (int p = 0; p < kWsPer; ++p) {
+            if ((uint32_t)(j + p * kWsLanes) < len) {
+                cur[t.cur_base + c0 + j + p * kWsLanes] = acc[p];
+                ov |= lov[p];  // duplicates past the tile end never report
+            }
         }
     }
 }
