@@ -344,7 +344,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(set_smem_once(kern, smem));
-    kern<<<num_sms(), pl::kWsThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
+    kern<<<num_sms(), pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                                   static_cast<T*>(cur), r0, r1, F0, F1, q.qtab, q.offs,
                                                   q.binom_pairs, guard, status);
     PL_CUDA(cudaGetLastError());

@@ -47,9 +47,7 @@
 namespace pl {
 
 constexpr int kWsGroupWarps = 8;
-constexpr int kWsGroups = 2;
-constexpr int kWsConsumerWarps = kWsGroupWarps * kWsGroups;
-constexpr int kWsThreads = 32 * (1 + kWsConsumerWarps);
+constexpr int kWsMaxGroups = 3;
 constexpr int kWsLanes = 32 * kWsGroupWarps;   // consumer threads per group
 constexpr int kWsPer = 2;                      // outputs per consumer thread per chunk (independent chains)
 constexpr int kWsChunk = kWsLanes * kWsPer;    // CH: outputs per chunk
@@ -60,9 +58,15 @@ constexpr int kWsEnd = -1;
 // Window width D and ring depth per element size (shared memory <= 227 KB;
 // what the ring leaves is L1 for the low-source gathers).
 __host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 17 : 17; }
+// Consumer groups per CTA: three for 8-byte elements (more warps to hide the
+// low-source gather latency); two for complex, whose arithmetic needs the
+// registers.
 template <int ELEM>
 struct WsGeom {
-    static constexpr int NSG = ELEM == 16 ? 2 : 4;  // stages per group ring (power of two)
+    static constexpr int G = ELEM == 16 ? 2 : 3;             // consumer groups
+    static constexpr int NSG = ELEM == 16 ? 2 : 4;           // stages per group ring (power of two)
+    static constexpr int kConsumerWarps = kWsGroupWarps * G;
+    static constexpr int kThreads = 32 * (1 + kConsumerWarps);
 };
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size_t(15); }
@@ -70,6 +74,8 @@ __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size
 template <class T>
 struct WsSmem {
     static constexpr int NSG = WsGeom<(int)sizeof(T)>::NSG;
+    static constexpr int G = WsGeom<(int)sizeof(T)>::G;
+    static constexpr int CW = WsGeom<(int)sizeof(T)>::kConsumerWarps;
     static constexpr size_t kSlot = round16(sizeof(T) * kWsChunk + 16) / sizeof(T);  // elements per segment slot
     uint2* B2;        // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
     T* row_low;       // [32]   a(k-1, v), v < D
@@ -80,8 +86,8 @@ struct WsSmem {
 
     __host__ __device__ static size_t bytes() {
         return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) +
-               round16(sizeof(T) * kMaxOrder * (kWsConsumerWarps + 1)) + round16(8 * 2 * kWsGroups * NSG) +
-               round16((size_t)kWsGroups * NSG * kWsFS * kSlot * sizeof(T));
+               round16(sizeof(T) * kMaxOrder * (CW + 1)) + round16(8 * 2 * G * NSG) +
+               round16((size_t)G * NSG * kWsFS * kSlot * sizeof(T));
     }
     __device__ explicit WsSmem(unsigned char* base) {
         size_t off = 0;
@@ -92,11 +98,11 @@ struct WsSmem {
         };
         B2 = reinterpret_cast<uint2*>(take(sizeof(uint2) * kBinomDim * kBinomDim));
         row_low = reinterpret_cast<T*>(take(sizeof(T) * 32));
-        coef = reinterpret_cast<T*>(take(sizeof(T) * kMaxOrder * (kWsConsumerWarps + 1)));
-        uint64_t* bars = reinterpret_cast<uint64_t*>(take(8 * 2 * kWsGroups * NSG));
+        coef = reinterpret_cast<T*>(take(sizeof(T) * kMaxOrder * (CW + 1)));
+        uint64_t* bars = reinterpret_cast<uint64_t*>(take(8 * 2 * G * NSG));
         full = bars;
-        empty = bars + kWsGroups * NSG;
-        stage = reinterpret_cast<T*>(take((size_t)kWsGroups * NSG * kWsFS * kSlot * sizeof(T)));
+        empty = bars + G * NSG;
+        stage = reinterpret_cast<T*>(take((size_t)G * NSG * kWsFS * kSlot * sizeof(T)));
     }
     __device__ T* slot(int g, int s, int li) const { return stage + (((size_t)g * NSG + s) * kWsFS + li) * kSlot; }
     __device__ uint64_t* full_bar(int g, int s) const { return full + g * NSG + s; }
@@ -333,7 +339,8 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
 #pragma unroll
         for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(t.q0 + c * kWsChunk + j + p * kWsLanes, t.q1 - 1));
     }
-    for (; c < t.nchunks; c += kWsGroups) {
+    constexpr int G = WsSmem<T>::G;
+    for (; c < t.nchunks; c += G) {
         const uint32_t c0 = t.q0 + c * kWsChunk;
         const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
         // Lanes past the tile end compute a duplicate of its last output
@@ -341,10 +348,10 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
         uint32_t e[kWsPer];
 #pragma unroll
         for (int p = 0; p < kWsPer; ++p) e[p] = e_next[p];
-        if (m >= 1 && c + kWsGroups < t.nchunks) {
+        if (m >= 1 && c + G < t.nchunks) {
 #pragma unroll
             for (int p = 0; p < kWsPer; ++p)
-                e_next[p] = __ldg(qt + min(c0 + kWsGroups * kWsChunk + j + p * kWsLanes, t.q1 - 1));
+                e_next[p] = __ldg(qt + min(c0 + G * kWsChunk + j + p * kWsLanes, t.q1 - 1));
         }
         bool lov[kWsPer];
         T acc[kWsPer];
@@ -383,7 +390,7 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
 // ---------------------------------------------------------------- kernel
 
 template <class R, class RU>
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 1)
     sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, uint32_t F0, uint32_t F1,
                  const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
@@ -392,7 +399,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint64_t sbase_sh[kWsConsumerWarps + 1][kMaxOrder];  // per-warp stream bases (8-byte pads)
+    __shared__ uint64_t sbase_sh[kWsGroupWarps * kWsMaxGroups + 1][kMaxOrder];  // per-warp stream bases (8-byte pads)
+    constexpr int G = WsSmem<T>::G;
+    constexpr int CW = WsSmem<T>::CW;
     const WsSmem<T> sm(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* row = a + (size_t)(k - 1) * n;
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) sm.B2[e] = __ldg(&binom_pairs[e]);
     for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kWsGroups * NSG; ++s) {
+        for (int s = 0; s < G * NSG; ++s) {
             mbar_init(&sm.full[s], 1);               // producer's arrive.expect_tx
             mbar_init(&sm.empty[s], kWsGroupWarps);  // the owning group's warps
         }
@@ -409,16 +418,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     __syncthreads();
 
     uint32_t cursor = F0 + blockIdx.x;
-    if (warp == kWsConsumerWarps) {
+    if (warp == CW) {
         // ------------------------------------------------------------ producer
-        uint32_t seqg[kWsGroups] = {};
+        uint32_t seqg[G] = {};
         uint32_t gchunk = 0;  // running chunk counter over the tile sequence
         for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
             // lane l holds the base of stream tile F \ {F_l}
             const uint64_t my_base = lane < t.f ? ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2) : 0;
-            int g = (int)(gchunk % kWsGroups);
-            for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == kWsGroups) ? 0 : g + 1) {
+            int g = (int)(gchunk % G);
+            for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == G) ? 0 : g + 1) {
                 const uint32_t c0 = t.q0 + c * kWsChunk;
                 const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
                 for (int l0 = 0; l0 < t.f; l0 += kWsFS) {
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
             // this group's first chunk of the tile; skip tiles with none (no stages either)
-            const uint32_t c_first = (uint32_t)((g - (int)(gchunk % kWsGroups) + kWsGroups) % kWsGroups);
+            const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
             gchunk += t.nchunks;
             if (c_first >= t.nchunks) continue;
             __syncwarp();
