@@ -259,6 +259,68 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
 // Low-window width D of the tiled layer kernel: as wide as one tile source
 // (C(D, D/2) entries) fits in shared memory, but leaving >= 10 high columns so
 // a layer has enough tiles (>= 2^10 high masks) to keep every SM busy.
+// Tile schedule of one layer range for the layer kernel: the valid tiles F of
+// [r0, r1) in increasing order, each dealt to the CTA with the least load so
+// far (load = chunks of kWsChunk outputs, at least one per tile). Device
+// layout: offsets[grid + 1] then the concatenated per-CTA lists. Cached per
+// (device, n, k, D, r0, r1, grid).
+pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, const uint32_t** out) {
+    static std::mutex mu;
+    static std::map<std::vector<uint64_t>, uint32_t*> cache;
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    const std::vector<uint64_t> key = {(uint64_t)dev, (uint64_t)n, (uint64_t)k, (uint64_t)D, r0, r1, (uint64_t)grid};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return PL_OK;
+    }
+    const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
+    const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
+    std::vector<std::vector<uint32_t>> lists(grid);
+    std::vector<std::pair<uint64_t, int>> heap;  // (load, cta), min-heap
+    for (int b = 0; b < grid; ++b) heap.push_back({0, b});
+    auto cmp = [](const std::pair<uint64_t, int>& x, const std::pair<uint64_t, int>& y) { return x > y; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (uint32_t F = F0; F <= F1; ++F) {
+        const int f = __builtin_popcount(F), m = k - f;
+        if (m < 0 || m > D) continue;
+        uint64_t base = 0;
+        int l = 1;
+        for (uint32_t ff = F; ff; ff &= ff - 1, ++l) base += pl::binom_u64(D + __builtin_ctz(ff), m + l);
+        const uint64_t len = pl::binom_u64(D, m);
+        const uint64_t lo = std::max(base, r0), hi = std::min(base + len, r1);
+        if (hi <= lo) continue;
+        const uint64_t chunks = (hi - lo + pl::kWsChunk - 1) / pl::kWsChunk;
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto& top = heap.back();
+        lists[top.second].push_back(F);
+        top.first += chunks;
+        std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    std::vector<uint32_t> flat(grid + 1, 0);
+    for (int b = 0; b < grid; ++b) flat[b + 1] = flat[b] + (uint32_t)lists[b].size();
+    for (int b = 0; b < grid; ++b) flat.insert(flat.end(), lists[b].begin(), lists[b].end());
+    uint32_t* d = nullptr;
+    PL_CUDA(cudaMalloc(&d, flat.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMemcpy(d, flat.data(), flat.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    cache[key] = d;
+    *out = d;
+    return PL_OK;
+}
+
+// L2 hint mode of the layer kernel (bits 0-1 stream policy: 0 none, 1 evict-first beyond
+// the reuse horizon, 2 + evict-last within it; bit 2 evict-first output stores; bits 8-15
+// log2 of the horizon in tiles). PL_WS_HINTS overrides it for tuning.
+uint32_t ws_hints() {
+    static const uint32_t h = [] {
+        const char* e = std::getenv("PL_WS_HINTS");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0u;
+    }();
+    return h;
+}
+
 int tile_window(size_t elem, int n) {
     static const int override_d = [] {
         const char* e = std::getenv("PL_WS_WINDOW");  // tuning/debug override of the window width
@@ -339,14 +401,15 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     Qtab q;
     pl_status s = get_qtab(D, &q);
     if (s != PL_OK) return s;
-    const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
-    const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
+    const uint32_t* sched = nullptr;
+    s = get_sched(n, k, D, r0, r1, num_sms(), &sched);
+    if (s != PL_OK) return s;
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(set_smem_once(kern, smem));
     kern<<<num_sms(), pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                                                  static_cast<T*>(cur), r0, r1, F0, F1, q.qtab, q.offs,
-                                                  q.binom_pairs, guard, status);
+                                                  static_cast<T*>(cur), r0, r1, sched, q.qtab, q.offs,
+                                                  q.binom_pairs, guard, status, ws_hints());
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

@@ -148,6 +148,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+// Same, with an L2 eviction-priority hint for the source lines.
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
 // A run [start, start + len) of T staged by a 16-byte aligned bulk copy. For
 // 8-byte T the copy starts at the aligned element below (pad = 1 when start
 // is odd) and is rounded up to whole 16-byte units: it may read one element
@@ -178,16 +200,23 @@ struct WsTile {
     uint64_t cur_base, src_base;
 };
 
-// Next valid tile of this CTA's static interleaved share (F with
-// 0 <= k - |F| <= D), or kWsEnd. Every warp walks the same sequence.
-__device__ __forceinline__ int32_t ws_next(uint32_t& cursor, uint32_t F1, int k, int D) {
-    for (;;) {
-        const uint32_t t = cursor;
-        if (t > F1) return kWsEnd;
-        cursor += gridDim.x;
-        const int mm = k - __popc(t);
-        if (mm >= 0 && mm <= D) return (int32_t)t;
-    }
+// Next tile of this CTA's list, or kWsEnd. The host deals the layer's tiles,
+// in increasing F, to the least-loaded CTA (load = chunks), so all CTAs sweep
+// the layer as one tight front and the stream tiles of near high columns are
+// still in L2 when they are re-read. Every warp walks the same list.
+struct WsCursor {
+    const uint32_t* list;
+    uint32_t pos, end;
+};
+
+__device__ __forceinline__ WsCursor ws_cursor(const uint32_t* __restrict__ sched) {
+    const uint32_t* off = sched;
+    return {sched + gridDim.x + 1, __ldg(off + blockIdx.x), __ldg(off + blockIdx.x + 1)};
+}
+
+__device__ __forceinline__ int32_t ws_next(WsCursor& c) {
+    if (c.pos >= c.end) return kWsEnd;
+    return (int32_t)__ldg(c.list + c.pos++);
 }
 
 __device__ __forceinline__ WsTile ws_tile(int32_t F, int k, int D, uint64_t r0, uint64_t r1,
@@ -253,6 +282,18 @@ __device__ __forceinline__ T ldg_keep(const T* p, uint64_t pol) {
         unsigned long long v;
         asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;\n" : "=l"(v) : "l"(p), "l"(pol));
         return *reinterpret_cast<T*>(&v);
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void stg_hint(T* p, const T& v, uint64_t pol) {
+    if constexpr (sizeof(T) == 16) {
+        const double2 d = *reinterpret_cast<const double2*>(&v);
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(d.x), "d"(d.y), "l"(pol)
+                     : "memory");
+    } else {
+        const unsigned long long d = *reinterpret_cast<const unsigned long long*>(&v);
+        asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;\n" ::"l"(p), "l"(d), "l"(pol) : "memory");
     }
 }
 
@@ -327,10 +368,11 @@ template <class RR, class T>
 __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTile& t, const T* __restrict__ src,
                                                 const T* __restrict__ coef, const uint64_t* __restrict__ sbase_pad,
                                                 const uint32_t* __restrict__ qt, T* __restrict__ cur, int g, int j,
-                                                uint32_t c_first, uint32_t& seq, bool& ov) {
+                                                uint32_t c_first, uint32_t& seq, bool& ov, bool store_first) {
     constexpr int NSG = WsSmem<T>::NSG;
     const int m = t.m, f = t.f;
     const uint64_t keep = l2_evict_last_policy();
+    const uint64_t pol_store = l2_evict_first_policy();
     uint32_t c = c_first;
     // each thread owns outputs j and j + kWsLanes of every chunk: two independent
     // accumulation chains; qtab entries are prefetched one chunk ahead
@@ -380,7 +422,10 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
 #pragma unroll
         for (int p = 0; p < kWsPer; ++p) {
             if ((uint32_t)(j + p * kWsLanes) < len) {
-                cur[t.cur_base + c0 + j + p * kWsLanes] = acc[p];
+                if (store_first)
+                    stg_hint(cur + t.cur_base + c0 + j + p * kWsLanes, acc[p], pol_store);
+                else
+                    cur[t.cur_base + c0 + j + p * kWsLanes] = acc[p];
                 ov |= lov[p];  // duplicates past the tile end never report
             }
         }
@@ -392,10 +437,10 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
 template <class R, class RU>
 __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 1)
     sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
-                 typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, uint32_t F0, uint32_t F1,
+                 typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ sched,
                  const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
                  const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
-                 int32_t* __restrict__ status) {
+                 int32_t* __restrict__ status, uint32_t hints) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -417,15 +462,32 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     }
     __syncthreads();
 
-    uint32_t cursor = F0 + blockIdx.x;
+    WsCursor cursor = ws_cursor(sched);
     if (warp == CW) {
         // ------------------------------------------------------------ producer
         uint32_t seqg[G] = {};
         uint32_t gchunk = 0;  // running chunk counter over the tile sequence
-        for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
+        const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
+        for (int32_t F = ws_next(cursor); F != kWsEnd; F = ws_next(cursor)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
             // lane l holds the base of stream tile F \ {F_l}
             const uint64_t my_base = lane < t.f ? ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2) : 0;
+            // and its L2 policy: the next read of tile F' = F \ {F_l} in this layer comes from
+            // F' + 2^h2 (h2 = lowest free high column above F_l); beyond the reuse horizon the
+            // lines are marked evict-first so they do not displace tiles with near reuse.
+            int my_mode = 0;  // 0 plain, 1 evict_first, 2 evict_last
+            if ((hints & 3u) != 0 && lane < t.f) {
+                const int H = n - D;
+                const int h = ws_high_col((uint32_t)F, lane, D) - D;
+                const uint32_t Fp = (uint32_t)F & ~(1u << h);
+                const uint32_t z = ~Fp & ((1u << H) - 1u) & ~((2u << h) - 1u);
+                bool far = true;
+                if (z != 0) {
+                    const int h2 = __ffs(z) - 1;
+                    far = ((1u << h2) - (1u << h)) > (1u << ((hints >> 8) & 31u));
+                }
+                my_mode = far ? 1 : ((hints & 3u) == 2 ? 2 : 0);
+            }
             int g = (int)(gchunk % G);
             for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == G) ? 0 : g + 1) {
                 const uint32_t c0 = t.q0 + c * kWsChunk;
@@ -433,6 +495,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 for (int l0 = 0; l0 < t.f; l0 += kWsFS) {
                     const int nl = min(kWsFS, t.f - l0);
                     const uint64_t base = __shfl_sync(0xffffffffu, my_base, (l0 + lane) & 31);
+                    const int mode = __shfl_sync(0xffffffffu, my_mode, (l0 + lane) & 31);
                     const uint32_t sq = seqg[g]++;
                     const int s = (int)(sq % NSG);
                     mbar_wait(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
@@ -441,7 +504,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                     const unsigned total = __reduce_add_sync(0xffffffffu, seg.bytes);
                     if (lane == 0) mbar_arrive_expect_tx(sm.full_bar(g, s), total);
                     __syncwarp();
-                    if (lane < nl) bulk_g2s(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s));
+                    if (lane < nl) {
+                        if (mode == 0)
+                            bulk_g2s(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s));
+                        else
+                            bulk_g2s_hint(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s),
+                                          mode == 1 ? pol_first : pol_last);
+                    }
                 }
             }
             gchunk += t.nchunks;
@@ -455,8 +524,9 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         bool use_checked = false;
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
+        const bool store_first = (hints & 4u) != 0;
         uint32_t seq = 0, gchunk = 0;
-        for (int32_t F = ws_next(cursor, F1, k, D); F != kWsEnd; F = ws_next(cursor, F1, k, D)) {
+        for (int32_t F = ws_next(cursor); F != kWsEnd; F = ws_next(cursor)) {
             const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
             // this group's first chunk of the tile; skip tiles with none (no stages either)
             const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
@@ -472,12 +542,12 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             const T* src = prev + t.src_base;
             if constexpr (R::kChecked) {
                 if (use_checked) {
-                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
+                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
                 } else {
-                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
+                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
                 }
             } else {
-                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov);
+                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
             }
         }
         if (ov) atomicOr(status, 1);
