@@ -402,14 +402,23 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     pl_status s = get_qtab(D, &q);
     if (s != PL_OK) return s;
     const uint32_t* sched = nullptr;
-    s = get_sched(n, k, D, r0, r1, num_sms(), &sched);
+    static const int team = [] {
+        const char* e = std::getenv("PL_WS_TEAM");  // tuning override: CTAs per tile
+        return e ? std::max(1, std::min(atoi(e), 8)) : 1;
+    }();
+    static const int grid = [] {
+        const char* e = std::getenv("PL_WS_GRID");  // tuning override of the layer-kernel grid
+        const int g = e ? std::max(1, std::min(atoi(e), num_sms())) : num_sms();
+        return std::max(team, g / team * team);
+    }();
+    s = get_sched(n, k, D, r0, r1, grid / team, &sched);
     if (s != PL_OK) return s;
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(set_smem_once(kern, smem));
-    kern<<<num_sms(), pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
+    kern<<<grid, pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                                   static_cast<T*>(cur), r0, r1, sched, q.qtab, q.offs,
-                                                  q.binom_pairs, guard, status, ws_hints());
+                                                  q.binom_pairs, guard, status, ws_hints(), team);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

@@ -9,8 +9,8 @@
 //     rank(S) = rank_D(V) + sum_{l=1..f} C(F_l, m + l),
 // so the k-subsets sharing F form one contiguous colex range, the tile (F, k),
 // of C(D, m) entries indexed by q = rank_D(V). Output q needs
-//   * low terms  S \ {v_i}: inside the tile (F, k-1), a small contiguous
-//     region (<= C(D, D/2) entries) gathered through L1 (__ldg);
+//   * low terms  S \ {v_i}: inside the tile's low source (F, k-1), C(D, m-1)
+//     contiguous entries staged whole in shared memory by one bulk copy;
 //     rank_D(V \ {v_i}) = P_i + Q_i (P_i = sum_{l<i} C(v_l, l),
 //     Q_i = sum_{l>i} C(v_l, l-1)), one paired-binomial lookup per term;
 //   * high terms S \ {F_l}: entry q of the tile (F \ {F_l}, k-1) -> aligned
@@ -19,25 +19,24 @@
 // ascending" is the reference's ascending-j order; the non-FMA rings keep its
 // rounding sequence bit for bit.
 //
-// Schedule. One CTA per SM, persistent. CTA b takes the b-th, (b+G)-th, ...
-// valid tile in increasing F (increasing colex order), so the GPU sweeps each
-// layer front to back and stream tiles of nearby high columns are re-read
-// from L2. Every warp walks the same tile sequence and derives each tile's
-// descriptor itself: there is no per-tile synchronisation at all.
+// Schedule. One CTA per SM, persistent. The host deals the layer's tiles, in
+// increasing F (increasing colex order), to the least-loaded CTA, so the GPU
+// sweeps each layer as one tight front and stream tiles of nearby high columns
+// are re-read from L2.
 //
 // Roles.
-//   last warp, producer  streams the high-term segments of every chunk of CH
-//                        outputs into the owning consumer group's NSG-stage
-//                        shared-memory ring, FS segments per stage, one
-//                        cp.async.bulk per segment, completion by mbarrier
-//                        transaction counts (~160 KB in flight per SM). It is
-//                        the highest warp id: the issue arbiter favours high
-//                        ids over the consumers.
-//   warps 0..15          two consumer groups of 8 warps taking alternate
-//                        chunks, one output per thread: low terms (L1
-//                        gathers), high terms from the group's ring, coalesced
-//                        store. Each group owns its ring, so every waiter is
-//                        at most one mbarrier phase ahead of the producer.
+//   last warp, producer  walks the CTA's tile list. Per tile it builds the
+//                        tile header (bases, clip range, coefficients, stream
+//                        bases: two warp scans, no loops), publishes it with
+//                        the tile's low source in one of NSRC source slots,
+//                        then streams the high-term segments of every chunk of
+//                        CH outputs into the owning consumer group's NSG-stage
+//                        ring, FS segments per stage, one cp.async.bulk per
+//                        segment, completion by mbarrier transaction counts.
+//   consumer warps       G groups of 8 warps taking alternate chunks, two
+//                        outputs per thread: low terms from the source slot,
+//                        high terms from the group's ring, coalesced store.
+//                        They read everything about a tile from its header.
 #pragma once
 
 #include <cstdint>
@@ -47,47 +46,72 @@
 namespace pl {
 
 constexpr int kWsGroupWarps = 8;
-constexpr int kWsMaxGroups = 3;
 constexpr int kWsLanes = 32 * kWsGroupWarps;   // consumer threads per group
 constexpr int kWsPer = 2;                      // outputs per consumer thread per chunk (independent chains)
 constexpr int kWsChunk = kWsLanes * kWsPer;    // CH: outputs per chunk
-constexpr int kWsFS = 4;                      // stream segments per ring stage
-constexpr int kQtabShift = 17;                // qtab entry: mask(V) | rank(V \ {min V}) << 17
+constexpr int kWsMaxHigh = 32;                 // high columns per tile (n - D <= 31)
+constexpr int kQtabShift = 17;                 // qtab entry: mask(V) | rank(V \ {min V}) << 17
 constexpr int kWsEnd = -1;
+constexpr int kWaitHintNs = 20000;             // mbarrier try_wait suspend-time hint
 
-// Window width D and ring depth per element size (shared memory <= 227 KB;
-// what the ring leaves is L1 for the low-source gathers).
-__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 17 : 17; }
-// Consumer groups per CTA: three for 8-byte elements (more warps to hide the
-// low-source gather latency); two for complex, whose arithmetic needs the
-// registers.
+// Low window D per element size: the largest tile source C(D, D/2) must fit a
+// shared-memory slot next to the stage rings (<= 227 KB in all).
+__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 14 : 14; }
+
+// Consumer groups per CTA: three for 8-byte elements, two for complex, whose
+// arithmetic needs the registers.
 template <int ELEM>
 struct WsGeom {
-    static constexpr int G = ELEM == 16 ? 2 : 3;             // consumer groups
-    static constexpr int NSG = ELEM == 16 ? 2 : 4;           // stages per group ring (power of two)
+    static constexpr int G = ELEM == 16 ? 2 : 3;  // consumer groups
+    static constexpr int NSG = 2;                 // stages per group ring (power of two)
+    static constexpr int FS = ELEM == 16 ? 3 : 4; // stream segments per ring stage
+    static constexpr int NSRC = ELEM == 16 ? 2 : 3;  // tile slots (header + low source) in flight
+    // elements per low-source slot: the largest tile source C(D, D/2), plus the
+    // 8-byte alignment pad and round-up of bulk_span
+    static constexpr int kSrcSlot =
+        (int)((binom_u64(ws_window(ELEM), ws_window(ELEM) / 2) + 2 + 16 / ELEM - 1) / (16 / ELEM) * (16 / ELEM));
     static constexpr int kConsumerWarps = kWsGroupWarps * G;
-    static constexpr int kThreads = 32 * (1 + kConsumerWarps);
+    static constexpr int kThreads = 32 * (kConsumerWarps + G + 1);  // consumers, G streamers, publisher
 };
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Tile header, written by the producer into a tile slot before the slot's
+// full barrier completes.
+template <class T>
+struct WsHdr {
+    int32_t m, f;                    // m < 0: end of the CTA's tile list
+    uint32_t q1, nchunks, cb, cs;    // clip end; this CTA's chunks start at cb + i * cs
+    uint64_t cur_base;               // rank of the tile's first output
+    uint32_t qoff, pad_src;          // qtab offset for m; 8-byte alignment pad of the source
+    T coef[kWsMaxHigh];              // a(k-1, F_l)
+    uint64_t sbase[kWsMaxHigh];      // base rank of stream tile (F \ {F_l}, k-1)
+    int32_t mode[kWsMaxHigh];        // L2 policy of stream l (0 plain, 1 evict-first, 2 evict-last)
+};
 
 template <class T>
 struct WsSmem {
     static constexpr int NSG = WsGeom<(int)sizeof(T)>::NSG;
     static constexpr int G = WsGeom<(int)sizeof(T)>::G;
     static constexpr int CW = WsGeom<(int)sizeof(T)>::kConsumerWarps;
+    static constexpr int NSRC = WsGeom<(int)sizeof(T)>::NSRC;
+    static constexpr int kSrcSlot = WsGeom<(int)sizeof(T)>::kSrcSlot;
+    static constexpr int FS = WsGeom<(int)sizeof(T)>::FS;
     static constexpr size_t kSlot = round16(sizeof(T) * kWsChunk + 16) / sizeof(T);  // elements per segment slot
-    uint2* B2;        // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
-    T* row_low;       // [32]   a(k-1, v), v < D
-    T* coef;          // [warps][kMaxOrder]  per-warp a(k-1, F_l) of the warp's current tile
-    uint64_t* full;   // [G][NSG]
-    uint64_t* empty;  // [G][NSG]
-    T* stage;         // [G][NSG][FS][kSlot]
+    uint2* B2;            // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
+    T* row_low;           // [32]   a(k-1, v), v < D
+    uint64_t* full;       // [G][NSG]
+    uint64_t* empty;      // [G][NSG]
+    T* stage;             // [G][NSG][FS][kSlot]
+    uint64_t* src_full;   // [NSRC]
+    uint64_t* src_empty;  // [NSRC]
+    WsHdr<T>* hdr;        // [NSRC]
+    T* src;               // [NSRC][kSrcSlot]  tile low sources X(F, k-1)
 
     __host__ __device__ static size_t bytes() {
-        return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) +
-               round16(sizeof(T) * kMaxOrder * (CW + 1)) + round16(8 * 2 * G * NSG) +
-               round16((size_t)G * NSG * kWsFS * kSlot * sizeof(T));
+        return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) + round16(8 * 2 * G * NSG) +
+               round16((size_t)G * NSG * FS * kSlot * sizeof(T)) + round16(8 * 2 * NSRC) +
+               round16(sizeof(WsHdr<T>) * NSRC) + round16((size_t)NSRC * kSrcSlot * sizeof(T));
     }
     __device__ explicit WsSmem(unsigned char* base) {
         size_t off = 0;
@@ -98,16 +122,18 @@ struct WsSmem {
         };
         B2 = reinterpret_cast<uint2*>(take(sizeof(uint2) * kBinomDim * kBinomDim));
         row_low = reinterpret_cast<T*>(take(sizeof(T) * 32));
-        coef = reinterpret_cast<T*>(take(sizeof(T) * kMaxOrder * (CW + 1)));
         uint64_t* bars = reinterpret_cast<uint64_t*>(take(8 * 2 * G * NSG));
         full = bars;
         empty = bars + G * NSG;
-        stage = reinterpret_cast<T*>(take((size_t)G * NSG * kWsFS * kSlot * sizeof(T)));
+        stage = reinterpret_cast<T*>(take((size_t)G * NSG * FS * kSlot * sizeof(T)));
+        src_full = reinterpret_cast<uint64_t*>(take(8 * 2 * NSRC));
+        src_empty = src_full + NSRC;
+        hdr = reinterpret_cast<WsHdr<T>*>(take(sizeof(WsHdr<T>) * NSRC));
+        src = reinterpret_cast<T*>(take((size_t)NSRC * kSrcSlot * sizeof(T)));
     }
-    __device__ T* slot(int g, int s, int li) const { return stage + (((size_t)g * NSG + s) * kWsFS + li) * kSlot; }
+    __device__ T* slot(int g, int s, int li) const { return stage + (((size_t)g * NSG + s) * FS + li) * kSlot; }
     __device__ uint64_t* full_bar(int g, int s) const { return full + g * NSG + s; }
     __device__ uint64_t* empty_bar(int g, int s) const { return empty + g * NSG + s; }
-    __device__ T* warp_coef(int w) const { return coef + (size_t)w * kMaxOrder; }
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -132,10 +158,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "n"(kWaitHintNs)
+        : "memory");
+}
+
+// Same wait, separate code location (profiles attribute tile-slot waits here).
+__device__ __forceinline__ void mbar_wait_slot(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(kWaitHintNs)
+        : "memory");
+}
+
+// Same wait, separate code location (producer's ring-slot waits).
+__device__ __forceinline__ void mbar_wait_prod(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(kWaitHintNs)
         : "memory");
 }
 
@@ -164,10 +216,27 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     return p;
 }
 
-__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
     return p;
+}
+
+template <class T>
+__device__ __forceinline__ void stg_hint(T* p, const T& v, uint64_t pol) {
+    if constexpr (sizeof(T) == 16) {
+        const double2 d = *reinterpret_cast<const double2*>(&v);
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(d.x), "d"(d.y), "l"(pol)
+                     : "memory");
+    } else {
+        const unsigned long long d = *reinterpret_cast<const unsigned long long*>(&v);
+        asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;\n" ::"l"(p), "l"(d), "l"(pol) : "memory");
+    }
+}
+
+// L2 prefetch of a 16-byte aligned run (no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // A run [start, start + len) of T staged by a 16-byte aligned bulk copy. For
@@ -192,114 +261,37 @@ __device__ __forceinline__ BulkSpan<T> bulk_span(const T* base, uint64_t start, 
     }
 }
 
-// ---------------------------------------------------------------- tiles
+// Inclusive warp prefix sum (lane order).
+__device__ __forceinline__ uint64_t warp_scan_u64(uint64_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
 
-struct WsTile {
-    int32_t F, m, f;
-    uint32_t q0, q1, nchunks;
-    uint64_t cur_base, src_base;
-};
+// ---------------------------------------------------------------- tile list
 
-// Next tile of this CTA's list, or kWsEnd. The host deals the layer's tiles,
-// in increasing F, to the least-loaded CTA (load = chunks), so all CTAs sweep
-// the layer as one tight front and the stream tiles of near high columns are
-// still in L2 when they are re-read. Every warp walks the same list.
+// The CTA's tile list. The host deals the layer's tiles, in increasing F, to
+// the least-loaded team (load = chunks); a team of tP CTAs shares one list and
+// splits every tile's chunks (CTA tp takes chunks tp, tp + tP, ...).
 struct WsCursor {
     const uint32_t* list;
     uint32_t pos, end;
 };
 
-__device__ __forceinline__ WsCursor ws_cursor(const uint32_t* __restrict__ sched) {
+__device__ __forceinline__ WsCursor ws_cursor(const uint32_t* __restrict__ sched, int nteams, int team) {
     const uint32_t* off = sched;
-    return {sched + gridDim.x + 1, __ldg(off + blockIdx.x), __ldg(off + blockIdx.x + 1)};
-}
-
-__device__ __forceinline__ int32_t ws_next(WsCursor& c) {
-    if (c.pos >= c.end) return kWsEnd;
-    return (int32_t)__ldg(c.list + c.pos++);
-}
-
-__device__ __forceinline__ WsTile ws_tile(int32_t F, int k, int D, uint64_t r0, uint64_t r1,
-                                          const uint2* __restrict__ B2) {
-    WsTile t;
-    t.F = F;
-    t.f = __popc((uint32_t)F);
-    t.m = k - t.f;
-    t.cur_base = 0;
-    t.src_base = 0;
-    int l = 1;
-    for (uint32_t ff = (uint32_t)F; ff; ff &= ff - 1, ++l) {
-        const int col = D + __ffs(ff) - 1;
-        const uint2 b = B2[(t.m + l) * kBinomDim + col];
-        t.cur_base += b.x;
-        t.src_base += b.y;
-    }
-    const uint32_t len = B2[t.m * kBinomDim + D].x;
-    t.q0 = r0 > t.cur_base ? (uint32_t)(r0 - t.cur_base) : 0u;
-    t.q1 = (r1 - t.cur_base) < len ? (uint32_t)(r1 - t.cur_base) : len;
-    t.nchunks = t.q1 > t.q0 ? (t.q1 - t.q0 + kWsChunk - 1) / kWsChunk : 0u;
-    return t;
-}
-
-// Column of the l-th (0-based) high element of F.
-__device__ __forceinline__ int ws_high_col(uint32_t F, int l, int D) {
-    for (int i = 0; i < l; ++i) F &= F - 1;
-    return D + __ffs(F) - 1;
-}
-
-// Base rank, in the previous layer, of the stream tile (F \ {F_l}, k-1): the
-// remaining high elements keep the low count m and shift down one position.
-__device__ __forceinline__ uint64_t ws_stream_base(uint32_t F, int l, int m, int D, const uint2* __restrict__ B2) {
-    uint64_t b = 0;
-    int i = 0, p = 1;
-    for (uint32_t ff = F; ff; ff &= ff - 1, ++i) {
-        if (i == l) continue;
-        b += B2[(m + p) * kBinomDim + D + __ffs(ff) - 1].x;
-        ++p;
-    }
-    return b;
+    return {sched + nteams + 1, __ldg(off + team), __ldg(off + team + 1)};
 }
 
 // ---------------------------------------------------------------- consumer math
 
-// Low-source gathers: the tile's source region is re-read for the whole life of
-// the tile, so its lines are kept in L2 with an evict-last policy.
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-    return p;
-}
-
-template <class T>
-__device__ __forceinline__ T ldg_keep(const T* p, uint64_t pol) {
-    if constexpr (sizeof(T) == 16) {
-        double2 v;
-        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n"
-                     : "=d"(v.x), "=d"(v.y)
-                     : "l"(p), "l"(pol));
-        return *reinterpret_cast<T*>(&v);
-    } else {
-        unsigned long long v;
-        asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;\n" : "=l"(v) : "l"(p), "l"(pol));
-        return *reinterpret_cast<T*>(&v);
-    }
-}
-
-template <class T>
-__device__ __forceinline__ void stg_hint(T* p, const T& v, uint64_t pol) {
-    if constexpr (sizeof(T) == 16) {
-        const double2 d = *reinterpret_cast<const double2*>(&v);
-        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(d.x), "d"(d.y), "l"(pol)
-                     : "memory");
-    } else {
-        const unsigned long long d = *reinterpret_cast<const unsigned long long*>(&v);
-        asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;\n" ::"l"(p), "l"(d), "l"(pol) : "memory");
-    }
-}
-
 template <class RR, int M, class T>
 __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const T* __restrict__ row_low,
-                                    const uint2* __restrict__ B2, uint64_t pol, bool& ov) {
+                                    const uint2* __restrict__ B2, bool& ov) {
     uint32_t V = e & ((1u << kQtabShift) - 1);
     uint32_t Q = e >> kQtabShift, P = 0;
     int sv[M];
@@ -316,7 +308,7 @@ __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const
     }
     T x[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x[i] = ldg_keep(src + pr[i], pol);
+    for (int i = 0; i < M; ++i) x[i] = src[pr[i]];  // shared-memory tile source
     T acc = RR::mul(row_low[sv[0]], x[0], ov);
 #pragma unroll
     for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[sv[i]], x[i], ov);
@@ -325,75 +317,52 @@ __device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const
 
 template <class RR, class T>
 __device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, const T* row_low, const uint2* B2,
-                                             uint64_t pol, bool& ov) {
+                                             bool& ov) {
     switch (m) {
 #define PL_WS_CASE(M) \
     case M:           \
-        return ws_low<RR, M>(e, src, row_low, B2, pol, ov);
+        return ws_low<RR, M>(e, src, row_low, B2, ov);
         PL_WS_CASE(1) PL_WS_CASE(2) PL_WS_CASE(3) PL_WS_CASE(4) PL_WS_CASE(5) PL_WS_CASE(6) PL_WS_CASE(7)
         PL_WS_CASE(8) PL_WS_CASE(9) PL_WS_CASE(10) PL_WS_CASE(11) PL_WS_CASE(12) PL_WS_CASE(13) PL_WS_CASE(14)
-        PL_WS_CASE(15) PL_WS_CASE(16) PL_WS_CASE(17)
 #undef PL_WS_CASE
     }
     return RR::zero();
 }
 
-// One ring stage's high terms for output j (a full stage needs no predicates).
-template <class RR, class T>
-__device__ __forceinline__ T ws_stage_terms(T acc, const WsSmem<T>& sm, const T* __restrict__ coef, int g, int s,
-                                            int l0, int nl, const int* __restrict__ pads, int j, bool init_first,
-                                            bool& ov) {
-    const T* st = sm.slot(g, s, 0) + j;
-    if (nl == kWsFS && !init_first) {
-#pragma unroll
-        for (int li = 0; li < kWsFS; ++li) acc = RR::mac(acc, coef[l0 + li], st[li * WsSmem<T>::kSlot + pads[li]], ov);
-        return acc;
-    }
-#pragma unroll
-    for (int li = 0; li < kWsFS; ++li) {
-        if (li < nl) {
-            const T x = st[li * WsSmem<T>::kSlot + pads[li]];
-            acc = (init_first && li == 0) ? RR::mul(coef[l0 + li], x, ov) : RR::mac(acc, coef[l0 + li], x, ov);
-        }
-    }
-    return acc;
-}
-
-// Consumer group g's share of one tile: chunks c0g, c0g + G, ... (chunks are
-// dealt to groups round-robin over the CTA's whole tile sequence, so tiles of
-// a single chunk alternate between groups). Each of
-// its chunks takes ceil(f / FS) consecutive stages of the group's own ring;
+// Consumer group g's share of one tile: its chunks c_first, c_first + G, ...
+// (chunks are dealt to groups round-robin over the CTA's whole tile sequence).
+// Each chunk takes ceil(f / FS) consecutive stages of the group's own ring;
 // `seq` is the group's running stage counter (stage seq % NSG, use seq / NSG).
 template <class RR, class T>
-__device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTile& t, const T* __restrict__ src,
-                                                const T* __restrict__ coef, const uint64_t* __restrict__ sbase_pad,
+__device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr<T>& h, const T* __restrict__ src,
                                                 const uint32_t* __restrict__ qt, T* __restrict__ cur, int g, int j,
-                                                uint32_t c_first, uint32_t& seq, bool& ov, bool store_first) {
+                                                uint32_t c_first, uint32_t& seq, bool& ov, uint32_t hints) {
     constexpr int NSG = WsSmem<T>::NSG;
-    const int m = t.m, f = t.f;
-    const uint64_t keep = l2_evict_last_policy();
+    constexpr int G = WsSmem<T>::G;
+    constexpr int FS = WsSmem<T>::FS;
+    const int m = h.m, f = h.f;
+    const uint32_t q1 = h.q1, nchunks = h.nchunks, cb = h.cb, cs = h.cs;
+    const uint64_t cur_base = h.cur_base;
     const uint64_t pol_store = l2_evict_first_policy();
     uint32_t c = c_first;
     // each thread owns outputs j and j + kWsLanes of every chunk: two independent
     // accumulation chains; qtab entries are prefetched one chunk ahead
     uint32_t e_next[kWsPer] = {};
-    if (m >= 1 && c < t.nchunks) {
+    if (m >= 1) {
 #pragma unroll
-        for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(t.q0 + c * kWsChunk + j + p * kWsLanes, t.q1 - 1));
+        for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(cb + c * cs + j + p * kWsLanes, q1 - 1));
     }
-    constexpr int G = WsSmem<T>::G;
-    for (; c < t.nchunks; c += G) {
-        const uint32_t c0 = t.q0 + c * kWsChunk;
-        const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
+    for (; c < nchunks; c += G) {
+        const uint32_t c0 = cb + c * cs;
+        const uint32_t len = min((uint32_t)kWsChunk, q1 - c0);
         // Lanes past the tile end compute a duplicate of its last output
         // (no divergence); only their store and overflow flag are dropped.
         uint32_t e[kWsPer];
 #pragma unroll
         for (int p = 0; p < kWsPer; ++p) e[p] = e_next[p];
-        if (m >= 1 && c + G < t.nchunks) {
+        if (m >= 1 && c + G < nchunks) {
 #pragma unroll
-            for (int p = 0; p < kWsPer; ++p)
-                e_next[p] = __ldg(qt + min(c0 + G * kWsChunk + j + p * kWsLanes, t.q1 - 1));
+            for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(c0 + G * cs + j + p * kWsLanes, q1 - 1));
         }
         bool lov[kWsPer];
         T acc[kWsPer];
@@ -401,31 +370,65 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsTil
         for (int p = 0; p < kWsPer; ++p) {
             lov[p] = false;
             acc[p] = RR::zero();
-            if (m >= 1) acc[p] = ws_low_dispatch<RR>(m, e[p], src, sm.row_low, sm.B2, keep, lov[p]);
+            if (m >= 1 && !(hints & 128u)) acc[p] = ws_low_dispatch<RR>(m, e[p], src, sm.row_low, sm.B2, lov[p]);  // 128: probe
         }
-        for (int l0 = 0; l0 < f; l0 += kWsFS, ++seq) {
-            const int nl = min(kWsFS, f - l0);
-            int pads[kWsFS];
+        for (int l0 = 0; l0 < f; l0 += FS, ++seq) {
+            const int nl = min(FS, f - l0);
+            int pads[FS];
 #pragma unroll
-            for (int li = 0; li < kWsFS; ++li) {
-                pads[li] = sizeof(T) == 16 || li >= nl ? 0 : (int)((sbase_pad[l0 + li] + c0) & 1u);
+            for (int li = 0; li < FS; ++li) {
+                pads[li] = sizeof(T) == 16 || li >= nl ? 0 : (int)((h.sbase[l0 + li] + c0) & 1u);
             }
             const int s = (int)(seq % NSG);
             mbar_wait(sm.full_bar(g, s), (seq / NSG) & 1u);
+            // read the stage into registers and hand the slot back before the math,
+            // so the producer refills it one compute phase earlier
+            T xs[kWsPer][FS];
+            const T* st = sm.slot(g, s, 0) + j;
+            if (nl == FS) {
 #pragma unroll
-            for (int p = 0; p < kWsPer; ++p)
-                acc[p] = ws_stage_terms<RR>(acc[p], sm, coef, g, s, l0, nl, pads, j + p * kWsLanes, m == 0 && l0 == 0,
-                                            lov[p]);
+                for (int p = 0; p < kWsPer; ++p)
+#pragma unroll
+                    for (int li = 0; li < FS; ++li) xs[p][li] = st[p * kWsLanes + li * WsSmem<T>::kSlot + pads[li]];
+            } else {
+#pragma unroll
+                for (int p = 0; p < kWsPer; ++p)
+#pragma unroll
+                    for (int li = 0; li < FS; ++li)
+                        xs[p][li] = li < nl ? st[p * kWsLanes + li * WsSmem<T>::kSlot + pads[li]] : RR::zero();
+            }
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
+            const bool init_first = m == 0 && l0 == 0;
+            if (hints & 64u) {  // timing probe: no high-term math
+#pragma unroll
+                for (int p = 0; p < kWsPer; ++p)
+#pragma unroll
+                    for (int li = 0; li < FS; ++li) acc[p] = RR::add(acc[p], xs[p][li], lov[p]);
+                continue;
+            }
+#pragma unroll
+            for (int p = 0; p < kWsPer; ++p) {
+                if (nl == FS && !init_first) {
+#pragma unroll
+                    for (int li = 0; li < FS; ++li) acc[p] = RR::mac(acc[p], h.coef[l0 + li], xs[p][li], lov[p]);
+                } else {
+#pragma unroll
+                    for (int li = 0; li < FS; ++li) {
+                        if (li < nl)
+                            acc[p] = (init_first && li == 0) ? RR::mul(h.coef[l0 + li], xs[p][li], lov[p])
+                                                             : RR::mac(acc[p], h.coef[l0 + li], xs[p][li], lov[p]);
+                    }
+                }
+            }
         }
 #pragma unroll
         for (int p = 0; p < kWsPer; ++p) {
             if ((uint32_t)(j + p * kWsLanes) < len) {
-                if (store_first)
-                    stg_hint(cur + t.cur_base + c0 + j + p * kWsLanes, acc[p], pol_store);
+                if (hints & 4u)
+                    stg_hint(cur + cur_base + c0 + j + p * kWsLanes, acc[p], pol_store);
                 else
-                    cur[t.cur_base + c0 + j + p * kWsLanes] = acc[p];
+                    cur[cur_base + c0 + j + p * kWsLanes] = acc[p];
                 ov |= lov[p];  // duplicates past the tile end never report
             }
         }
@@ -440,71 +443,162 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ sched,
                  const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
                  const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
-                 int32_t* __restrict__ status, uint32_t hints) {
+                 int32_t* __restrict__ status, uint32_t hints, int tP) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint64_t sbase_sh[kWsGroupWarps * kWsMaxGroups + 1][kMaxOrder];  // per-warp stream bases (8-byte pads)
+    constexpr int NSRC = WsSmem<T>::NSRC;
     constexpr int G = WsSmem<T>::G;
     constexpr int CW = WsSmem<T>::CW;
+    constexpr int FS = WsSmem<T>::FS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ T row_sh[kMaxOrder];
+    __shared__ uint32_t qoff_sh[kMaxOrder + 2];
     const WsSmem<T> sm(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* row = a + (size_t)(k - 1) * n;
 
     for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) sm.B2[e] = __ldg(&binom_pairs[e]);
     for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
+    for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
+    for (int v = threadIdx.x; v <= D; v += blockDim.x) qoff_sh[v] = __ldg(qtab_off + v);
     if (threadIdx.x == 0) {
         for (int s = 0; s < G * NSG; ++s) {
-            mbar_init(&sm.full[s], 1);               // producer's arrive.expect_tx
-            mbar_init(&sm.empty[s], kWsGroupWarps);  // the owning group's warps
+            mbar_init(&sm.full[s], 1);               // the group's streamer: arrive.expect_tx
+            mbar_init(&sm.empty[s], kWsGroupWarps);  // the group's consumer warps
+        }
+        for (int s = 0; s < NSRC; ++s) {
+            mbar_init(&sm.src_full[s], 1);        // publisher: arrive.expect_tx
+            mbar_init(&sm.src_empty[s], CW + G);  // every consumer and streamer warp, once per tile
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    WsCursor cursor = ws_cursor(sched);
-    if (warp == CW) {
-        // ------------------------------------------------------------ producer
-        uint32_t seqg[G] = {};
-        uint32_t gchunk = 0;  // running chunk counter over the tile sequence
-        const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
-        for (int32_t F = ws_next(cursor); F != kWsEnd; F = ws_next(cursor)) {
-            const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
-            // lane l holds the base of stream tile F \ {F_l}
-            const uint64_t my_base = lane < t.f ? ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2) : 0;
-            // and its L2 policy: the next read of tile F' = F \ {F_l} in this layer comes from
-            // F' + 2^h2 (h2 = lowest free high column above F_l); beyond the reuse horizon the
-            // lines are marked evict-first so they do not displace tiles with near reuse.
-            int my_mode = 0;  // 0 plain, 1 evict_first, 2 evict_last
-            if ((hints & 3u) != 0 && lane < t.f) {
-                const int H = n - D;
-                const int h = ws_high_col((uint32_t)F, lane, D) - D;
-                const uint32_t Fp = (uint32_t)F & ~(1u << h);
-                const uint32_t z = ~Fp & ((1u << H) - 1u) & ~((2u << h) - 1u);
-                bool far = true;
-                if (z != 0) {
-                    const int h2 = __ffs(z) - 1;
-                    far = ((1u << h2) - (1u << h)) > (1u << ((hints >> 8) & 31u));
-                }
-                my_mode = far ? 1 : ((hints & 3u) == 2 ? 2 : 0);
+    const int nteams = (int)gridDim.x / tP;
+    const int tp = (int)blockIdx.x / nteams;
+    if (warp == CW + G) {
+        // ------------------------------------------------------------ publisher
+        // Walks the CTA's tile list; per tile with work for this CTA it builds
+        // the header (two warp scans, no loops) and stages the low source into
+        // the next tile slot; a terminal header ends the sequence.
+        WsCursor lst = ws_cursor(sched, nteams, (int)blockIdx.x % nteams);
+        const int H = n - D;
+        uint32_t pub = 0;
+        uint32_t F_next = lst.pos < lst.end ? __ldg(lst.list + lst.pos) : 0u;
+        for (; lst.pos < lst.end;) {
+            const uint32_t F = F_next;
+            ++lst.pos;
+            if (lst.pos < lst.end) F_next = __ldg(lst.list + lst.pos);
+            const int f = __popc(F), m = k - f;
+            // lane h stands for high column D + h; set lanes are F's elements in
+            // increasing order, idx = position among them
+            const bool set = (F >> lane) & 1u;
+            const int idx = __popc(F & ((1u << lane) - 1u));
+            uint64_t x = 0, y = 0;
+            if (set) {
+                const uint2 b = sm.B2[(m + idx + 1) * kBinomDim + D + lane];  // (C(D+h, m+l), C(D+h, m+l-1))
+                x = b.x;
+                y = b.y;
             }
-            int g = (int)(gchunk % G);
-            for (uint32_t c = 0; c < t.nchunks; ++c, g = (g + 1 == G) ? 0 : g + 1) {
-                const uint32_t c0 = t.q0 + c * kWsChunk;
-                const uint32_t len = min((uint32_t)kWsChunk, t.q1 - c0);
-                for (int l0 = 0; l0 < t.f; l0 += kWsFS) {
-                    const int nl = min(kWsFS, t.f - l0);
-                    const uint64_t base = __shfl_sync(0xffffffffu, my_base, (l0 + lane) & 31);
-                    const int mode = __shfl_sync(0xffffffffu, my_mode, (l0 + lane) & 31);
-                    const uint32_t sq = seqg[g]++;
+            const uint64_t ix = warp_scan_u64(x), iy = warp_scan_u64(y);
+            const uint64_t cur_base = __shfl_sync(0xffffffffu, ix, 31);
+            const uint64_t src_base = __shfl_sync(0xffffffffu, iy, 31);
+            // stream tile (F \ {F_idx}, k-1): elements below keep their position,
+            // elements above shift down one
+            const uint64_t sbase = (ix - x) + (src_base - iy);
+            const uint32_t len = sm.B2[m * kBinomDim + D].x;
+            const uint32_t q0 = r0 > cur_base ? (uint32_t)(r0 - cur_base) : 0u;
+            const uint32_t q1 = (r1 - cur_base) < len ? (uint32_t)(r1 - cur_base) : len;
+            const uint32_t total = q1 > q0 ? (q1 - q0 + kWsChunk - 1) / kWsChunk : 0u;
+            const uint32_t nchunks = total > (uint32_t)tp ? (total - tp + tP - 1) / tP : 0u;
+            if (nchunks == 0) continue;
+
+            const int ss = (int)(pub % NSRC);
+            mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
+            ++pub;
+            WsHdr<T>& h = sm.hdr[ss];
+            if (set) {
+                h.coef[idx] = row_sh[D + lane];
+                h.sbase[idx] = sbase;
+                int mode = 0;
+                if ((hints & 3u) != 0) {
+                    // the next read of stream tile F' = F \ {h} in this layer comes from
+                    // F' + 2^h2 (h2 = lowest free high column above h); beyond the reuse
+                    // horizon its lines are marked evict-first
+                    const uint32_t Fp = F & ~(1u << lane);
+                    const uint32_t z = ~Fp & ((1u << H) - 1u) & ~((2u << lane) - 1u);
+                    bool far = true;
+                    if (z != 0) far = ((1u << (__ffs(z) - 1)) - (1u << lane)) > (1u << ((hints >> 8) & 31u));
+                    mode = far ? 1 : ((hints & 3u) == 2 ? 2 : 0);
+                }
+                h.mode[idx] = mode;
+            }
+            if (lane == 0) {
+                h.m = m;
+                h.f = f;
+                h.q1 = q1;
+                h.nchunks = nchunks;
+                h.cb = q0 + tp * kWsChunk;
+                h.cs = tP * kWsChunk;
+                h.cur_base = cur_base;
+                h.qoff = qoff_sh[m];
+                h.pad_src = sizeof(T) == 16 ? 0u : (uint32_t)(src_base & 1u);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const uint32_t slen = m >= 1 ? sm.B2[(m - 1) * kBinomDim + D].x : 0u;
+                const BulkSpan<T> sp = slen ? bulk_span(prev, src_base, slen) : BulkSpan<T>{prev, 0u, 0};
+                mbar_arrive_expect_tx(&sm.src_full[ss], sp.bytes);
+                if (sp.bytes) bulk_g2s(sm.src + (size_t)ss * WsSmem<T>::kSrcSlot, sp.src, sp.bytes, &sm.src_full[ss]);
+            }
+            __syncwarp();
+        }
+        const int ss = (int)(pub % NSRC);
+        mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
+        if (lane == 0) {
+            sm.hdr[ss].m = kWsEnd;
+            __threadfence_block();
+            mbar_arrive(&sm.src_full[ss]);
+        }
+    } else if (warp >= CW) {
+        // ------------------------------------------------------------ streamer of group g
+        // Streams the high-term segments of group g's chunks into its ring.
+        const int g = warp - CW;
+        const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
+        uint32_t sq = 0, gchunk = 0;
+        for (uint32_t ts = 0;; ++ts) {
+            const int ss = (int)(ts % NSRC);
+            mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
+            const WsHdr<T>& h = sm.hdr[ss];
+            if (h.m < 0) break;
+            const int f = h.f;
+            const uint32_t nchunks = h.nchunks, cb = h.cb, cs = h.cs, q1 = h.q1;
+            uint64_t base = 0;
+            int mode = 0;
+            const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
+            gchunk += nchunks;
+            for (uint32_t c = c_first; c < nchunks; c += G) {
+                const uint32_t c0 = cb + c * cs;
+                const uint32_t clen = min((uint32_t)kWsChunk, q1 - c0);
+                for (int l0 = 0; l0 < f; l0 += FS, ++sq) {
+                    const int nl = min(FS, f - l0);
                     const int s = (int)(sq % NSG);
-                    mbar_wait(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
-                    BulkSpan<T> seg{prev, 0u, 0};
-                    if (lane < nl) seg = bulk_span(prev, base + c0, len);
-                    const unsigned total = __reduce_add_sync(0xffffffffu, seg.bytes);
-                    if (lane == 0) mbar_arrive_expect_tx(sm.full_bar(g, s), total);
-                    __syncwarp();
                     if (lane < nl) {
+                        base = h.sbase[l0 + lane];
+                        mode = h.mode[l0 + lane];
+                    }
+                    mbar_wait_prod(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
+                    BulkSpan<T> seg{prev, 0u, 0};
+                    if (lane < nl && !(hints & 32u)) seg = bulk_span(prev, base + c0, clen);  // 32: timing probe
+                    unsigned bytes;
+                    if constexpr (sizeof(T) == 16)
+                        bytes = (hints & 32u) ? 0u : (unsigned)nl * clen * 16u;
+                    else
+                        bytes = __reduce_add_sync(0xffffffffu, seg.bytes);
+                    if (lane == 0) mbar_arrive_expect_tx(sm.full_bar(g, s), bytes);
+                    __syncwarp();
+                    if (lane < nl && seg.bytes) {
                         if (mode == 0)
                             bulk_g2s(sm.slot(g, s, lane), seg.src, seg.bytes, sm.full_bar(g, s));
                         else
@@ -513,42 +607,41 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                     }
                 }
             }
-            gchunk += t.nchunks;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.src_empty[ss]);
         }
     } else {
         // ------------------------------------------------------------ consumers
         const int g = warp / kWsGroupWarps;
         const int j = (warp % kWsGroupWarps) * 32 + lane;
-        T* coef = sm.warp_coef(warp);
-        uint64_t* sb = sbase_sh[warp];
         bool use_checked = false;
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
-        const bool store_first = (hints & 4u) != 0;
         uint32_t seq = 0, gchunk = 0;
-        for (int32_t F = ws_next(cursor); F != kWsEnd; F = ws_next(cursor)) {
-            const WsTile t = ws_tile(F, k, D, r0, r1, sm.B2);
-            // this group's first chunk of the tile; skip tiles with none (no stages either)
+        for (uint32_t ts = 0;; ++ts) {
+            const int ss = (int)(ts % NSRC);
+            mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
+            const WsHdr<T>& h = sm.hdr[ss];
+            if (h.m < 0) break;
+            // this group's first chunk of the tile (a group with none takes no stages)
+            const uint32_t nchunks = h.nchunks;
             const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
-            gchunk += t.nchunks;
-            if (c_first >= t.nchunks) continue;
-            __syncwarp();
-            if (lane < t.f) {
-                coef[lane] = row[ws_high_col((uint32_t)F, lane, D)];
-                if constexpr (sizeof(T) != 16) sb[lane] = ws_stream_base((uint32_t)F, lane, t.m, D, sm.B2);
-            }
-            __syncwarp();
-            const uint32_t* qt = qtab + qtab_off[t.m];
-            const T* src = prev + t.src_base;
-            if constexpr (R::kChecked) {
-                if (use_checked) {
-                    ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
+            gchunk += nchunks;
+            if (c_first < nchunks) {
+                const uint32_t* qt = qtab + h.qoff;
+                const T* src = sm.src + (size_t)ss * WsSmem<T>::kSrcSlot + h.pad_src;
+                if constexpr (R::kChecked) {
+                    if (use_checked) {
+                        ws_consume_tile<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
+                    } else {
+                        ws_consume_tile<RU>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
+                    }
                 } else {
-                    ws_consume_tile<RU>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
+                    ws_consume_tile<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
                 }
-            } else {
-                ws_consume_tile<R>(sm, t, src, coef, sb, qt, cur, g, j, c_first, seq, ov, store_first);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.src_empty[ss]);
         }
         if (ov) atomicOr(status, 1);
     }
