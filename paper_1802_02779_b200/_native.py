@@ -8,10 +8,11 @@ point fails with ``PL_ERR_NODEVICE`` when no CUDA device is present.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libpermlab_b200.so"
+LIB_PATH = Path(os.environ.get("PL_NATIVE_LIB", PKG_DIR / "libpermlab_b200.so"))  # override: tuning variants
 GEN_PATH = PKG_DIR / "libpermlab_gen.so"
 
 PL_OK, PL_ERR_ARG, PL_ERR_LIMIT, PL_ERR_OVERFLOW, PL_ERR_NOMEM, PL_ERR_CUDA, PL_ERR_NODEVICE = range(7)

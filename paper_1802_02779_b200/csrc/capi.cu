@@ -264,12 +264,12 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
 // far (load = chunks of kWsChunk outputs, at least one per tile). Device
 // layout: offsets[grid + 1] then the concatenated per-CTA lists. Cached per
 // (device, n, k, D, r0, r1, grid).
-pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, const uint32_t** out) {
+pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int chunk, const uint32_t** out) {
     static std::mutex mu;
     static std::map<std::vector<uint64_t>, uint32_t*> cache;
     int dev = 0;
     PL_CUDA(cudaGetDevice(&dev));
-    const std::vector<uint64_t> key = {(uint64_t)dev, (uint64_t)n, (uint64_t)k, (uint64_t)D, r0, r1, (uint64_t)grid};
+    const std::vector<uint64_t> key = {(uint64_t)dev, (uint64_t)n, (uint64_t)k, (uint64_t)D, r0, r1, (uint64_t)grid, (uint64_t)chunk};
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
@@ -283,16 +283,28 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, con
     for (int b = 0; b < grid; ++b) heap.push_back({0, b});
     auto cmp = [](const std::pair<uint64_t, int>& x, const std::pair<uint64_t, int>& y) { return x > y; };
     std::make_heap(heap.begin(), heap.end(), cmp);
+    static const auto C = [] {
+        std::vector<uint64_t> c(pl::kBinomDim * pl::kBinomDim);
+        for (int a = 0; a < pl::kBinomDim; ++a)
+            for (int b = 0; b < pl::kBinomDim; ++b) c[a * pl::kBinomDim + b] = pl::binom_u64(a, b);
+        return c;
+    }();
+    auto binom = [&](int a, int b) { return C[a * pl::kBinomDim + b]; };
+    const bool whole = r0 == 0 && r1 == binom(n, k);
     for (uint32_t F = F0; F <= F1; ++F) {
         const int f = __builtin_popcount(F), m = k - f;
         if (m < 0 || m > D) continue;
-        uint64_t base = 0;
-        int l = 1;
-        for (uint32_t ff = F; ff; ff &= ff - 1, ++l) base += pl::binom_u64(D + __builtin_ctz(ff), m + l);
-        const uint64_t len = pl::binom_u64(D, m);
-        const uint64_t lo = std::max(base, r0), hi = std::min(base + len, r1);
+        const uint64_t len = binom(D, m);
+        uint64_t lo = 0, hi = len;
+        if (!whole) {
+            uint64_t base = 0;
+            int l = 1;
+            for (uint32_t ff = F; ff; ff &= ff - 1, ++l) base += binom(D + __builtin_ctz(ff), m + l);
+            lo = std::max(base, r0);
+            hi = std::min(base + len, r1);
+        }
         if (hi <= lo) continue;
-        const uint64_t chunks = (hi - lo + pl::kWsChunk - 1) / pl::kWsChunk;
+        const uint64_t chunks = (hi - lo + chunk - 1) / chunk;
         std::pop_heap(heap.begin(), heap.end(), cmp);
         auto& top = heap.back();
         lists[top.second].push_back(F);
@@ -312,11 +324,12 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, con
 
 // L2 hint mode of the layer kernel (bits 0-1 stream policy: 0 none, 1 evict-first beyond
 // the reuse horizon, 2 + evict-last within it; bit 2 evict-first output stores; bits 8-15
-// log2 of the horizon in tiles). PL_WS_HINTS overrides it for tuning.
+// log2 of the horizon in tiles; bits 4+ are timing probes, see sz_ws.cuh). Default: far
+// streams and output stores evict-first, horizon 2^7 tiles. PL_WS_HINTS overrides it.
 uint32_t ws_hints() {
     static const uint32_t h = [] {
         const char* e = std::getenv("PL_WS_HINTS");
-        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0u;
+        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0x705u;
     }();
     return h;
 }
@@ -331,14 +344,18 @@ int tile_window(size_t elem, int n) {
 }
 
 struct Qtab {
-    uint32_t* qtab = nullptr;
-    uint32_t* offs = nullptr;
+    uint4* ltab = nullptr;         // low-term table, 16 u16 entries (two uint4) per low subset
+    uint32_t* offs = nullptr;      // offs[m]: first uint4 of the m-subsets
     uint2* binom_pairs = nullptr;  // [i * 35 + s] = (C(s, i), C(s, i - 1)), shared by every D
 };
 
-// qtab[offs[m] + q] for window D on the current device, built once (host
-// enumeration of the 2^D low masks, copied to device memory).
+// Low-term table for window D on the current device, built once on the host.
+// For the m-subset V of [0, D) of colex rank q, entry i (ascending v_i) is
+//     rank_D(V \ {v_i}) | v_i << 12
+// at u16 index 16 * (offs[m] / 2 + q) + i: the consumer reads its output's
+// whole list with one or two 16-byte loads instead of unranking V.
 pl_status get_qtab(int D, Qtab* out) {
+    static_assert(pl::kWsLtabRankBits == 12, "ltab entry layout");
     static std::mutex mu;
     static std::map<std::pair<int, int>, Qtab> cache;
     int dev = 0;
@@ -349,16 +366,25 @@ pl_status get_qtab(int D, Qtab* out) {
         *out = it->second;
         return PL_OK;
     }
+    if (D > 14) return fail(PL_ERR_LIMIT, "layer window %d exceeds the low-term table layout (<= 14)", D);
     std::vector<uint32_t> offs(D + 2, 0);
-    for (int m = 0; m <= D; ++m) offs[m + 1] = offs[m] + (uint32_t)pl::binom_u64(D, m);
-    std::vector<uint32_t> tab(1u << D);
+    for (int m = 0; m <= D; ++m) offs[m + 1] = offs[m] + 2u * (uint32_t)pl::binom_u64(D, m);
+    std::vector<uint16_t> tab((size_t)offs[D + 1] * 8, 0);
     for (uint32_t mask = 0; mask < (1u << D); ++mask) {
-        uint32_t r = 0, r1 = 0;
+        const int m = __builtin_popcount(mask);
+        uint32_t r = 0;
         int i = 1;
         for (uint32_t mm = mask; mm; mm &= mm - 1, ++i) r += (uint32_t)pl::binom_u64(__builtin_ctz(mm), i);
-        i = 1;
-        for (uint32_t mm = mask & (mask - 1); mm; mm &= mm - 1, ++i) r1 += (uint32_t)pl::binom_u64(__builtin_ctz(mm), i);
-        tab[offs[__builtin_popcount(mask)] + r] = mask | (r1 << pl::kQtabShift);
+        uint16_t* e = &tab[(size_t)(offs[m] / 2 + r) * 16];
+        int t = 0;
+        for (uint32_t mm = mask; mm; mm &= mm - 1, ++t) {
+            const int v = __builtin_ctz(mm);
+            const uint32_t rest = mask & ~(1u << v);
+            uint32_t rr = 0;
+            int l = 1;
+            for (uint32_t q = rest; q; q &= q - 1, ++l) rr += (uint32_t)pl::binom_u64(__builtin_ctz(q), l);
+            e[t] = (uint16_t)(rr | (uint32_t)v << pl::kWsLtabRankBits);
+        }
     }
     Qtab q;
     std::vector<uint2> bp(pl::kBinomDim * pl::kBinomDim);
@@ -367,9 +393,9 @@ pl_status get_qtab(int D, Qtab* out) {
             bp[i * pl::kBinomDim + sc] = make_uint2((uint32_t)pl::binom_u64(sc, i), i >= 1 ? (uint32_t)pl::binom_u64(sc, i - 1) : 0u);
     PL_CUDA(cudaMalloc(&q.binom_pairs, bp.size() * sizeof(uint2)));
     PL_CUDA(cudaMemcpy(q.binom_pairs, bp.data(), bp.size() * sizeof(uint2), cudaMemcpyHostToDevice));
-    PL_CUDA(cudaMalloc(&q.qtab, tab.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMalloc(&q.ltab, tab.size() * sizeof(uint16_t)));
     PL_CUDA(cudaMalloc(&q.offs, offs.size() * sizeof(uint32_t)));
-    PL_CUDA(cudaMemcpy(q.qtab, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    PL_CUDA(cudaMemcpy(q.ltab, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     PL_CUDA(cudaMemcpy(q.offs, offs.data(), offs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     cache[{dev, D}] = q;
     *out = q;
@@ -411,13 +437,13 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         const int g = e ? std::max(1, std::min(atoi(e), num_sms())) : num_sms();
         return std::max(team, g / team * team);
     }();
-    s = get_sched(n, k, D, r0, r1, grid / team, &sched);
+    s = get_sched(n, k, D, r0, r1, grid / team, pl::WsGeom<(int)sizeof(T)>::CHUNK, &sched);
     if (s != PL_OK) return s;
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(set_smem_once(kern, smem));
     kern<<<grid, pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                                                  static_cast<T*>(cur), r0, r1, sched, q.qtab, q.offs,
+                                                  static_cast<T*>(cur), r0, r1, sched, q.ltab, q.offs,
                                                   q.binom_pairs, guard, status, ws_hints(), team);
     PL_CUDA(cudaGetLastError());
     return PL_OK;

@@ -45,32 +45,75 @@
 
 namespace pl {
 
-constexpr int kWsGroupWarps = 8;
-constexpr int kWsLanes = 32 * kWsGroupWarps;   // consumer threads per group
-constexpr int kWsPer = 2;                      // outputs per consumer thread per chunk (independent chains)
-constexpr int kWsChunk = kWsLanes * kWsPer;    // CH: outputs per chunk
 constexpr int kWsMaxHigh = 32;                 // high columns per tile (n - D <= 31)
-constexpr int kQtabShift = 17;                 // qtab entry: mask(V) | rank(V \ {min V}) << 17
+constexpr int kWsLtabRankBits = 12;           // ltab entry: rank_D(V \ {v}) | v << 12 (D <= 14)
 constexpr int kWsEnd = -1;
 constexpr int kWaitHintNs = 20000;             // mbarrier try_wait suspend-time hint
 
 // Low window D per element size: the largest tile source C(D, D/2) must fit a
 // shared-memory slot next to the stage rings (<= 227 KB in all).
-__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? 14 : 14; }
+// (PL_WS_* macros: build-time tuning overrides.)
+#ifndef PL_WS_D16
+#define PL_WS_D16 14
+#endif
+#ifndef PL_WS_D8
+#define PL_WS_D8 14
+#endif
+#ifndef PL_WS_NSG16
+#define PL_WS_NSG16 2
+#endif
+#ifndef PL_WS_NSG8
+#define PL_WS_NSG8 2
+#endif
+#ifndef PL_WS_FS16
+#define PL_WS_FS16 3
+#endif
+#ifndef PL_WS_FS8
+#define PL_WS_FS8 4
+#endif
+#ifndef PL_WS_NSRC16
+#define PL_WS_NSRC16 2
+#endif
+#ifndef PL_WS_NSRC8
+#define PL_WS_NSRC8 3
+#endif
+#ifndef PL_WS_G16
+#define PL_WS_G16 2
+#endif
+#ifndef PL_WS_G8
+#define PL_WS_G8 3
+#endif
+#ifndef PL_WS_GW16
+#define PL_WS_GW16 8
+#endif
+#ifndef PL_WS_GW8
+#define PL_WS_GW8 8
+#endif
+#ifndef PL_WS_PER16
+#define PL_WS_PER16 2
+#endif
+#ifndef PL_WS_PER8
+#define PL_WS_PER8 2
+#endif
+__host__ __device__ constexpr int ws_window(int elem_bytes) { return elem_bytes == 16 ? PL_WS_D16 : PL_WS_D8; }
 
 // Consumer groups per CTA: three for 8-byte elements, two for complex, whose
 // arithmetic needs the registers.
 template <int ELEM>
 struct WsGeom {
-    static constexpr int G = ELEM == 16 ? 2 : 3;  // consumer groups
-    static constexpr int NSG = 2;                 // stages per group ring (power of two)
-    static constexpr int FS = ELEM == 16 ? 3 : 4; // stream segments per ring stage
-    static constexpr int NSRC = ELEM == 16 ? 2 : 3;  // tile slots (header + low source) in flight
+    static constexpr int G = ELEM == 16 ? PL_WS_G16 : PL_WS_G8;       // consumer groups
+    static constexpr int GW = ELEM == 16 ? PL_WS_GW16 : PL_WS_GW8;    // warps per group
+    static constexpr int PER = ELEM == 16 ? PL_WS_PER16 : PL_WS_PER8; // outputs per thread per chunk
+    static constexpr int LANES = 32 * GW;                             // consumer threads per group
+    static constexpr int CHUNK = LANES * PER;                         // CH: outputs per chunk
+    static constexpr int NSG = ELEM == 16 ? PL_WS_NSG16 : PL_WS_NSG8;     // stages per group ring
+    static constexpr int FS = ELEM == 16 ? PL_WS_FS16 : PL_WS_FS8;        // stream segments per ring stage
+    static constexpr int NSRC = ELEM == 16 ? PL_WS_NSRC16 : PL_WS_NSRC8;  // tile slots (header + low source)
     // elements per low-source slot: the largest tile source C(D, D/2), plus the
     // 8-byte alignment pad and round-up of bulk_span
     static constexpr int kSrcSlot =
         (int)((binom_u64(ws_window(ELEM), ws_window(ELEM) / 2) + 2 + 16 / ELEM - 1) / (16 / ELEM) * (16 / ELEM));
-    static constexpr int kConsumerWarps = kWsGroupWarps * G;
+    static constexpr int kConsumerWarps = GW * G;
     static constexpr int kThreads = 32 * (kConsumerWarps + G + 1);  // consumers, G streamers, publisher
 };
 
@@ -97,7 +140,11 @@ struct WsSmem {
     static constexpr int NSRC = WsGeom<(int)sizeof(T)>::NSRC;
     static constexpr int kSrcSlot = WsGeom<(int)sizeof(T)>::kSrcSlot;
     static constexpr int FS = WsGeom<(int)sizeof(T)>::FS;
-    static constexpr size_t kSlot = round16(sizeof(T) * kWsChunk + 16) / sizeof(T);  // elements per segment slot
+    static constexpr int GW = WsGeom<(int)sizeof(T)>::GW;
+    static constexpr int PER = WsGeom<(int)sizeof(T)>::PER;
+    static constexpr int LANES = WsGeom<(int)sizeof(T)>::LANES;
+    static constexpr int CHUNK = WsGeom<(int)sizeof(T)>::CHUNK;
+    static constexpr size_t kSlot = round16(sizeof(T) * CHUNK + 16) / sizeof(T);  // elements per segment slot
     uint2* B2;            // B2[i * kBinomDim + s] = (C(s, i), C(s, i - 1))
     T* row_low;           // [32]   a(k-1, v), v < D
     uint64_t* full;       // [G][NSG]
@@ -289,39 +336,34 @@ __device__ __forceinline__ WsCursor ws_cursor(const uint32_t* __restrict__ sched
 
 // ---------------------------------------------------------------- consumer math
 
+// Low terms of one output from its ltab list (entries rank | column << 12,
+// ascending column): gathers from the shared-memory tile source.
+__device__ __forceinline__ uint32_t ltab_entry(const uint4& a, const uint4& b, int i) {
+    const uint4& v = i < 8 ? a : b;
+    const int w = (i & 7) >> 1;
+    const uint32_t word = w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+    return (i & 1) ? word >> 16 : word & 0xffffu;
+}
+
 template <class RR, int M, class T>
-__device__ __forceinline__ T ws_low(uint32_t e, const T* __restrict__ src, const T* __restrict__ row_low,
-                                    const uint2* __restrict__ B2, bool& ov) {
-    uint32_t V = e & ((1u << kQtabShift) - 1);
-    uint32_t Q = e >> kQtabShift, P = 0;
-    int sv[M];
-    uint32_t pr[M];
-#pragma unroll
-    for (int i = 1; i <= M; ++i) {
-        const int s = __ffs(V) - 1;
-        V &= V - 1;
-        const uint2 b = B2[i * kBinomDim + s];  // (C(s, i), C(s, i-1))
-        if (i >= 2) Q -= b.y;
-        sv[i - 1] = s;
-        pr[i - 1] = P + Q;
-        P += b.x;
-    }
+__device__ __forceinline__ T ws_low(const uint4& ea, const uint4& eb, const T* __restrict__ src,
+                                    const T* __restrict__ row_low, bool& ov) {
     T x[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x[i] = src[pr[i]];  // shared-memory tile source
-    T acc = RR::mul(row_low[sv[0]], x[0], ov);
+    for (int i = 0; i < M; ++i) x[i] = src[ltab_entry(ea, eb, i) & ((1u << kWsLtabRankBits) - 1)];
+    T acc = RR::mul(row_low[ltab_entry(ea, eb, 0) >> kWsLtabRankBits], x[0], ov);
 #pragma unroll
-    for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[sv[i]], x[i], ov);
+    for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[ltab_entry(ea, eb, i) >> kWsLtabRankBits], x[i], ov);
     return acc;
 }
 
 template <class RR, class T>
-__device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, const T* row_low, const uint2* B2,
+__device__ __forceinline__ T ws_low_dispatch(int m, const uint4& ea, const uint4& eb, const T* src, const T* row_low,
                                              bool& ov) {
     switch (m) {
 #define PL_WS_CASE(M) \
     case M:           \
-        return ws_low<RR, M>(e, src, row_low, B2, ov);
+        return ws_low<RR, M>(ea, eb, src, row_low, ov);
         PL_WS_CASE(1) PL_WS_CASE(2) PL_WS_CASE(3) PL_WS_CASE(4) PL_WS_CASE(5) PL_WS_CASE(6) PL_WS_CASE(7)
         PL_WS_CASE(8) PL_WS_CASE(9) PL_WS_CASE(10) PL_WS_CASE(11) PL_WS_CASE(12) PL_WS_CASE(13) PL_WS_CASE(14)
 #undef PL_WS_CASE
@@ -335,42 +377,57 @@ __device__ __forceinline__ T ws_low_dispatch(int m, uint32_t e, const T* src, co
 // `seq` is the group's running stage counter (stage seq % NSG, use seq / NSG).
 template <class RR, class T>
 __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr<T>& h, const T* __restrict__ src,
-                                                const uint32_t* __restrict__ qt, T* __restrict__ cur, int g, int j,
+                                                const uint4* __restrict__ qt, T* __restrict__ cur, int g, int j,
                                                 uint32_t c_first, uint32_t& seq, bool& ov, uint32_t hints) {
     constexpr int NSG = WsSmem<T>::NSG;
     constexpr int G = WsSmem<T>::G;
     constexpr int FS = WsSmem<T>::FS;
+    constexpr int PER = WsSmem<T>::PER, LANES = WsSmem<T>::LANES, CHUNK = WsSmem<T>::CHUNK;
     const int m = h.m, f = h.f;
     const uint32_t q1 = h.q1, nchunks = h.nchunks, cb = h.cb, cs = h.cs;
     const uint64_t cur_base = h.cur_base;
     const uint64_t pol_store = l2_evict_first_policy();
     uint32_t c = c_first;
-    // each thread owns outputs j and j + kWsLanes of every chunk: two independent
-    // accumulation chains; qtab entries are prefetched one chunk ahead
-    uint32_t e_next[kWsPer] = {};
-    if (m >= 1) {
+    // each thread owns outputs j and j + LANES of every chunk: two independent
+    // accumulation chains; ltab lists are prefetched one chunk ahead
+    uint4 ea_next[PER], eb_next[PER];
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(cb + c * cs + j + p * kWsLanes, q1 - 1));
+    for (int p = 0; p < PER; ++p) {
+        ea_next[p] = z4;
+        eb_next[p] = z4;
+        if (m >= 1) {
+            const uint32_t q = min(cb + c * cs + j + p * LANES, q1 - 1);
+            ea_next[p] = __ldg(qt + 2 * q);
+            if (m > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
+        }
     }
     for (; c < nchunks; c += G) {
         const uint32_t c0 = cb + c * cs;
-        const uint32_t len = min((uint32_t)kWsChunk, q1 - c0);
+        const uint32_t len = min((uint32_t)CHUNK, q1 - c0);
         // Lanes past the tile end compute a duplicate of its last output
         // (no divergence); only their store and overflow flag are dropped.
-        uint32_t e[kWsPer];
+        uint4 ea[PER], eb[PER];
 #pragma unroll
-        for (int p = 0; p < kWsPer; ++p) e[p] = e_next[p];
+        for (int p = 0; p < PER; ++p) {
+            ea[p] = ea_next[p];
+            eb[p] = eb_next[p];
+        }
         if (m >= 1 && c + G < nchunks) {
 #pragma unroll
-            for (int p = 0; p < kWsPer; ++p) e_next[p] = __ldg(qt + min(c0 + G * cs + j + p * kWsLanes, q1 - 1));
+            for (int p = 0; p < PER; ++p) {
+                const uint32_t q = min(c0 + G * cs + j + p * LANES, q1 - 1);
+                ea_next[p] = __ldg(qt + 2 * q);
+                if (m > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
+            }
         }
-        bool lov[kWsPer];
-        T acc[kWsPer];
+        bool lov[PER];
+        T acc[PER];
 #pragma unroll
-        for (int p = 0; p < kWsPer; ++p) {
+        for (int p = 0; p < PER; ++p) {
             lov[p] = false;
             acc[p] = RR::zero();
-            if (m >= 1 && !(hints & 128u)) acc[p] = ws_low_dispatch<RR>(m, e[p], src, sm.row_low, sm.B2, lov[p]);  // 128: probe
+            if (m >= 1 && !(hints & 128u)) acc[p] = ws_low_dispatch<RR>(m, ea[p], eb[p], src, sm.row_low, lov[p]);  // 128: probe
         }
         for (int l0 = 0; l0 < f; l0 += FS, ++seq) {
             const int nl = min(FS, f - l0);
@@ -383,32 +440,32 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
             mbar_wait(sm.full_bar(g, s), (seq / NSG) & 1u);
             // read the stage into registers and hand the slot back before the math,
             // so the producer refills it one compute phase earlier
-            T xs[kWsPer][FS];
+            T xs[PER][FS];
             const T* st = sm.slot(g, s, 0) + j;
             if (nl == FS) {
 #pragma unroll
-                for (int p = 0; p < kWsPer; ++p)
+                for (int p = 0; p < PER; ++p)
 #pragma unroll
-                    for (int li = 0; li < FS; ++li) xs[p][li] = st[p * kWsLanes + li * WsSmem<T>::kSlot + pads[li]];
+                    for (int li = 0; li < FS; ++li) xs[p][li] = st[p * LANES + li * WsSmem<T>::kSlot + pads[li]];
             } else {
 #pragma unroll
-                for (int p = 0; p < kWsPer; ++p)
+                for (int p = 0; p < PER; ++p)
 #pragma unroll
                     for (int li = 0; li < FS; ++li)
-                        xs[p][li] = li < nl ? st[p * kWsLanes + li * WsSmem<T>::kSlot + pads[li]] : RR::zero();
+                        xs[p][li] = li < nl ? st[p * LANES + li * WsSmem<T>::kSlot + pads[li]] : RR::zero();
             }
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
             const bool init_first = m == 0 && l0 == 0;
             if (hints & 64u) {  // timing probe: no high-term math
 #pragma unroll
-                for (int p = 0; p < kWsPer; ++p)
+                for (int p = 0; p < PER; ++p)
 #pragma unroll
                     for (int li = 0; li < FS; ++li) acc[p] = RR::add(acc[p], xs[p][li], lov[p]);
                 continue;
             }
 #pragma unroll
-            for (int p = 0; p < kWsPer; ++p) {
+            for (int p = 0; p < PER; ++p) {
                 if (nl == FS && !init_first) {
 #pragma unroll
                     for (int li = 0; li < FS; ++li) acc[p] = RR::mac(acc[p], h.coef[l0 + li], xs[p][li], lov[p]);
@@ -423,12 +480,12 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
             }
         }
 #pragma unroll
-        for (int p = 0; p < kWsPer; ++p) {
-            if ((uint32_t)(j + p * kWsLanes) < len) {
+        for (int p = 0; p < PER; ++p) {
+            if ((uint32_t)(j + p * LANES) < len) {
                 if (hints & 4u)
-                    stg_hint(cur + cur_base + c0 + j + p * kWsLanes, acc[p], pol_store);
+                    stg_hint(cur + cur_base + c0 + j + p * LANES, acc[p], pol_store);
                 else
-                    cur[cur_base + c0 + j + p * kWsLanes] = acc[p];
+                    cur[cur_base + c0 + j + p * LANES] = acc[p];
                 ov |= lov[p];  // duplicates past the tile end never report
             }
         }
@@ -441,7 +498,7 @@ template <class R, class RU>
 __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 1)
     sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ sched,
-                 const uint32_t* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
+                 const uint4* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
                  const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
                  int32_t* __restrict__ status, uint32_t hints, int tP) {
     using T = typename R::T;
@@ -450,6 +507,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     constexpr int G = WsSmem<T>::G;
     constexpr int CW = WsSmem<T>::CW;
     constexpr int FS = WsSmem<T>::FS;
+    constexpr int GW = WsSmem<T>::GW, CHUNK = WsSmem<T>::CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ T row_sh[kMaxOrder];
     __shared__ uint32_t qoff_sh[kMaxOrder + 2];
@@ -464,7 +522,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     if (threadIdx.x == 0) {
         for (int s = 0; s < G * NSG; ++s) {
             mbar_init(&sm.full[s], 1);               // the group's streamer: arrive.expect_tx
-            mbar_init(&sm.empty[s], kWsGroupWarps);  // the group's consumer warps
+            mbar_init(&sm.empty[s], GW);  // the group's consumer warps
         }
         for (int s = 0; s < NSRC; ++s) {
             mbar_init(&sm.src_full[s], 1);        // publisher: arrive.expect_tx
@@ -509,7 +567,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             const uint32_t len = sm.B2[m * kBinomDim + D].x;
             const uint32_t q0 = r0 > cur_base ? (uint32_t)(r0 - cur_base) : 0u;
             const uint32_t q1 = (r1 - cur_base) < len ? (uint32_t)(r1 - cur_base) : len;
-            const uint32_t total = q1 > q0 ? (q1 - q0 + kWsChunk - 1) / kWsChunk : 0u;
+            const uint32_t total = q1 > q0 ? (q1 - q0 + CHUNK - 1) / CHUNK : 0u;
             const uint32_t nchunks = total > (uint32_t)tp ? (total - tp + tP - 1) / tP : 0u;
             if (nchunks == 0) continue;
 
@@ -531,6 +589,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                     if (z != 0) far = ((1u << (__ffs(z) - 1)) - (1u << lane)) > (1u << ((hints >> 8) & 31u));
                     mode = far ? 1 : ((hints & 3u) == 2 ? 2 : 0);
                 }
+                if ((hints & 0x10000u) && lane >= (int)((hints >> 8) & 31u)) mode = 3;  // probe: drop far streams
                 h.mode[idx] = mode;
             }
             if (lane == 0) {
@@ -538,8 +597,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 h.f = f;
                 h.q1 = q1;
                 h.nchunks = nchunks;
-                h.cb = q0 + tp * kWsChunk;
-                h.cs = tP * kWsChunk;
+                h.cb = q0 + tp * CHUNK;
+                h.cs = tP * CHUNK;
                 h.cur_base = cur_base;
                 h.qoff = qoff_sh[m];
                 h.pad_src = sizeof(T) == 16 ? 0u : (uint32_t)(src_base & 1u);
@@ -580,7 +639,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             gchunk += nchunks;
             for (uint32_t c = c_first; c < nchunks; c += G) {
                 const uint32_t c0 = cb + c * cs;
-                const uint32_t clen = min((uint32_t)kWsChunk, q1 - c0);
+                const uint32_t clen = min((uint32_t)CHUNK, q1 - c0);
+                if ((hints & 0x20000u) && c + G < nchunks && lane < f) {
+                    // warm L2 with this group's next chunk of the tile (all its streams)
+                    const uint32_t n0 = c0 + G * cs;
+                    const BulkSpan<T> sp = bulk_span(prev, h.sbase[lane] + n0, min((uint32_t)CHUNK, q1 - n0));
+                    bulk_prefetch_l2(sp.src, sp.bytes);
+                }
                 for (int l0 = 0; l0 < f; l0 += FS, ++sq) {
                     const int nl = min(FS, f - l0);
                     const int s = (int)(sq % NSG);
@@ -590,10 +655,10 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                     }
                     mbar_wait_prod(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
                     BulkSpan<T> seg{prev, 0u, 0};
-                    if (lane < nl && !(hints & 32u)) seg = bulk_span(prev, base + c0, clen);  // 32: timing probe
+                    if (lane < nl && !(hints & 32u) && mode != 3) seg = bulk_span(prev, base + c0, clen);  // 32: timing probe
                     unsigned bytes;
                     if constexpr (sizeof(T) == 16)
-                        bytes = (hints & 32u) ? 0u : (unsigned)nl * clen * 16u;
+                        bytes = (hints & 0x10020u) ? __reduce_add_sync(0xffffffffu, seg.bytes) : (unsigned)nl * clen * 16u;
                     else
                         bytes = __reduce_add_sync(0xffffffffu, seg.bytes);
                     if (lane == 0) mbar_arrive_expect_tx(sm.full_bar(g, s), bytes);
@@ -612,8 +677,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         }
     } else {
         // ------------------------------------------------------------ consumers
-        const int g = warp / kWsGroupWarps;
-        const int j = (warp % kWsGroupWarps) * 32 + lane;
+        const int g = warp / GW;
+        const int j = (warp % GW) * 32 + lane;
         bool use_checked = false;
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
@@ -628,7 +693,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
             gchunk += nchunks;
             if (c_first < nchunks) {
-                const uint32_t* qt = qtab + h.qoff;
+                const uint4* qt = qtab + h.qoff;
                 const T* src = sm.src + (size_t)ss * WsSmem<T>::kSrcSlot + h.pad_src;
                 if constexpr (R::kChecked) {
                     if (use_checked) {

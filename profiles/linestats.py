@@ -47,3 +47,16 @@ print(f"total warp instructions {ti:.4g}, stall samples {ts:.4g}")
 for ln, c in inst.most_common(int(sys.argv[4]) if len(sys.argv) > 4 else 40):
     top = ", ".join(f"{o} {v / c * 100:.0f}%" for o, v in ops[ln].most_common(3))
     print(f"{ln:28s} inst {c / ti * 100:5.1f}%  stalls {samp[ln] / ts * 100:5.1f}%   [{top}]")
+
+if "--top-sass" in sys.argv:
+    print("\ntop SASS instructions by stall samples:")
+    recs = []
+    for r in data:
+        if len(r) <= ie:
+            continue
+        off = int(r[ia], 16) - base
+        ln, op = fun.get(off, ("?", "?"))
+        recs.append((float(r[isamp] or 0), off, ln, r[hdr.index("Source")].strip(), float(r[ie] or 0)))
+    recs.sort(reverse=True)
+    for s_, off, ln, src_, c in recs[:30]:
+        print(f"{s_ / ts * 100:5.1f}%  {off:6x}  {ln:26s} {src_[:60]:60s} inst {c:.3g}")
