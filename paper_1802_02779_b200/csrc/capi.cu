@@ -442,10 +442,32 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
     PL_CUDA(set_smem_once(kern, smem));
+    // PL_WS_TRACE=<file> PL_WS_TRACE_K=<k>: event trace of CTA 0 for layer k (debug)
+    static const char* trace_path = std::getenv("PL_WS_TRACE");
+    static const int trace_k = std::getenv("PL_WS_TRACE_K") ? atoi(std::getenv("PL_WS_TRACE_K")) : -1;
+    unsigned long long* trace = nullptr;
+    if (trace_path && k == trace_k) {
+        const size_t tb = (size_t)4 * pl::kWsTraceCap * 2 * sizeof(unsigned long long);
+        PL_CUDA(cudaMalloc(&trace, tb));
+        PL_CUDA(cudaMemset(trace, 0, tb));
+        PL_CUDA(cudaMemcpyToSymbol(pl::g_ws_trace, &trace, sizeof(trace)));
+    }
     kern<<<grid, pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                                   static_cast<T*>(cur), r0, r1, sched, q.ltab, q.offs,
                                                   q.binom_pairs, guard, status, ws_hints(), team);
     PL_CUDA(cudaGetLastError());
+    if (trace) {
+        PL_CUDA(cudaStreamSynchronize(st));
+        std::vector<unsigned long long> hb((size_t)4 * pl::kWsTraceCap * 2);
+        PL_CUDA(cudaMemcpy(hb.data(), trace, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long* null = nullptr;
+        PL_CUDA(cudaMemcpyToSymbol(pl::g_ws_trace, &null, sizeof(null)));
+        PL_CUDA(cudaFree(trace));
+        if (FILE* fp = std::fopen(trace_path, "wb")) {
+            std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), fp);
+            std::fclose(fp);
+        }
+    }
     return PL_OK;
 }
 

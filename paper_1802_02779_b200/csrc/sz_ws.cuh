@@ -49,6 +49,14 @@ constexpr int kWsMaxHigh = 32;                 // high columns per tile (n - D <
 constexpr int kWsLtabRankBits = 12;           // ltab entry: rank_D(V \ {v}) | v << 12 (D <= 14)
 constexpr int kWsEnd = -1;
 constexpr int kWaitHintNs = 20000;             // mbarrier try_wait suspend-time hint
+#ifndef PL_WS_PSLEEP
+#define PL_WS_PSLEEP 0
+#endif
+#ifndef PL_WS_PUBSLEEP
+#define PL_WS_PUBSLEEP 0
+#endif
+constexpr unsigned kProdSleepNs = PL_WS_PSLEEP;     // max poll sleep of streamer waits (0: try_wait)
+constexpr unsigned kPubSleepNs = PL_WS_PUBSLEEP;    // max poll sleep of publisher waits (0: try_wait)
 
 // Low window D per element size: the largest tile source C(D, D/2) must fit a
 // shared-memory slot next to the stage rings (<= 227 KB in all).
@@ -126,7 +134,8 @@ struct WsHdr {
     int32_t m, f;                    // m < 0: end of the CTA's tile list
     uint32_t q1, nchunks, cb, cs;    // clip end; this CTA's chunks start at cb + i * cs
     uint64_t cur_base;               // rank of the tile's first output
-    uint32_t qoff, pad_src;          // qtab offset for m; 8-byte alignment pad of the source
+    uint32_t qoff, pad_src;          // ltab offset for m; 8-byte alignment pad of the source
+    uint32_t padmask;                // bit l: 8-byte alignment pad of stream l's chunks (cb, cs even)
     T coef[kWsMaxHigh];              // a(k-1, F_l)
     uint64_t sbase[kWsMaxHigh];      // base rank of stream tile (F \ {F_l}, k-1)
     int32_t mode[kWsMaxHigh];        // L2 policy of stream l (0 plain, 1 evict-first, 2 evict-last)
@@ -226,16 +235,37 @@ __device__ __forceinline__ void mbar_wait_slot(uint64_t* bar, unsigned parity) {
 }
 
 // Same wait, separate code location (producer's ring-slot waits).
-__device__ __forceinline__ void mbar_wait_prod(uint64_t* bar, unsigned parity) {
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "n"(kWaitHintNs)
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+// Wait of a warp that is normally ahead (streamer on a full ring, publisher
+// on busy slots): poll with a growing sleep so that it leaves the issue
+// slots to the consumer warps.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, unsigned parity, unsigned max_ns) {
+    unsigned ns = 32;
+    while (!mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 < max_ns ? ns * 2 : max_ns;
+    }
+}
+
+// Same wait, separate code location (producer's ring-slot waits).
+__device__ __forceinline__ void mbar_wait_prod(uint64_t* bar, unsigned parity) {
+    if constexpr (kProdSleepNs == 0)
+        mbar_wait_slot(bar, parity);
+    else
+        mbar_wait_backoff(bar, parity, kProdSleepNs);
 }
 
 // TMA 1D bulk copy global -> shared, completion counted on `bar` in bytes.
@@ -319,6 +349,36 @@ __device__ __forceinline__ uint64_t warp_scan_u64(uint64_t v) {
     return v;
 }
 
+// ---------------------------------------------------------------- debug trace
+// Event trace of CTA 0 for pipeline analysis (PL_WS_TRACE, see capi.cu):
+// region r holds (clock64, event | arg << 8) pairs; r = 0/1 first warp of
+// consumer group 0/1, 2 streamer of group 0, 3 publisher.
+__device__ unsigned long long* g_ws_trace = nullptr;
+constexpr int kWsTraceCap = 65536;
+
+#ifndef PL_WS_TRACE_ENABLE
+struct WsTrace {  // compiled out unless built with -DPL_WS_TRACE_ENABLE
+    __device__ __forceinline__ void init(int) {}
+    __device__ __forceinline__ void ev(uint32_t, uint32_t = 0) {}
+};
+#else
+struct WsTrace {
+    unsigned long long* p = nullptr;
+    uint32_t i = 0;
+    __device__ __forceinline__ void init(int region) {
+        p = (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && g_ws_trace) ? g_ws_trace + (size_t)region * kWsTraceCap * 2
+                                                                          : nullptr;
+    }
+    __device__ __forceinline__ void ev(uint32_t e, uint32_t arg = 0) {
+        if (p && i < kWsTraceCap) {
+            p[2 * i] = clock64();
+            p[2 * i + 1] = e | (unsigned long long)arg << 8;
+            ++i;
+        }
+    }
+};
+#endif
+
 // ---------------------------------------------------------------- tile list
 
 // The CTA's tile list. The host deals the layer's tiles, in increasing F, to
@@ -357,50 +417,32 @@ __device__ __forceinline__ T ws_low(const uint4& ea, const uint4& eb, const T* _
     return acc;
 }
 
-template <class RR, class T>
-__device__ __forceinline__ T ws_low_dispatch(int m, const uint4& ea, const uint4& eb, const T* src, const T* row_low,
-                                             bool& ov) {
-    switch (m) {
-#define PL_WS_CASE(M) \
-    case M:           \
-        return ws_low<RR, M>(ea, eb, src, row_low, ov);
-        PL_WS_CASE(1) PL_WS_CASE(2) PL_WS_CASE(3) PL_WS_CASE(4) PL_WS_CASE(5) PL_WS_CASE(6) PL_WS_CASE(7)
-        PL_WS_CASE(8) PL_WS_CASE(9) PL_WS_CASE(10) PL_WS_CASE(11) PL_WS_CASE(12) PL_WS_CASE(13) PL_WS_CASE(14)
-#undef PL_WS_CASE
-    }
-    return RR::zero();
-}
-
 // Consumer group g's share of one tile: its chunks c_first, c_first + G, ...
 // (chunks are dealt to groups round-robin over the CTA's whole tile sequence).
 // Each chunk takes ceil(f / FS) consecutive stages of the group's own ring;
 // `seq` is the group's running stage counter (stage seq % NSG, use seq / NSG).
-template <class RR, class T>
+template <class RR, int M, class T>
 __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr<T>& h, const T* __restrict__ src,
                                                 const uint4* __restrict__ qt, T* __restrict__ cur, int g, int j,
-                                                uint32_t c_first, uint32_t& seq, bool& ov, uint32_t hints) {
+                                                uint32_t c_first, uint32_t& seq, bool& ov, uint32_t hints,
+                                                WsTrace& tr) {
     constexpr int NSG = WsSmem<T>::NSG;
     constexpr int G = WsSmem<T>::G;
     constexpr int FS = WsSmem<T>::FS;
     constexpr int PER = WsSmem<T>::PER, LANES = WsSmem<T>::LANES, CHUNK = WsSmem<T>::CHUNK;
-    const int m = h.m, f = h.f;
-    const uint32_t q1 = h.q1, nchunks = h.nchunks, cb = h.cb, cs = h.cs;
+    const int f = h.f;
+    const uint32_t q1 = h.q1, nchunks = h.nchunks, cb = h.cb, cs = h.cs, padmask = h.padmask;
     const uint64_t cur_base = h.cur_base;
     const uint64_t pol_store = l2_evict_first_policy();
     uint32_t c = c_first;
-    // each thread owns outputs j and j + LANES of every chunk: two independent
+    // each thread owns outputs j + p * LANES of every chunk: independent
     // accumulation chains; ltab lists are prefetched one chunk ahead
     uint4 ea_next[PER], eb_next[PER];
-    const uint4 z4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
-        ea_next[p] = z4;
-        eb_next[p] = z4;
-        if (m >= 1) {
-            const uint32_t q = min(cb + c * cs + j + p * LANES, q1 - 1);
-            ea_next[p] = __ldg(qt + 2 * q);
-            if (m > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
-        }
+        const uint32_t q = min(cb + c * cs + j + p * LANES, q1 - 1);
+        if constexpr (M >= 1) ea_next[p] = __ldg(qt + 2 * q);
+        if constexpr (M > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
     }
     for (; c < nchunks; c += G) {
         const uint32_t c0 = cb + c * cs;
@@ -413,12 +455,12 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
             ea[p] = ea_next[p];
             eb[p] = eb_next[p];
         }
-        if (m >= 1 && c + G < nchunks) {
+        if (c + G < nchunks) {
 #pragma unroll
             for (int p = 0; p < PER; ++p) {
                 const uint32_t q = min(c0 + G * cs + j + p * LANES, q1 - 1);
-                ea_next[p] = __ldg(qt + 2 * q);
-                if (m > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
+                if constexpr (M >= 1) ea_next[p] = __ldg(qt + 2 * q);
+                if constexpr (M > 8) eb_next[p] = __ldg(qt + 2 * q + 1);
             }
         }
         bool lov[PER];
@@ -427,17 +469,17 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
         for (int p = 0; p < PER; ++p) {
             lov[p] = false;
             acc[p] = RR::zero();
-            if (m >= 1 && !(hints & 128u)) acc[p] = ws_low_dispatch<RR>(m, ea[p], eb[p], src, sm.row_low, lov[p]);  // 128: probe
+            if constexpr (M >= 1) acc[p] = ws_low<RR, M>(ea[p], eb[p], src, sm.row_low, lov[p]);
         }
         for (int l0 = 0; l0 < f; l0 += FS, ++seq) {
             const int nl = min(FS, f - l0);
             int pads[FS];
 #pragma unroll
-            for (int li = 0; li < FS; ++li) {
-                pads[li] = sizeof(T) == 16 || li >= nl ? 0 : (int)((h.sbase[l0 + li] + c0) & 1u);
-            }
+            for (int li = 0; li < FS; ++li) pads[li] = sizeof(T) == 16 ? 0 : (int)((padmask >> (l0 + li)) & 1u);
             const int s = (int)(seq % NSG);
+            tr.ev(3, seq);
             mbar_wait(sm.full_bar(g, s), (seq / NSG) & 1u);
+            tr.ev(4, seq);
             // read the stage into registers and hand the slot back before the math,
             // so the producer refills it one compute phase earlier
             T xs[PER][FS];
@@ -456,14 +498,7 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
             }
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
-            const bool init_first = m == 0 && l0 == 0;
-            if (hints & 64u) {  // timing probe: no high-term math
-#pragma unroll
-                for (int p = 0; p < PER; ++p)
-#pragma unroll
-                    for (int li = 0; li < FS; ++li) acc[p] = RR::add(acc[p], xs[p][li], lov[p]);
-                continue;
-            }
+            const bool init_first = M == 0 && l0 == 0;
 #pragma unroll
             for (int p = 0; p < PER; ++p) {
                 if (nl == FS && !init_first) {
@@ -489,6 +524,22 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
                 ov |= lov[p];  // duplicates past the tile end never report
             }
         }
+    }
+}
+
+// The low count m is uniform over a tile: one specialised chunk loop per m.
+template <class RR, class T>
+__device__ __forceinline__ void ws_consume_dispatch(const WsSmem<T>& sm, const WsHdr<T>& h, const T* src,
+                                                    const uint4* qt, T* cur, int g, int j, uint32_t c_first,
+                                                    uint32_t& seq, bool& ov, uint32_t hints, WsTrace& tr) {
+    switch (h.m) {
+#define PL_WS_CT(M)                                                                        \
+    case M:                                                                                \
+        ws_consume_tile<RR, M>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints, tr); \
+        break;
+        PL_WS_CT(0) PL_WS_CT(1) PL_WS_CT(2) PL_WS_CT(3) PL_WS_CT(4) PL_WS_CT(5) PL_WS_CT(6) PL_WS_CT(7)
+        PL_WS_CT(8) PL_WS_CT(9) PL_WS_CT(10) PL_WS_CT(11) PL_WS_CT(12) PL_WS_CT(13) PL_WS_CT(14)
+#undef PL_WS_CT
     }
 }
 
@@ -542,6 +593,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         WsCursor lst = ws_cursor(sched, nteams, (int)blockIdx.x % nteams);
         const int H = n - D;
         uint32_t pub = 0;
+        WsTrace tr;
+        tr.init(3);
         uint32_t F_next = lst.pos < lst.end ? __ldg(lst.list + lst.pos) : 0u;
         for (; lst.pos < lst.end;) {
             const uint32_t F = F_next;
@@ -572,7 +625,12 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             if (nchunks == 0) continue;
 
             const int ss = (int)(pub % NSRC);
-            mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
+            tr.ev(8, pub);
+            if constexpr (kPubSleepNs == 0)
+                mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
+            else
+                mbar_wait_backoff(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u, kPubSleepNs);
+            tr.ev(9, pub);
             ++pub;
             WsHdr<T>& h = sm.hdr[ss];
             if (set) {
@@ -603,6 +661,12 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 h.qoff = qoff_sh[m];
                 h.pad_src = sizeof(T) == 16 ? 0u : (uint32_t)(src_base & 1u);
             }
+            {
+                // chunk starts cb + i * cs share cb's parity (cs is even)
+                const uint32_t cbv = q0 + tp * CHUNK;
+                const uint32_t pm = __reduce_or_sync(0xffffffffu, set && ((sbase + cbv) & 1u) ? 1u << idx : 0u);
+                if (lane == 0) h.padmask = sizeof(T) == 16 ? 0u : pm;
+            }
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
@@ -626,6 +690,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         const int g = warp - CW;
         const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
         uint32_t sq = 0, gchunk = 0;
+        WsTrace tr;
+        if (g == 0) tr.init(2);
         for (uint32_t ts = 0;; ++ts) {
             const int ss = (int)(ts % NSRC);
             mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
@@ -653,7 +719,9 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                         base = h.sbase[l0 + lane];
                         mode = h.mode[l0 + lane];
                     }
+                    tr.ev(6, sq);
                     mbar_wait_prod(sm.empty_bar(g, s), ((sq / NSG) & 1u) ^ 1u);
+                    tr.ev(7, sq);
                     BulkSpan<T> seg{prev, 0u, 0};
                     if (lane < nl && !(hints & 32u) && mode != 3) seg = bulk_span(prev, base + c0, clen);  // 32: timing probe
                     unsigned bytes;
@@ -683,9 +751,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
         bool ov = false;
         uint32_t seq = 0, gchunk = 0;
+        WsTrace tr;
+        if (warp % GW == 0 && warp / GW < 2) tr.init(warp / GW);
         for (uint32_t ts = 0;; ++ts) {
             const int ss = (int)(ts % NSRC);
+            tr.ev(1, ts);
             mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
+            tr.ev(2, ts);
             const WsHdr<T>& h = sm.hdr[ss];
             if (h.m < 0) break;
             // this group's first chunk of the tile (a group with none takes no stages)
@@ -697,12 +769,12 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 const T* src = sm.src + (size_t)ss * WsSmem<T>::kSrcSlot + h.pad_src;
                 if constexpr (R::kChecked) {
                     if (use_checked) {
-                        ws_consume_tile<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
+                        ws_consume_dispatch<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints, tr);
                     } else {
-                        ws_consume_tile<RU>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
+                        ws_consume_dispatch<RU>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints, tr);
                     }
                 } else {
-                    ws_consume_tile<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints);
+                    ws_consume_dispatch<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints, tr);
                 }
             }
             __syncwarp();
