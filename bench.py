@@ -254,7 +254,11 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
     barrier()
     evs = []
     for _ in range(steps):
-        flush_buf.add_(1)  # evict the (< L2) inputs between timed steps (outside the event pair)
+        # evict the (< L2) inputs between timed steps, outside the event pair: write a
+        # 256 MiB buffer, then read a second one so that the write's dirty lines are
+        # written back before the timed step rather than during it
+        flush_buf[0].add_(1)
+        flush_buf[1].sum(dtype=torch.float32)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step()  # asynchronous: the host runs ahead, the device never waits on it
@@ -352,7 +356,7 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    flush_buf = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB > 126 MB L2
+    flush_buf = torch.zeros(2, 64 * 1024 * 1024, dtype=torch.float32, device=device)  # 2 x 256 MiB > 126 MB L2
     peak, peak_src = load_peaks()
     traffic = load_traffic()
 
@@ -386,7 +390,7 @@ def main():
             "dtype": DT_SHORT[spec["dtype"]],
             "data": "synthetic (seeded generators following BASELINE.json recipes; no public dataset)",
             "config": {"workload": f"{args.config}: {spec['desc']}", "n": spec["n"], "count": spec["count"],
-                       "per_rank_count": spec["count"], "l2": "flushed between timed steps (256 MiB write)",
+                       "per_rank_count": spec["count"], "l2": "flushed between timed steps (256 MiB write, then 256 MiB read)",
                        "arith": "fma" if args.fma else "reference rounding order (no FMA)",
                        "parallelism": f"dp{world} (batch by matrix, no collective)"},
             "roofline": roofline_of(head, peak, peak_src, traffic),

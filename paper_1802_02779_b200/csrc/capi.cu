@@ -21,6 +21,7 @@
 #include "../../include/permlab_b200.h"
 #include "sz_kernels.cuh"
 #include "sz_ws.cuh"
+#include "sz_batch.cuh"
 
 namespace {
 
@@ -141,16 +142,23 @@ cudaError_t set_smem_once(K kern, size_t bytes) {
     return e;
 }
 
-constexpr int kRegsThreads = 128;
 constexpr int kRegsMaxOrder = 5;  // n = 6 spills in registers; it runs in the shared-memory kernel
 
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
-    auto kern = pl::sz_batch_regs_kernel<R, N, kRegsThreads>;
-    const size_t smem = 0;
-    const int64_t blocks = (count + kRegsThreads - 1) / kRegsThreads;
-    kern<<<(unsigned)blocks, kRegsThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, status);
+    using Gm = pl::BatchGeom<T, N>;
+    auto kern = pl::sz_batch_tma_kernel<R, N>;
+    PL_CUDA(set_smem_once(kern, Gm::kSmem));
+    static int per_sm = 0;  // resident CTAs per SM (per instantiation)
+    if (per_sm == 0) {
+        PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Gm::kThreads, Gm::kSmem));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t batches = (count + Gm::kBatch - 1) / Gm::kBatch;
+    const int64_t blocks = std::min<int64_t>((batches + Gm::kWarps - 1) / Gm::kWarps, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, Gm::kThreads, Gm::kSmem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count,
+                                                            status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

@@ -1,0 +1,134 @@
+// Batched small orders (n <= 5): one thread per matrix, the whole DP in
+// registers (perm_in_registers, compile-time subset masks), inputs staged per
+// warp through shared memory.
+//
+// Each warp owns batches of 32 consecutive matrices (32 * n^2 entries, one
+// contiguous run) and two shared-memory buffers. One lane issues a single
+// cp.async.bulk (TMA) for the warp's next batch while the warp computes the
+// current one, so HBM reads are whole-batch bulk transfers that overlap the
+// FP64/INT64 arithmetic; thread `lane` then reads its own matrix from shared
+// memory (stride n^2 elements: conflict-free for 8- and 16-byte entries).
+// A trailing partial batch, or an input pointer that is not 16-byte aligned,
+// is read directly from global memory.
+//
+// Reference: the per-matrix recurrence is proj/src/permanent.cpp:254-302
+// (see sz_kernels.cuh for the evaluation order).
+#pragma once
+
+#include <cstdint>
+
+#include "sz_kernels.cuh"
+#include "sz_ws.cuh"
+
+namespace pl {
+
+template <class T, int N>
+struct BatchGeom {
+    static constexpr int kEnt = N * N;
+    static constexpr int kBatch = 32;                                   // matrices per warp batch
+    static constexpr int kBatchElems = kBatch * kEnt;                   // entries per batch
+    static constexpr unsigned kBatchBytes = kBatchElems * sizeof(T);    // a multiple of 16 (kBatch = 32)
+    static constexpr int kWarps = 4;                                    // warps per CTA
+    static constexpr int kThreads = 32 * kWarps;
+#ifndef PL_BATCH_NBUF
+#define PL_BATCH_NBUF 1
+#endif
+    static constexpr int kBufs = PL_BATCH_NBUF;  // 1: matrices copied to registers, buffer refilled at once
+    static constexpr size_t kSmem = (size_t)kWarps * kBufs * kBatchBytes + kWarps * 2 * sizeof(uint64_t);
+};
+
+template <class R, int N>
+__device__ __forceinline__ typename R::T batch_eval(const typename R::T* local, bool& ov) {
+    using T = typename R::T;
+    constexpr int kEnt = N * N;
+    if constexpr (R::kChecked) {
+        // int64, warp-uniform choice: exact doubles with FMA when every lane's
+        // guard bound is below 2^53 (see i64_fits_f64), wrapping int64 below
+        // 2^63, checked int64 otherwise.
+        const bool ok = i64_guard_ok_n<N>(local);
+        const unsigned act = __activemask();
+        if (__all_sync(act, ok && i64_fits_f64_n<N>(local))) {
+            double dv[kEnt];
+#pragma unroll
+            for (int e = 0; e < kEnt; ++e) dv[e] = (double)local[e];
+            return (T)perm_in_registers<RF64<true>, N>(dv, ov);
+        } else if (__all_sync(act, ok)) {
+            return perm_in_registers<RI64<false>, N>(local, ov);
+        }
+        return perm_in_registers<R, N>(local, ov);
+    } else {
+        return perm_in_registers<R, N>(local, ov);
+    }
+}
+
+template <class R, int N>
+__global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads)
+    sz_batch_tma_kernel(const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
+                        int32_t* __restrict__ status) {
+    using T = typename R::T;
+    using Gm = BatchGeom<T, N>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* buf = reinterpret_cast<T*>(smem_raw) + (size_t)warp * Gm::kBufs * Gm::kBatchElems;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)Gm::kWarps * Gm::kBufs * Gm::kBatchBytes) + warp * 2;
+
+    const int64_t nbatch = (count + Gm::kBatch - 1) / Gm::kBatch;
+    // batches staged by TMA: the full ones, when the input is 16-byte aligned
+    const int64_t nfull = (reinterpret_cast<uintptr_t>(a) & 15u) ? 0 : count / Gm::kBatch;
+    const int64_t stride = (int64_t)gridDim.x * Gm::kWarps;
+    int64_t b = (int64_t)blockIdx.x * Gm::kWarps + warp;
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int64_t batch, int slot) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&bar[slot], Gm::kBatchBytes);
+            bulk_g2s(buf + (Gm::kBufs == 1 ? 0 : slot) * Gm::kBatchElems, a + batch * Gm::kBatchElems, Gm::kBatchBytes,
+                     &bar[slot]);
+        }
+    };
+    if (b < nfull) issue(b, 0);
+    bool ov_any = false;
+    for (uint32_t it = 0; b < nbatch; b += stride, ++it) {
+        const int64_t mi = b * Gm::kBatch + lane;
+        bool ov = false;
+        T v = R::zero();
+        if constexpr (Gm::kBufs == 1) {
+            if (b < nfull) {
+                // pull the matrix into registers, hand the buffer to the next batch, compute
+                mbar_wait(&bar[0], it & 1u);
+                MatRegs<T, Gm::kEnt> m;
+                const T* src = buf + lane * Gm::kEnt;
+#pragma unroll
+                for (int e = 0; e < Gm::kEnt; ++e) m.v[e] = src[e];
+                __syncwarp();
+                if (b + stride < nfull) issue(b + stride, 0);
+                v = batch_eval<R, N>(m.v, ov);
+            }
+        } else {
+            const int slot = it & 1;
+            if (b + stride < nfull) issue(b + stride, slot ^ 1);  // that buffer was released at the end of it - 1
+            if (b < nfull) {
+                mbar_wait(&bar[slot], (it >> 1) & 1u);
+                v = batch_eval<R, N>(buf + slot * Gm::kBatchElems + lane * Gm::kEnt, ov);
+            }
+        }
+        if (b >= nfull && mi < count) {
+            MatRegs<T, Gm::kEnt> m;
+            load_matrix<T, Gm::kEnt>(a + mi * Gm::kEnt, m);
+            v = batch_eval<R, N>(m.v, ov);
+        }
+        if (mi < count) {
+            if (ov) v = R::zero();
+            out[mi] = v;
+            ov_any |= ov;
+        }
+        __syncwarp();
+    }
+    if (ov_any) atomicOr(status, 1);
+}
+
+}  // namespace pl

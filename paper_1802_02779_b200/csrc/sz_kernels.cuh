@@ -15,10 +15,8 @@
 // term), visiting the terms in the reference's ascending-j order.
 //
 // Kernels here:
-//   sz_batch_regs_kernel  n <= 5: one thread per matrix, the whole DP in
-//                         registers (compile-time subset masks), inputs staged
-//                         through shared memory by double-buffered TMA bulk
-//                         copies (persistent CTAs).
+//   (n <= 5: sz_batch_tma_kernel in sz_batch.cuh, one thread per matrix with
+//                         the whole DP in registers, warp batches staged by TMA.)
 //   sz_batch_smem_kernel  6 <= n <= 14: one CTA per matrix, ping-pong
 //                         layers and the matrix in shared memory, predecessor
 //                         ranks from a host-built table shared by the batch.
@@ -268,46 +266,6 @@ __device__ __forceinline__ bool i64_fits_f64_n(const long long* a) {
         prod *= rs < 1.0 ? 1.0 : rs;
     }
     return prod < 9007199254740992.0;
-}
-
-template <class R, int N, int THREADS>
-__global__ void __launch_bounds__(THREADS, sizeof(typename R::T) == 16 ? 2 : 4)
-    sz_batch_regs_kernel(const typename R::T* __restrict__ a,
-                                                                   typename R::T* __restrict__ out, int64_t count,
-                                                                   int32_t* __restrict__ status) {
-    using T = typename R::T;
-    constexpr int kEnt = N * N;
-    const int64_t b = (int64_t)blockIdx.x * THREADS + threadIdx.x;
-    if (b >= count) return;
-    MatRegs<T, kEnt> m;
-    load_matrix<T, kEnt>(a + b * kEnt, m);
-    const T* local = m.v;
-    bool ov = false;
-    T v;
-    if constexpr (R::kChecked) {
-        // int64, warp-uniform choice: exact doubles with FMA when every lane's
-        // guard bound is below 2^53 (see i64_fits_f64), wrapping int64 below
-        // 2^63, checked int64 otherwise.
-        const bool ok = i64_guard_ok_n<N>(local);
-        const unsigned act = __activemask();
-        if (__all_sync(act, ok && i64_fits_f64_n<N>(local))) {
-            double dv[kEnt];
-#pragma unroll
-            for (int e = 0; e < kEnt; ++e) dv[e] = (double)local[e];
-            v = (T)perm_in_registers<RF64<true>, N>(dv, ov);
-        } else if (__all_sync(act, ok)) {
-            v = perm_in_registers<RI64<false>, N>(local, ov);
-        } else {
-            v = perm_in_registers<R, N>(local, ov);
-        }
-    } else {
-        v = perm_in_registers<R, N>(local, ov);
-    }
-    if (ov) {
-        atomicOr(status, 1);
-        v = R::zero();
-    }
-    out[b] = v;
 }
 
 // ---------------------------------------------------------------- 6 <= n <= 14

@@ -123,6 +123,30 @@ def test_empty_and_ragged_batches():
             assert np.array_equal(pl.store_zechin_permanent_batch(a), O.sz_batch(a))
 
 
+@pytest.mark.parametrize("dt", [np.int64, np.float64, np.complex128])
+def test_small_orders_batches_tails_and_alignment(dt):
+    # n <= 5 stage whole 32-matrix batches through shared memory by TMA; tails and
+    # inputs that are not 16-byte aligned take the direct path
+    import torch
+
+    for n in (1, 2, 3, 4, 5):
+        for count in (1, 32, 33, 95, 4097):
+            if dt is np.int64:
+                a = configs.int_matrices(n, count + 1, seed=n * 131 + count)
+            else:
+                a = configs.uniform((count + 1, n, n), seed=n * 131 + count).astype(dt)
+                if dt is np.complex128:
+                    a = a + 1j * configs.uniform((count + 1, n, n), seed=n * 7 + count)
+            want = O.sz_batch(a)
+            got = pl.store_zechin_permanent_batch(a[1:])
+            assert np.array_equal(np.asarray(got).view(np.uint64), want[1:].view(np.uint64)), (n, count)
+            # device tensor viewed one matrix in: 16-byte aligned only when n^2 * size is
+            t = torch.from_numpy(a).cuda()
+            out = torch.empty(count, dtype=t.dtype, device="cuda")
+            pl.store_zechin_permanent_batch(t[1:], out=out)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want[1:].view(np.uint64)), (n, count, "dev")
+
+
 def test_reference_goldens_on_device():
     dev4 = np.array([7, 0, 1, 2, 5, 3, 4, 5, 3, 5, 6, 7, 1, 7, 8, 9]).reshape(4, 4)
     assert pl.store_zechin_permanent(dev4).value == 9722
