@@ -325,8 +325,8 @@ def roofline_of(res, peak, peak_src, traffic):
     tr = traffic.get(res["name"])
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": tr, "peak_source": peak_src,
-            "kernel": "sz_batch_regs_kernel" if res["spec"]["n"] <= 6 else (
-                "sz_batch_smem_kernel" if res["spec"]["n"] <= 16 else "sz_layer_kernel (all layers of one step)"),
+            "kernel": "sz_batch_tma_kernel" if res["spec"]["n"] <= 5 else (
+                "sz_batch_smem_kernel" if res["spec"]["n"] <= 14 else "sz_ws_kernel (all layers of one step)"),
             "fp_rate_tflops": res["flops_per_step"] / res["per_step_s"] / 1e12}
 
 

@@ -16,7 +16,7 @@ python profiles/run_config.py c3 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:sz_batch -c 1 \
       -o gpurun_out/${TAG}_full_c3 python profiles/run_config.py c3 > /dev/null 2>&1
 python profiles/run_config.py c4 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:sz_ws -s 11 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:sz_ws -s 10 -c 1 \
       -o gpurun_out/${TAG}_full_c4 python profiles/run_config.py c4 > /dev/null 2>&1
 python profiles/run_config.py c5 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:sz_ws -s 13 -c 1 \

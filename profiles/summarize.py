@@ -61,7 +61,7 @@ def summarize_launches(tag: str, path: Path):
     (HERE / f"{tag}_launches.md").write_text("\n".join(out) + "\n")
     # DRAM bytes per step per config: batched configs launch one kernel per step; a layer-DP
     # step (C4 f64 n=26, C5 c128 n=32) is every sz_ kernel of that ring, counted per top kernel.
-    groups = {"c1": ("sz_batch_regs_kernel<pl::RI64", None), "c2": ("sz_batch_regs_kernel<pl::RC128", None),
+    groups = {"c1": ("sz_batch_tma_kernel<pl::RI64", None), "c2": ("sz_batch_tma_kernel<pl::RC128", None),
               "c3": ("sz_batch_smem_kernel<pl::RI64", None), "c4": ("RF64", "sz_top_kernel<pl::RF64"),
               "c5": ("RC128<", "sz_top_kernel<pl::RC128")}
     traffic, times = {}, {}
