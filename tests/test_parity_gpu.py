@@ -253,6 +253,31 @@ def test_layer_primitive_ranges_match_oracle():
     assert hexf(v) == hexf(O.sz_f64(a_np))
 
 
+def test_layer_slices_large_order_bitwise():
+    # rank slices that cut tiles anywhere (world 2, 5, 8) through the tiled layer kernel
+    import torch
+
+    from paper_1802_02779_b200.sharded import device_hooks, layer_slices
+
+    n = 22
+    a_np = configs.uniform((n, n), seed=2222)
+    a = torch.from_numpy(a_np).cuda()
+    layer_fn, _ = device_hooks(a)
+    size = O.binom(n, n // 2) + 64
+    prev = torch.zeros(size, dtype=a.dtype, device="cuda")
+    cur = torch.zeros_like(prev)
+    for k in (3, 8, 11, 15, 20):
+        full = torch.from_numpy(O.sz_layer_f64(a_np, k)).cuda()
+        src = torch.from_numpy(O.sz_layer_f64(a_np, k - 1)).cuda()
+        prev[: src.numel()] = src
+        for world in (2, 5, 8):
+            _, sl = layer_slices(n, k, world)
+            cur.zero_()
+            for r0, r1 in sl:
+                layer_fn(k, prev, cur, r0, r1)
+            assert torch.equal(cur[: full.numel()], full), (k, world)
+
+
 def test_cpp_device_suite():
     exe = ROOT / "tests" / "cpp" / "test_permanent_device"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
