@@ -264,12 +264,9 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
     return PL_OK;
 }
 
-// Low-window width D of the tiled layer kernel: as wide as one tile source
-// (C(D, D/2) entries) fits in shared memory, but leaving >= 10 high columns so
-// a layer has enough tiles (>= 2^10 high masks) to keep every SM busy.
 // Tile schedule of one layer range for the layer kernel: the valid tiles F of
 // [r0, r1) in increasing order, each dealt to the CTA with the least load so
-// far (load = chunks of kWsChunk outputs, at least one per tile). Device
+// far (load = chunks of `chunk` outputs, at least one per tile). Device
 // layout: offsets[grid + 1] then the concatenated per-CTA lists. Cached per
 // (device, n, k, D, r0, r1, grid).
 pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int chunk, const uint32_t** out) {
@@ -342,6 +339,10 @@ uint32_t ws_hints() {
     return h;
 }
 
+// Low-window width D of the tiled layer kernel: as wide as one tile source
+// (C(D, D/2) entries) fits a shared-memory slot (ws_window), but leaving >= 10
+// high columns so a layer has enough tiles (>= 2^10 high masks) to keep every
+// SM busy. PL_WS_WINDOW narrows it for tuning.
 int tile_window(size_t elem, int n) {
     static const int override_d = [] {
         const char* e = std::getenv("PL_WS_WINDOW");  // tuning/debug override of the window width
