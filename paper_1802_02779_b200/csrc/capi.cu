@@ -244,24 +244,39 @@ int num_sms() {
     return sms;
 }
 
-template <class R>
-pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t count, int32_t* status,
-                      cudaStream_t st) {
+template <class R, int N>
+pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st,
+                        const Ptab& pt) {
     using T = typename R::T;
-    Ptab pt;
-    pl_status s = get_ptab(n, &pt);
-    if (s != PL_OK) return s;
-    const size_t smem = smem_per_warp(dt, n) + 32;  // one matrix per CTA
-    auto kern = pl::sz_batch_smem_kernel<R>;
+    const size_t smem = smem_per_warp(dt, N) + 32;  // one matrix per CTA
+    auto kern = pl::sz_batch_smem_kernel<R, N>;
     PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;
     PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     per_sm = std::max(per_sm, 1);
     const int64_t blocks = std::min<int64_t>(count, (int64_t)num_sms() * per_sm);
-    kern<<<(unsigned)blocks, 128, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, n,
-                                              (int)max_layer(n), pt.tab, pt.off, status);
+    kern<<<(unsigned)blocks, 128, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, N,
+                                              (int)max_layer(N), pt.tab, pt.off, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
+}
+
+// 6 <= n <= 14: the shared-memory kernel, specialised per order.
+template <class R>
+pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t count, int32_t* status,
+                      cudaStream_t st) {
+    Ptab pt;
+    pl_status s = get_ptab(n, &pt);
+    if (s != PL_OK) return s;
+    switch (n) {
+#define PL_SMEM_N(NN) \
+    case NN:          \
+        return launch_smem_n<R, NN>(dt, a, out, count, status, st, pt);
+        PL_SMEM_N(6) PL_SMEM_N(7) PL_SMEM_N(8) PL_SMEM_N(9) PL_SMEM_N(10) PL_SMEM_N(11) PL_SMEM_N(12)
+        PL_SMEM_N(13) PL_SMEM_N(14)
+#undef PL_SMEM_N
+    }
+    return fail(PL_ERR_ARG, "shared-memory kernel order out of range");
 }
 
 // Tile schedule of one layer range for the layer kernel: the valid tiles F of

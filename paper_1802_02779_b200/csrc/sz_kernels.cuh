@@ -288,10 +288,12 @@ __device__ __forceinline__ bool i64_fits_f64(const long long* a, int n) {
 }
 
 // The layer DP of one matrix held in shared memory (see sz_batch_smem_kernel).
-template <class RR, class TT>
-__device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, int n,
+// N > 0: the order is a compile-time constant (layer and term loops unroll).
+template <class RR, class TT, int N = 0>
+__device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, int n_rt,
                                              const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff,
                                              bool& ov) {
+    const int n = N > 0 ? N : n_rt;
     const int tid = threadIdx.x, nt = blockDim.x;
     const uint32_t c2 = poff[3] - poff[2];
     for (uint32_t r = tid; r < c2; r += nt) {
@@ -301,8 +303,9 @@ __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, 
     __syncthreads();
     TT* prev = buf0;
     TT* cur = buf1;
+#pragma unroll
     for (int k = 3; k < n; ++k) {
-        const uint32_t ck = (poff[k + 1] - poff[k]) / (uint32_t)k;
+        const uint32_t ck = N > 0 ? (uint32_t)binom_u64(N, k) : (poff[k + 1] - poff[k]) / (uint32_t)k;
         const uint16_t* pt = ptab + poff[k];
         const TT* row = mat + (k - 1) * n;
         for (uint32_t r = tid; r < ck; r += nt) {
@@ -331,10 +334,12 @@ __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, 
     return prev;
 }
 
-template <class RR, class TT>
-__device__ __forceinline__ TT smem_top(const TT* mat, const TT* last_layer, int n, bool& ov) {
+template <class RR, class TT, int N = 0>
+__device__ __forceinline__ TT smem_top(const TT* mat, const TT* last_layer, int n_rt, bool& ov) {
+    const int n = N > 0 ? N : n_rt;
     const TT* last = mat + (n - 1) * n;
     TT total = RR::mul(last[0], last_layer[n - 1], ov);
+#pragma unroll
     for (int j = 1; j < n; ++j) total = RR::mac(total, last[j], last_layer[n - 1 - j], ov);
     return total;
 }
@@ -350,13 +355,14 @@ __device__ __forceinline__ TT smem_top(const TT* mat, const TT* last_layer, int 
 // Integer matrices take one of three exact paths per matrix: doubles with FMA
 // when the guard bound is below 2^53, wrapping int64 below 2^63, checked int64
 // otherwise.
-template <class R>
+template <class R, int N>
 __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
                                                             typename R::T* __restrict__ out, int64_t count,
-                                                            int n, int maxc, const uint16_t* __restrict__ ptab,
+                                                            int n_rt, int maxc, const uint16_t* __restrict__ ptab,
                                                             const uint32_t* __restrict__ poff,
                                                             int32_t* __restrict__ status) {
     using T = typename R::T;
+    constexpr int n = N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int flag, mode;
     T* mat = reinterpret_cast<T*>(smem_raw);
@@ -381,21 +387,21 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
                 double* dm = reinterpret_cast<double*>(mat);
                 for (int e = tid; e < n * n; e += nt) dm[e] = (double)mat[e];
                 __syncthreads();
-                const double* last = smem_dp<RF64<true>>(dm, reinterpret_cast<double*>(buf0),
+                const double* last = smem_dp<RF64<true>, double, N>(dm, reinterpret_cast<double*>(buf0),
                                                          reinterpret_cast<double*>(buf1), n, ptab, poff, ov);
-                if (tid == 0) total = (T)smem_top<RF64<true>>(dm, last, n, ov);
+                if (tid == 0) total = (T)smem_top<RF64<true>, double, N>(dm, last, n, ov);
             } else if (mode == 1) {
-                const T* last = smem_dp<RI64<false>>(mat, buf0, buf1, n, ptab, poff, ov);
-                if (tid == 0) total = smem_top<RI64<false>>(mat, last, n, ov);
+                const T* last = smem_dp<RI64<false>, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
+                if (tid == 0) total = smem_top<RI64<false>, T, N>(mat, last, n, ov);
             } else {
-                const T* last = smem_dp<R>(mat, buf0, buf1, n, ptab, poff, ov);
+                const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
                 if (ov) atomicOr(&flag, 1);
                 __syncthreads();
-                if (tid == 0 && !(flag & 1)) total = smem_top<R>(mat, last, n, ov);
+                if (tid == 0 && !(flag & 1)) total = smem_top<R, T, N>(mat, last, n, ov);
             }
         } else {
-            const T* last = smem_dp<R>(mat, buf0, buf1, n, ptab, poff, ov);
-            if (tid == 0) total = smem_top<R>(mat, last, n, ov);
+            const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
+            if (tid == 0) total = smem_top<R, T, N>(mat, last, n, ov);
         }
         if (tid == 0) {
             if ((flag & 1) || ov) {
