@@ -21,8 +21,9 @@ layer kernel (C4/C5) numbers are visible next to the batched ones.
          reference sources) on a bounded sample, all host threads.
 
 Multi-GPU (torchrun): batches shard by matrix with no collective, each rank a
-full batch (weak scaling); C4/C5 in the suite use the per-layer all-gather
-schedule (sharded.py, strong scaling).
+full batch (weak scaling); C4/C5 in the suite run one matrix on all ranks
+(sharded.py, strong scaling): top-column blocks with point-to-point exchange
+for power-of-two worlds, equal slices with an all-gather otherwise.
 
 --impl reference times the reference's own CPU path (oracle/_ref; the oracle
 port for C5, which the reference cannot run) on this config with all host
@@ -356,6 +357,8 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    from paper_1802_02779_b200.sharded import block_plan_applies
+
     flush_buf = torch.zeros(2, 64 * 1024 * 1024, dtype=torch.float32, device=device)  # 2 x 256 MiB > 126 MB L2
     peak, peak_src = load_peaks()
     traffic = load_traffic()
@@ -372,7 +375,8 @@ def main():
                                "steps": args.steps if name == args.config else k,
                                "time_to_permanent_ms": r["ms_per_step"] if r["spec"]["count"] == 1 else None,
                                "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"],
-                               "sharded_allgather": r["sharded"]}
+                               "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
+                                            else "equal slices, all-gather") if r["sharded"] else None)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

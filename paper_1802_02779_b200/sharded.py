@@ -1,13 +1,24 @@
 """Multi-GPU Store-zechin for large orders: per-layer subset-range sharding.
 
 One process per GPU (torchrun); ``torch.distributed`` over NCCL is the
-plumbing. Every layer k of the DP (subset size k, colex order) is split into
-``world`` equal padded slices of ``L_k = ceil(C(n,k) / world)`` ranks; rank g
-computes ``[g L_k, min((g+1) L_k, C(n,k)))`` with the device layer kernel
-(``pl_sz_layer``) and an in-place all-gather replicates the layer on every
-GPU, because the next layer reads predecessors from the whole previous layer
-(the last slice of layer k needs all of layer k-1). The final n-term
-development runs on every rank from its replicated layer n-1 (``pl_sz_top``).
+plumbing. Two plans, both computing every output once with the device layer
+kernel (``pl_sz_layer`` on a colex-rank range) and ending with the n-term
+development (``pl_sz_top``) on every rank:
+
+* **top-column blocks** (world = 2^t, the default when it applies): rank g
+  owns the k-subsets whose intersection with the top t columns is the pattern
+  P_g = {n - t + i : bit i of g}. In colex order those subsets are ONE
+  contiguous range of C(n - t, k - |P_g|) ranks (the top elements are the most
+  significant), and every predecessor of such a subset lies in block P_g or in
+  a block P_g minus one top column. So after each layer a rank only sends its
+  block to the t - |P_g| ranks g | 2^i and receives the |P_g| blocks of ranks
+  g & ~2^i — point-to-point, about (t / 2) / 2^t of a layer per rank instead of
+  the (2^t - 1) / 2^t an all-gather moves.
+* **equal slices + all-gather** (any world): every layer is split into
+  ``world`` equal padded slices of ``L_k = ceil(C(n,k) / world)`` ranks, rank g
+  computes ``[g L_k, min((g+1) L_k, C(n,k)))`` and an in-place all-gather
+  replicates the layer, because an arbitrary rank range of layer k reads
+  predecessors from all of layer k-1.
 
 Batches are not handled here: they shard trivially by matrix with no
 collective (``bench.py`` gives each rank its contiguous slice).
@@ -70,16 +81,108 @@ class ShardPlan:
         return per, r0, r1
 
 
+def top_columns(world: int) -> int:
+    """t with world = 2^t, or -1 when world is not a power of two."""
+    return world.bit_length() - 1 if world >= 1 and world & (world - 1) == 0 else -1
+
+
+def block_plan_applies(n: int, world: int) -> bool:
+    t = top_columns(world)
+    return t >= 1 and n - t >= 3
+
+
+def top_block(n: int, k: int, world: int, g: int) -> Tuple[int, int]:
+    """Colex-rank range of layer k owned by rank g under the top-column plan:
+    the k-subsets S with S n {n-t..n-1} = P_g. Empty (0, 0) when no such subset."""
+    t = top_columns(world)
+    cols = [n - t + i for i in range(t) if (g >> i) & 1]  # ascending
+    m = k - len(cols)
+    if m < 0 or m > n - t:
+        return 0, 0
+    base = sum(comb(p, m + l + 1) for l, p in enumerate(cols))
+    return base, base + comb(n - t, m)
+
+
+def exchange_blocks(buf: torch.Tensor, n: int, k: int, rank: int, world: int, group=None):
+    """After layer k: hand rank `rank`'s block of layer k to the ranks that add
+    one top column to its pattern, and receive the blocks with one column less."""
+    t = top_columns(world)
+    ops = []
+    for i in range(t):
+        partner = rank ^ (1 << i)
+        if rank >> i & 1:  # receive block P \ {n-t+i}
+            r0, r1 = top_block(n, k, world, partner)
+            if r1 > r0:
+                ops.append(("recv", partner, r0, r1))
+        else:  # send own block to P u {n-t+i}
+            r0, r1 = top_block(n, k, world, rank)
+            if r1 > r0:
+                ops.append(("send", partner, r0, r1))
+    if not ops:
+        return
+    if buf.is_cuda:
+        p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, _as_gather_view(buf[r0:r1]), peer,
+                          group=group) for kind, peer, r0, r1 in ops]
+        for req in dist.batch_isend_irecv(p2p):
+            req.wait()
+    else:
+        reqs = []
+        for kind, peer, r0, r1 in ops:
+            view = _as_gather_view(buf[r0:r1])
+            reqs.append(dist.isend(view, peer, group=group) if kind == "send" else dist.irecv(view, peer, group=group))
+        for req in reqs:
+            req.wait()
+
+
+def gather_last_layer(buf: torch.Tensor, n: int, rank: int, world: int, group=None):
+    """Replicate layer n-1 (n entries) from its owners onto every rank, bit for bit."""
+    k = n - 1
+    mine = torch.zeros(n, dtype=buf.dtype, device=buf.device)
+    r0, r1 = top_block(n, k, world, rank)
+    mine[r0:r1] = buf[r0:r1]
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    if buf.is_cuda:
+        flat = torch.zeros(world * n, dtype=buf.dtype, device=buf.device)
+        dist.all_gather_into_tensor(_as_gather_view(flat), _as_gather_view(mine), group=group)
+        parts = list(flat.chunk(world))
+    else:
+        rp = [_as_gather_view(p) for p in parts]
+        dist.all_gather(rp, _as_gather_view(mine), group=group)
+    for h in range(world):
+        h0, h1 = top_block(n, k, world, h)
+        buf[h0:h1] = parts[h][h0:h1]
+
+
 def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
                      layer_fn: Callable[[int, torch.Tensor, torch.Tensor, int, int], None],
                      top_fn: Callable[[torch.Tensor, torch.Tensor], object],
-                     group=None, on_layer: Callable[[int], None] | None = None):
+                     group=None, on_layer: Callable[[int], None] | None = None, plan: str = "auto"):
     """Run the layer DP of matrix `a` (n x n, already on this rank's device)
     sharded over `world` ranks. `layer_fn(k, prev, cur, r0, r1)` fills
-    cur[r0:r1] of layer k; `top_fn(a, last)` returns the permanent."""
+    cur[r0:r1] of layer k; `top_fn(a, last)` returns the permanent.
+    plan: "blocks" (top-column blocks, world = 2^t), "allgather", or "auto"."""
     n = a.shape[0]
     if n < 3:
         raise ValueError("sharded DP needs n >= 3")
+    if plan == "auto":
+        plan = "blocks" if world > 1 and block_plan_applies(n, world) else "allgather"
+    if plan == "blocks":
+        if not block_plan_applies(n, world):
+            raise ValueError("top-column blocks need world = 2^t with n - t >= 3")
+        size = max(comb(n, k) for k in range(2, n)) + 4
+        bufs = [torch.zeros(size, dtype=a.dtype, device=a.device) for _ in range(2)]
+        prev, cur = bufs
+        for k in range(2, n):
+            r0, r1 = top_block(n, k, world, rank)
+            if r1 > r0:
+                layer_fn(k, prev, cur, r0, r1)
+            if k < n - 1:
+                exchange_blocks(cur, n, k, rank, world, group)
+            if on_layer is not None:
+                on_layer(k)
+            prev, cur = cur, prev
+        gather_last_layer(prev, n, rank, world, group)
+        return top_fn(a, prev)
     size = max_padded_layer(n, world) + 4  # slack: 16-byte aligned ring copies may read one entry past a layer
     bufs = [torch.zeros(size, dtype=a.dtype, device=a.device) for _ in range(2)]
     plan = ShardPlan(n, world, rank)

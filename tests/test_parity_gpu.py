@@ -278,6 +278,50 @@ def test_layer_slices_large_order_bitwise():
             assert torch.equal(cur[: full.numel()], full), (k, world)
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_top_block_plan_on_device_virtual_ranks(world, cplx):
+    # the multi-GPU top-column plan with the device layer kernel: each virtual
+    # rank holds only its block and the blocks it receives (everything else NaN)
+    import torch
+    from math import comb
+
+    from paper_1802_02779_b200.sharded import device_hooks, top_block
+
+    n = 20
+    t = world.bit_length() - 1
+    a_np = configs.complex_uniform((n, n), seed=20 + world) if cplx else configs.uniform((n, n), seed=20 + world)
+    a = torch.from_numpy(a_np).cuda()
+    layer_fn, top_fn = device_hooks(a)
+    size = max(comb(n, k) for k in range(2, n)) + 64
+    nan = complex("nan") if cplx else float("nan")
+    reps = [[torch.full((size,), nan, dtype=a.dtype, device="cuda") for _ in range(2)] for _ in range(world)]
+    for k in range(2, n):
+        for g in range(world):
+            prev, cur = reps[g]
+            cur.fill_(nan)
+            r0, r1 = top_block(n, k, world, g)
+            if r1 > r0:
+                layer_fn(k, prev, cur, r0, r1)
+        if k < n - 1:
+            for g in range(world):
+                for i in range(t):
+                    if g >> i & 1:
+                        h = g ^ (1 << i)
+                        h0, h1 = top_block(n, k, world, h)
+                        reps[g][1][h0:h1] = reps[h][1][h0:h1]
+        for g in range(world):
+            reps[g].reverse()
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    last = reps[0][0].clone()
+    for h in range(world):
+        h0, h1 = top_block(n, n - 1, world, h)
+        last[h0:h1] = reps[h][0][h0:h1]
+    got = complex(top_fn(a, last))
+    want = complex(want)
+    assert (hexf(got.real), hexf(got.imag)) == (hexf(want.real), hexf(want.imag))
+
+
 def test_cpp_device_suite():
     exe = ROOT / "tests" / "cpp" / "test_permanent_device"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)

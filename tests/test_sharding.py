@@ -18,7 +18,10 @@ import torch.multiprocessing as mp
 
 from oracle import oracle as O
 from paper_1802_02779_b200 import configs
-from paper_1802_02779_b200.sharded import layer_slices, max_padded_layer, sharded_layer_dp
+from math import comb
+
+from paper_1802_02779_b200.sharded import (block_plan_applies, layer_slices, max_padded_layer, sharded_layer_dp,
+                                           top_block)
 
 _dp = C.POINTER(C.c_double)
 
@@ -96,6 +99,55 @@ def test_virtual_ranks_bitwise(world, cplx):
     assert values == {want}
 
 
+def test_top_blocks_tile_every_layer():
+    for n in (5, 9, 12, 26, 32, 34):
+        for world in (2, 4, 8, 16):
+            if not block_plan_applies(n, world):
+                continue
+            for k in range(2, n):
+                blocks = sorted(b for b in (top_block(n, k, world, g) for g in range(world)) if b[1] > b[0])
+                assert blocks[0][0] == 0 and blocks[-1][1] == comb(n, k)
+                assert all(blocks[i][1] == blocks[i + 1][0] for i in range(len(blocks) - 1))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_virtual_ranks_top_blocks_bitwise(world, cplx):
+    # each rank computes only its block and only receives the blocks with one
+    # top column less: a rank must never read a predecessor it was not sent
+    n = 11
+    t = world.bit_length() - 1
+    a_np = configs.complex_uniform((n, n), seed=17) if cplx else configs.uniform((n, n), seed=17)
+    a = torch.from_numpy(a_np)
+    layer_fn, top_fn = cpu_hooks(a)
+    size = max(comb(n, k) for k in range(2, n)) + 4
+    nan = complex("nan") if cplx else float("nan")
+    replicas = [[torch.full((size,), nan, dtype=a.dtype) for _ in range(2)] for _ in range(world)]
+    for k in range(2, n):
+        for g in range(world):
+            prev, cur = replicas[g]
+            cur.fill_(nan)  # whatever this rank does not own or receive stays NaN
+            r0, r1 = top_block(n, k, world, g)
+            if r1 > r0:
+                layer_fn(k, prev, cur, r0, r1)
+        if k < n - 1:
+            for g in range(world):  # point-to-point: g receives from g & ~2^i
+                for i in range(t):
+                    if g >> i & 1:
+                        h = g ^ (1 << i)
+                        h0, h1 = top_block(n, k, world, h)
+                        replicas[g][1][h0:h1] = replicas[h][1][h0:h1]
+        for g in range(world):
+            replicas[g].reverse()
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    for g in range(world):
+        last = replicas[g][0].clone()
+        for h in range(world):  # the final gather of layer n-1
+            h0, h1 = top_block(n, n - 1, world, h)
+            last[h0:h1] = replicas[h][0][h0:h1]
+        assert top_fn(a, last) == want
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -116,7 +168,7 @@ def _worker(rank, world, port, n, cplx, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])  # 2, 4: top-column blocks; 3: all-gather
 @pytest.mark.parametrize("cplx", [False, True])
 def test_gloo_sharded_dp_bitwise(world, cplx):
     n = 12
