@@ -172,6 +172,10 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
         size = max(comb(n, k) for k in range(2, n)) + 4
         bufs = [torch.zeros(size, dtype=a.dtype, device=a.device) for _ in range(2)]
         prev, cur = bufs
+        if world > 1 and a.is_cuda:
+            # NCCL: batched P2P among a subset of ranks is only defined once the
+            # group has run a collective
+            dist.barrier(group=group)
         for k in range(2, n):
             r0, r1 = top_block(n, k, world, rank)
             if r1 > r0:
