@@ -476,10 +476,22 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         PL_CUDA(cudaMemset(trace, 0, tb));
         PL_CUDA(cudaMemcpyToSymbol(pl::g_ws_trace, &trace, sizeof(trace)));
     }
-    kern<<<grid, pl::WsGeom<(int)sizeof(T)>::kThreads, smem, st>>>(static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                                                  static_cast<T*>(cur), r0, r1, sched, q.ltab, q.offs,
-                                                  q.binom_pairs, guard, status, ws_hints(), team);
-    PL_CUDA(cudaGetLastError());
+    // programmatic dependent launch (see sz_ws_kernel): the grid's prologue
+    // overlaps the tail of whatever precedes it on the stream
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(pl::WsGeom<(int)sizeof(T)>::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
+                               static_cast<T*>(cur), r0, r1, sched, static_cast<const uint4*>(q.ltab),
+                               static_cast<const uint32_t*>(q.offs), static_cast<const uint2*>(q.binom_pairs),
+                               guard, status, ws_hints(), team));
     if (trace) {
         PL_CUDA(cudaStreamSynchronize(st));
         std::vector<unsigned long long> hb((size_t)4 * pl::kWsTraceCap * 2);

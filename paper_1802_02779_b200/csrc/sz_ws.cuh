@@ -566,9 +566,12 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* row = a + (size_t)(k - 1) * n;
 
+    // Programmatic dependent launch: the next layer's grid may be scheduled as
+    // soon as SMs free up; this grid's prologue (engine tables, barriers)
+    // overlaps the previous layer's tail, and nothing it reads or writes in the
+    // layer buffers (or the matrix) is touched before griddepcontrol.wait.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) sm.B2[e] = __ldg(&binom_pairs[e]);
-    for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
-    for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
     for (int v = threadIdx.x; v <= D; v += blockDim.x) qoff_sh[v] = __ldg(qtab_off + v);
     if (threadIdx.x == 0) {
         for (int s = 0; s < G * NSG; ++s) {
@@ -581,6 +584,9 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous layer is complete and visible
+    for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
+    for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
     __syncthreads();
 
     const int nteams = (int)gridDim.x / tP;
