@@ -116,7 +116,8 @@ struct WsGeom {
     static constexpr int CHUNK = LANES * PER;                         // CH: outputs per chunk
     static constexpr int NSG = ELEM == 16 ? PL_WS_NSG16 : PL_WS_NSG8;     // stages per group ring
     static constexpr int FS = ELEM == 16 ? PL_WS_FS16 : PL_WS_FS8;        // stream segments per ring stage
-    static constexpr int NSRC = ELEM == 16 ? PL_WS_NSRC16 : PL_WS_NSRC8;  // tile slots (header + low source)
+    static constexpr int NSRC = ELEM == 16 ? PL_WS_NSRC16 : PL_WS_NSRC8;  // low-source ring, in largest tiles
+    static constexpr int NHDR = 8;                                        // tile headers in flight
     // elements per low-source slot: the largest tile source C(D, D/2), plus the
     // 8-byte alignment pad and round-up of bulk_span
     static constexpr int kSrcSlot =
@@ -136,9 +137,10 @@ struct WsHdr {
     uint64_t cur_base;               // rank of the tile's first output
     uint32_t qoff, pad_src;          // ltab offset for m; 8-byte alignment pad of the source
     uint32_t padmask;                // bit l: 8-byte alignment pad of stream l's chunks (cb, cs even)
+    uint32_t src_off, src_len;       // the low source's place in the source ring (elements)
     T coef[kWsMaxHigh];              // a(k-1, F_l)
     uint64_t sbase[kWsMaxHigh];      // base rank of stream tile (F \ {F_l}, k-1)
-    int32_t mode[kWsMaxHigh];        // L2 policy of stream l (0 plain, 1 evict-first, 2 evict-last)
+    int8_t mode[kWsMaxHigh];         // L2 policy of stream l (0 plain, 1 evict-first, 2 evict-last)
 };
 
 template <class T>
@@ -147,7 +149,9 @@ struct WsSmem {
     static constexpr int G = WsGeom<(int)sizeof(T)>::G;
     static constexpr int CW = WsGeom<(int)sizeof(T)>::kConsumerWarps;
     static constexpr int NSRC = WsGeom<(int)sizeof(T)>::NSRC;
+    static constexpr int NHDR = WsGeom<(int)sizeof(T)>::NHDR;
     static constexpr int kSrcSlot = WsGeom<(int)sizeof(T)>::kSrcSlot;
+    static constexpr uint32_t kSrcRing = (uint32_t)NSRC * kSrcSlot;  // ring elements (even)
     static constexpr int FS = WsGeom<(int)sizeof(T)>::FS;
     static constexpr int GW = WsGeom<(int)sizeof(T)>::GW;
     static constexpr int PER = WsGeom<(int)sizeof(T)>::PER;
@@ -159,15 +163,15 @@ struct WsSmem {
     uint64_t* full;       // [G][NSG]
     uint64_t* empty;      // [G][NSG]
     T* stage;             // [G][NSG][FS][kSlot]
-    uint64_t* src_full;   // [NSRC]
-    uint64_t* src_empty;  // [NSRC]
-    WsHdr<T>* hdr;        // [NSRC]
-    T* src;               // [NSRC][kSrcSlot]  tile low sources X(F, k-1)
+    uint64_t* src_full;   // [NHDR]
+    uint64_t* src_empty;  // [NHDR]
+    WsHdr<T>* hdr;        // [NHDR]
+    T* src;               // [kSrcRing]  ring of tile low sources X(F, k-1), variable size
 
     __host__ __device__ static size_t bytes() {
         return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) + round16(8 * 2 * G * NSG) +
-               round16((size_t)G * NSG * FS * kSlot * sizeof(T)) + round16(8 * 2 * NSRC) +
-               round16(sizeof(WsHdr<T>) * NSRC) + round16((size_t)NSRC * kSrcSlot * sizeof(T));
+               round16((size_t)G * NSG * FS * kSlot * sizeof(T)) + round16(8 * 2 * NHDR) +
+               round16(sizeof(WsHdr<T>) * NHDR) + round16((size_t)kSrcRing * sizeof(T));
     }
     __device__ explicit WsSmem(unsigned char* base) {
         size_t off = 0;
@@ -182,10 +186,10 @@ struct WsSmem {
         full = bars;
         empty = bars + G * NSG;
         stage = reinterpret_cast<T*>(take((size_t)G * NSG * FS * kSlot * sizeof(T)));
-        src_full = reinterpret_cast<uint64_t*>(take(8 * 2 * NSRC));
-        src_empty = src_full + NSRC;
-        hdr = reinterpret_cast<WsHdr<T>*>(take(sizeof(WsHdr<T>) * NSRC));
-        src = reinterpret_cast<T*>(take((size_t)NSRC * kSrcSlot * sizeof(T)));
+        src_full = reinterpret_cast<uint64_t*>(take(8 * 2 * NHDR));
+        src_empty = src_full + NHDR;
+        hdr = reinterpret_cast<WsHdr<T>*>(take(sizeof(WsHdr<T>) * NHDR));
+        src = reinterpret_cast<T*>(take((size_t)kSrcRing * sizeof(T)));
     }
     __device__ T* slot(int g, int s, int li) const { return stage + (((size_t)g * NSG + s) * FS + li) * kSlot; }
     __device__ uint64_t* full_bar(int g, int s) const { return full + g * NSG + s; }
@@ -554,7 +558,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                  int32_t* __restrict__ status, uint32_t hints, int tP) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
-    constexpr int NSRC = WsSmem<T>::NSRC;
+    constexpr int NHDR = WsSmem<T>::NHDR;
+    constexpr uint32_t SR = WsSmem<T>::kSrcRing;
     constexpr int G = WsSmem<T>::G;
     constexpr int CW = WsSmem<T>::CW;
     constexpr int FS = WsSmem<T>::FS;
@@ -578,7 +583,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             mbar_init(&sm.full[s], 1);               // the group's streamer: arrive.expect_tx
             mbar_init(&sm.empty[s], GW);  // the group's consumer warps
         }
-        for (int s = 0; s < NSRC; ++s) {
+        for (int s = 0; s < NHDR; ++s) {
             mbar_init(&sm.src_full[s], 1);        // publisher: arrive.expect_tx
             mbar_init(&sm.src_empty[s], CW + G);  // every consumer and streamer warp, once per tile
         }
@@ -598,7 +603,35 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         // the next tile slot; a terminal header ends the sequence.
         WsCursor lst = ws_cursor(sched, nteams, (int)blockIdx.x % nteams);
         const int H = n - D;
-        uint32_t pub = 0;
+        uint32_t pub = 0, rel = 0;   // tiles published / tiles whose release this warp has seen
+        uint32_t head = 0, tail = 0; // source ring: end of the newest, start of the oldest in-flight source
+        // wait until tile `rel` is released by every consumer and streamer warp
+        auto release_one = [&]() {
+            mbar_wait_slot(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u);
+            ++rel;
+            tail = rel < pub ? sm.hdr[rel % NHDR].src_off : head;
+        };
+        // place a source of L elements in the ring (FIFO; a source never wraps)
+        auto alloc = [&](uint32_t L) -> uint32_t {
+            for (;;) {
+                if (pub - rel >= (uint32_t)NHDR) {  // header slot of tile pub still in use
+                    release_one();
+                    continue;
+                }
+                if (pub == rel) {
+                    head = tail = 0;
+                    return 0;
+                }
+                if (L == 0) return head;
+                if (tail < head) {  // in flight: [tail, head)
+                    if (head + L <= SR) return head;
+                    if (L <= tail) return 0;
+                } else if (head + L <= tail) {  // in flight: [tail, SR) u [0, head)
+                    return head;
+                }
+                release_one();
+            }
+        };
         WsTrace tr;
         tr.init(3);
         uint32_t F_next = lst.pos < lst.end ? __ldg(lst.list + lst.pos) : 0u;
@@ -630,12 +663,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             const uint32_t nchunks = total > (uint32_t)tp ? (total - tp + tP - 1) / tP : 0u;
             if (nchunks == 0) continue;
 
-            const int ss = (int)(pub % NSRC);
+            // the low source X(F, k-1): C(D, m-1) entries (+ alignment pad and round-up)
+            const uint32_t slen = m >= 1 ? sm.B2[(m - 1) * kBinomDim + D].x : 0u;
+            const uint32_t salloc = slen ? (sizeof(T) == 16 ? slen : (slen + 3u) & ~1u) : 0u;
+            const int ss = (int)(pub % NHDR);
             tr.ev(8, pub);
-            if constexpr (kPubSleepNs == 0)
-                mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
-            else
-                mbar_wait_backoff(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u, kPubSleepNs);
+            const uint32_t soff = alloc(salloc);
+            head = soff + salloc;
             tr.ev(9, pub);
             ++pub;
             WsHdr<T>& h = sm.hdr[ss];
@@ -666,6 +700,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 h.cur_base = cur_base;
                 h.qoff = qoff_sh[m];
                 h.pad_src = sizeof(T) == 16 ? 0u : (uint32_t)(src_base & 1u);
+                h.src_off = soff;
+                h.src_len = salloc;
             }
             {
                 // chunk starts cb + i * cs share cb's parity (cs is even)
@@ -676,15 +712,14 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
-                const uint32_t slen = m >= 1 ? sm.B2[(m - 1) * kBinomDim + D].x : 0u;
                 const BulkSpan<T> sp = slen ? bulk_span(prev, src_base, slen) : BulkSpan<T>{prev, 0u, 0};
                 mbar_arrive_expect_tx(&sm.src_full[ss], sp.bytes);
-                if (sp.bytes) bulk_g2s(sm.src + (size_t)ss * WsSmem<T>::kSrcSlot, sp.src, sp.bytes, &sm.src_full[ss]);
+                if (sp.bytes) bulk_g2s(sm.src + soff, sp.src, sp.bytes, &sm.src_full[ss]);
             }
             __syncwarp();
         }
-        const int ss = (int)(pub % NSRC);
-        mbar_wait_slot(&sm.src_empty[ss], ((pub / NSRC) & 1u) ^ 1u);
+        while (pub - rel >= (uint32_t)NHDR) release_one();
+        const int ss = (int)(pub % NHDR);
         if (lane == 0) {
             sm.hdr[ss].m = kWsEnd;
             __threadfence_block();
@@ -699,8 +734,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         WsTrace tr;
         if (g == 0) tr.init(2);
         for (uint32_t ts = 0;; ++ts) {
-            const int ss = (int)(ts % NSRC);
-            mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
+            const int ss = (int)(ts % NHDR);
+            mbar_wait_slot(&sm.src_full[ss], (ts / NHDR) & 1u);
             const WsHdr<T>& h = sm.hdr[ss];
             if (h.m < 0) break;
             const int f = h.f;
@@ -760,9 +795,9 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         WsTrace tr;
         if (warp % GW == 0 && warp / GW < 2) tr.init(warp / GW);
         for (uint32_t ts = 0;; ++ts) {
-            const int ss = (int)(ts % NSRC);
+            const int ss = (int)(ts % NHDR);
             tr.ev(1, ts);
-            mbar_wait_slot(&sm.src_full[ss], (ts / NSRC) & 1u);
+            mbar_wait_slot(&sm.src_full[ss], (ts / NHDR) & 1u);
             tr.ev(2, ts);
             const WsHdr<T>& h = sm.hdr[ss];
             if (h.m < 0) break;
@@ -772,7 +807,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             gchunk += nchunks;
             if (c_first < nchunks) {
                 const uint4* qt = qtab + h.qoff;
-                const T* src = sm.src + (size_t)ss * WsSmem<T>::kSrcSlot + h.pad_src;
+                const T* src = sm.src + h.src_off + h.pad_src;
                 if constexpr (R::kChecked) {
                     if (use_checked) {
                         ws_consume_dispatch<R>(sm, h, src, qt, cur, g, j, c_first, seq, ov, hints, tr);
