@@ -48,6 +48,10 @@ namespace pl {
 constexpr int kWsMaxHigh = 32;                 // high columns per tile (n - D <= 31)
 constexpr int kWsLtabRankBits = 12;           // ltab entry: rank_D(V \ {v}) | v << 12 (D <= 14)
 constexpr int kWsEnd = -1;
+#ifndef PL_WS_LOW_INTERLEAVE
+#define PL_WS_LOW_INTERLEAVE 0
+#endif
+constexpr bool kWsLowInterleave = PL_WS_LOW_INTERLEAVE;  // large m: low terms of both outputs term by term
 constexpr int kWaitHintNs = 20000;             // mbarrier try_wait suspend-time hint
 #ifndef PL_WS_PSLEEP
 #define PL_WS_PSLEEP 0
@@ -74,7 +78,7 @@ constexpr unsigned kPubSleepNs = PL_WS_PUBSLEEP;    // max poll sleep of publish
 #define PL_WS_NSG8 2
 #endif
 #ifndef PL_WS_FS16
-#define PL_WS_FS16 3
+#define PL_WS_FS16 4
 #endif
 #ifndef PL_WS_FS8
 #define PL_WS_FS8 4
@@ -86,16 +90,22 @@ constexpr unsigned kPubSleepNs = PL_WS_PUBSLEEP;    // max poll sleep of publish
 #define PL_WS_NSRC8 3
 #endif
 #ifndef PL_WS_G16
-#define PL_WS_G16 2
+#define PL_WS_G16 3
 #endif
 #ifndef PL_WS_G8
 #define PL_WS_G8 3
 #endif
 #ifndef PL_WS_GW16
-#define PL_WS_GW16 8
+#define PL_WS_GW16 4
 #endif
 #ifndef PL_WS_GW8
 #define PL_WS_GW8 8
+#endif
+#ifndef PL_WS_NST16
+#define PL_WS_NST16 3
+#endif
+#ifndef PL_WS_NST8
+#define PL_WS_NST8 3
 #endif
 #ifndef PL_WS_PER16
 #define PL_WS_PER16 2
@@ -123,7 +133,10 @@ struct WsGeom {
     static constexpr int kSrcSlot =
         (int)((binom_u64(ws_window(ELEM), ws_window(ELEM) / 2) + 2 + 16 / ELEM - 1) / (16 / ELEM) * (16 / ELEM));
     static constexpr int kConsumerWarps = GW * G;
-    static constexpr int kThreads = 32 * (kConsumerWarps + G + 1);  // consumers, G streamers, publisher
+    static constexpr int NST = ELEM == 16 ? PL_WS_NST16 : PL_WS_NST8;  // streamer warps (streamer s feeds groups g = s mod NST)
+    static constexpr int kThreads = 32 * (kConsumerWarps + NST + 1);    // consumers, streamers, publisher
+    // registers per thread that still fit one CTA per SM (64K registers, 8-register units)
+    static constexpr int kMaxReg = (65536 / kThreads) / 8 * 8 > 255 ? 255 : (65536 / kThreads) / 8 * 8;
 };
 
 __host__ __device__ constexpr size_t round16(size_t b) { return (b + 15) & ~size_t(15); }
@@ -154,6 +167,7 @@ struct WsSmem {
     static constexpr uint32_t kSrcRing = (uint32_t)NSRC * kSrcSlot;  // ring elements (even)
     static constexpr int FS = WsGeom<(int)sizeof(T)>::FS;
     static constexpr int GW = WsGeom<(int)sizeof(T)>::GW;
+    static constexpr int NST = WsGeom<(int)sizeof(T)>::NST;
     static constexpr int PER = WsGeom<(int)sizeof(T)>::PER;
     static constexpr int LANES = WsGeom<(int)sizeof(T)>::LANES;
     static constexpr int CHUNK = WsGeom<(int)sizeof(T)>::CHUNK;
@@ -163,14 +177,15 @@ struct WsSmem {
     uint64_t* full;       // [G][NSG]
     uint64_t* empty;      // [G][NSG]
     T* stage;             // [G][NSG][FS][kSlot]
-    uint64_t* src_full;   // [NHDR]
-    uint64_t* src_empty;  // [NHDR]
+    uint64_t* src_full;   // [NHDR]  header written and low source landed (consumers)
+    uint64_t* src_empty;  // [NHDR]  tile released by every consumer and streamer warp
+    uint64_t* hdr_full;   // [NHDR]  header written (streamers: they need no source)
     WsHdr<T>* hdr;        // [NHDR]
     T* src;               // [kSrcRing]  ring of tile low sources X(F, k-1), variable size
 
     __host__ __device__ static size_t bytes() {
         return round16(sizeof(uint2) * kBinomDim * kBinomDim) + round16(sizeof(T) * 32) + round16(8 * 2 * G * NSG) +
-               round16((size_t)G * NSG * FS * kSlot * sizeof(T)) + round16(8 * 2 * NHDR) +
+               round16((size_t)G * NSG * FS * kSlot * sizeof(T)) + round16(8 * 3 * NHDR) +
                round16(sizeof(WsHdr<T>) * NHDR) + round16((size_t)kSrcRing * sizeof(T));
     }
     __device__ explicit WsSmem(unsigned char* base) {
@@ -186,8 +201,9 @@ struct WsSmem {
         full = bars;
         empty = bars + G * NSG;
         stage = reinterpret_cast<T*>(take((size_t)G * NSG * FS * kSlot * sizeof(T)));
-        src_full = reinterpret_cast<uint64_t*>(take(8 * 2 * NHDR));
+        src_full = reinterpret_cast<uint64_t*>(take(8 * 3 * NHDR));
         src_empty = src_full + NHDR;
+        hdr_full = src_full + 2 * NHDR;
         hdr = reinterpret_cast<WsHdr<T>*>(take(sizeof(WsHdr<T>) * NHDR));
         src = reinterpret_cast<T*>(take((size_t)kSrcRing * sizeof(T)));
     }
@@ -421,6 +437,25 @@ __device__ __forceinline__ T ws_low(const uint4& ea, const uint4& eb, const T* _
     return acc;
 }
 
+// Low terms of all PER outputs of a thread, term by term (the register
+// footprint stays bounded for large m; the scheduler still runs ahead on the
+// independent shared-memory loads).
+template <class RR, int M, int PER, class T>
+__device__ __forceinline__ void ws_low_interleaved(const uint4 (&ea)[PER], const uint4 (&eb)[PER],
+                                                   const T* __restrict__ src, const T* __restrict__ row_low,
+                                                   T (&acc)[PER], bool (&ov)[PER]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            const uint32_t e = ltab_entry(ea[p], eb[p], i);
+            const T x = src[e & ((1u << kWsLtabRankBits) - 1)];
+            const T c = row_low[e >> kWsLtabRankBits];
+            acc[p] = i == 0 ? RR::mul(c, x, ov[p]) : RR::mac(acc[p], c, x, ov[p]);
+        }
+    }
+}
+
 // Consumer group g's share of one tile: its chunks c_first, c_first + G, ...
 // (chunks are dealt to groups round-robin over the CTA's whole tile sequence).
 // Each chunk takes ceil(f / FS) consecutive stages of the group's own ring;
@@ -473,7 +508,13 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
         for (int p = 0; p < PER; ++p) {
             lov[p] = false;
             acc[p] = RR::zero();
-            if constexpr (M >= 1) acc[p] = ws_low<RR, M>(ea[p], eb[p], src, sm.row_low, lov[p]);
+        }
+        if constexpr (M >= 1) {
+            if constexpr (kWsLowInterleave && (sizeof(T) == 16 ? M > 6 : M > 10))
+                ws_low_interleaved<RR, M, PER>(ea, eb, src, sm.row_low, acc, lov);
+            else
+#pragma unroll
+                for (int p = 0; p < PER; ++p) acc[p] = ws_low<RR, M>(ea[p], eb[p], src, sm.row_low, lov[p]);
         }
         for (int l0 = 0; l0 < f; l0 += FS, ++seq) {
             const int nl = min(FS, f - l0);
@@ -551,7 +592,7 @@ __device__ __forceinline__ void ws_consume_dispatch(const WsSmem<T>& sm, const W
 
 template <class R, class RU>
 __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 1)
-    sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
+    __maxnreg__(WsGeom<(int)sizeof(typename R::T)>::kMaxReg) sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                  typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ sched,
                  const uint4* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
                  const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
@@ -585,7 +626,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         }
         for (int s = 0; s < NHDR; ++s) {
             mbar_init(&sm.src_full[s], 1);        // publisher: arrive.expect_tx
-            mbar_init(&sm.src_empty[s], CW + G);  // every consumer and streamer warp, once per tile
+            mbar_init(&sm.hdr_full[s], 1);        // publisher: arrive
+            mbar_init(&sm.src_empty[s], CW + WsSmem<T>::NST);  // every consumer and streamer warp, once per tile
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -596,7 +638,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
 
     const int nteams = (int)gridDim.x / tP;
     const int tp = (int)blockIdx.x / nteams;
-    if (warp == CW + G) {
+    if (warp == CW + WsSmem<T>::NST) {
         // ------------------------------------------------------------ publisher
         // Walks the CTA's tile list; per tile with work for this CTA it builds
         // the header (two warp scans, no loops) and stages the low source into
@@ -713,6 +755,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             if (lane == 0) {
                 __threadfence_block();
                 const BulkSpan<T> sp = slen ? bulk_span(prev, src_base, slen) : BulkSpan<T>{prev, 0u, 0};
+                mbar_arrive(&sm.hdr_full[ss]);  // the streamers may start on the tile now
                 mbar_arrive_expect_tx(&sm.src_full[ss], sp.bytes);
                 if (sp.bytes) bulk_g2s(sm.src + soff, sp.src, sp.bytes, &sm.src_full[ss]);
             }
@@ -723,28 +766,35 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         if (lane == 0) {
             sm.hdr[ss].m = kWsEnd;
             __threadfence_block();
+            mbar_arrive(&sm.hdr_full[ss]);
             mbar_arrive(&sm.src_full[ss]);
         }
     } else if (warp >= CW) {
-        // ------------------------------------------------------------ streamer of group g
-        // Streams the high-term segments of group g's chunks into its ring.
-        const int g = warp - CW;
+        // ------------------------------------------------------------ streamers
+        // Streamer s streams the high-term segments of the chunks of groups
+        // g = s mod NST into their rings.
+        constexpr int NST = WsSmem<T>::NST;
+        const int sid = warp - CW;
         const uint64_t pol_first = l2_evict_first_policy(), pol_last = l2_evict_last_policy();
-        uint32_t sq = 0, gchunk = 0;
+        uint32_t sqg[G] = {};
+        uint32_t gchunk = 0;
         WsTrace tr;
-        if (g == 0) tr.init(2);
+        if (sid == 0) tr.init(2);
         for (uint32_t ts = 0;; ++ts) {
             const int ss = (int)(ts % NHDR);
-            mbar_wait_slot(&sm.src_full[ss], (ts / NHDR) & 1u);
+            mbar_wait_slot(&sm.hdr_full[ss], (ts / NHDR) & 1u);
             const WsHdr<T>& h = sm.hdr[ss];
             if (h.m < 0) break;
             const int f = h.f;
             const uint32_t nchunks = h.nchunks, cb = h.cb, cs = h.cs, q1 = h.q1;
             uint64_t base = 0;
             int mode = 0;
-            const uint32_t c_first = (uint32_t)((g - (int)(gchunk % G) + G) % G);
+            const int g0 = (int)(gchunk % G);
             gchunk += nchunks;
-            for (uint32_t c = c_first; c < nchunks; c += G) {
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                const int g = (g0 + (int)(c % G)) % G;
+                if (g % NST != sid) continue;
+                uint32_t& sq = sqg[g];
                 const uint32_t c0 = cb + c * cs;
                 const uint32_t clen = min((uint32_t)CHUNK, q1 - c0);
                 if ((hints & 0x20000u) && c + G < nchunks && lane < f) {
