@@ -345,11 +345,11 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int
 // L2 hint mode of the layer kernel (bits 0-1 stream policy: 0 none, 1 evict-first beyond
 // the reuse horizon, 2 + evict-last within it; bit 2 evict-first output stores; bits 8-15
 // log2 of the horizon in tiles; bits 4+ are timing probes, see sz_ws.cuh). Default: far
-// streams and output stores evict-first, horizon 2^7 tiles. PL_WS_HINTS overrides it.
+// streams and output stores evict-first, horizon 2^9 tiles. PL_WS_HINTS overrides it.
 uint32_t ws_hints() {
     static const uint32_t h = [] {
         const char* e = std::getenv("PL_WS_HINTS");
-        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0x705u;
+        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0x905u;
     }();
     return h;
 }
