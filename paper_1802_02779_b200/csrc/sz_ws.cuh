@@ -649,7 +649,11 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         uint32_t head = 0, tail = 0; // source ring: end of the newest, start of the oldest in-flight source
         // wait until tile `rel` is released by every consumer and streamer warp
         auto release_one = [&]() {
-            mbar_wait_slot(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u);
+            // the publisher runs up to NHDR tiles ahead: it may poll lazily
+            if constexpr (kPubSleepNs == 0)
+                mbar_wait_slot(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u);
+            else
+                mbar_wait_backoff(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u, kPubSleepNs);
             ++rel;
             tail = rel < pub ? sm.hdr[rel % NHDR].src_off : head;
         };
