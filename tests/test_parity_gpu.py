@@ -204,6 +204,24 @@ def test_c5_row_linearity():
     assert abs(pb + pc - pa) <= 1e-9 * max(abs(pa), abs(pb), abs(pc))
 
 
+@pytest.mark.parametrize("n,cplx", [(33, False), (34, True)])
+def test_max_orders_power_of_two_scaling_bitwise(n, cplx):
+    # the order cap (n = 34, C(34,17) < 2^32 colex ranks): scaling one row by 2 scales
+    # every partial sum touching it by 2 exactly, so the permanent doubles bit for bit;
+    # a row swap leaves the result unchanged up to summation order (<= 1e-9)
+    a = configs.uniform((n, n), seed=n) * 0.3
+    if cplx:
+        a = a + 1j * configs.uniform((n, n), seed=n + 1) * 0.3
+    b = a.copy()
+    b[n // 2] *= 2.0
+    pa = complex(pl.store_zechin_permanent(a).value)
+    pb = complex(pl.store_zechin_permanent(b).value)
+    assert (hexf(pb.real), hexf(pb.imag)) == (hexf(2 * pa.real), hexf(2 * pa.imag))
+    c = a[:, ::-1].copy()  # column reversal: a different summation order, same value
+    pc = complex(pl.store_zechin_permanent(c).value)
+    assert abs(pc - pa) <= 1e-9 * abs(pa)
+
+
 # ---------------------------------------------------------------- device pointers / layer primitives
 
 def test_torch_device_batch_and_async_status():
