@@ -164,7 +164,11 @@ struct WsSmem {
     static constexpr int NSRC = WsGeom<(int)sizeof(T)>::NSRC;
     static constexpr int NHDR = WsGeom<(int)sizeof(T)>::NHDR;
     static constexpr int kSrcSlot = WsGeom<(int)sizeof(T)>::kSrcSlot;
+#ifdef PL_WS_SRCRING_PCT  // ring size in percent of NSRC largest sources (tuning)
+    static constexpr uint32_t kSrcRing = ((uint32_t)NSRC * kSrcSlot * PL_WS_SRCRING_PCT / 100) & ~1u;
+#else
     static constexpr uint32_t kSrcRing = (uint32_t)NSRC * kSrcSlot;  // ring elements (even)
+#endif
     static constexpr int FS = WsGeom<(int)sizeof(T)>::FS;
     static constexpr int GW = WsGeom<(int)sizeof(T)>::GW;
     static constexpr int NST = WsGeom<(int)sizeof(T)>::NST;
