@@ -10,9 +10,9 @@
 // so the k-subsets sharing F form one contiguous colex range, the tile (F, k),
 // of C(D, m) entries indexed by q = rank_D(V). Output q needs
 //   * low terms  S \ {v_i}: inside the tile's low source (F, k-1), C(D, m-1)
-//     contiguous entries staged whole in shared memory by one bulk copy;
-//     rank_D(V \ {v_i}) = P_i + Q_i (P_i = sum_{l<i} C(v_l, l),
-//     Q_i = sum_{l>i} C(v_l, l-1)), one paired-binomial lookup per term;
+//     contiguous entries staged whole in shared memory by one bulk copy; the
+//     ranks rank_D(V \ {v_i}) and columns v_i come from the host-built low-term
+//     table (ltab: one 16-byte load per output for m <= 8);
 //   * high terms S \ {F_l}: entry q of the tile (F \ {F_l}, k-1) -> aligned
 //     contiguous streams with a tile-uniform coefficient, staged by TMA.
 // Low columns are all below high columns, so "low ascending, then high
@@ -22,21 +22,27 @@
 // Schedule. One CTA per SM, persistent. The host deals the layer's tiles, in
 // increasing F (increasing colex order), to the least-loaded CTA, so the GPU
 // sweeps each layer as one tight front and stream tiles of nearby high columns
-// are re-read from L2.
+// are re-read from L2 (far ones are loaded evict-first). Launched with
+// programmatic dependent launch: the prologue overlaps the previous layer.
 //
-// Roles.
-//   last warp, producer  walks the CTA's tile list. Per tile it builds the
-//                        tile header (bases, clip range, coefficients, stream
-//                        bases: two warp scans, no loops), publishes it with
-//                        the tile's low source in one of NSRC source slots,
-//                        then streams the high-term segments of every chunk of
-//                        CH outputs into the owning consumer group's NSG-stage
-//                        ring, FS segments per stage, one cp.async.bulk per
-//                        segment, completion by mbarrier transaction counts.
-//   consumer warps       G groups of 8 warps taking alternate chunks, two
-//                        outputs per thread: low terms from the source slot,
-//                        high terms from the group's ring, coalesced store.
-//                        They read everything about a tile from its header.
+// Roles (warp-specialised, mbarrier hand-offs, no CTA-wide sync after setup).
+//   publisher (last warp)  walks the CTA's tile list; per tile builds the
+//                          header (bases and clip range by two warp scans,
+//                          coefficients, stream bases, pad mask), places the
+//                          tile's low source in a variable-size shared-memory
+//                          ring (FIFO, up to NHDR = 8 tiles in flight) and
+//                          stages it with one cp.async.bulk.
+//   streamers (NST warps)  for the chunks (CH outputs) of their consumer
+//                          groups, stream the high-term segments into the
+//                          group's NSG-stage ring, FS segments per stage, one
+//                          cp.async.bulk per segment, mbarrier tx counts.
+//   consumers (G groups    take alternate chunks, PER outputs per thread: low
+//   of GW warps)           terms from the source ring, high terms from the
+//                          group's ring (read to registers, slot handed back,
+//                          then the math), coalesced stores. The chunk loop is
+//                          specialised per low count m.
+// Geometry per element size (WsGeom): complex 3 groups x 4 warps, D = 14,
+// FS = 4; 8-byte 3 groups x 8 warps, D = 14, FS = 4.
 #pragma once
 
 #include <cstdint>
