@@ -14,12 +14,22 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude
 CUDA_HOME ?= /usr/local/cuda
 
-KERNEL_HDRS := $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh $(wildcard $(CSRC)/*.cuh) include/permlab_b200.h
+KERNEL_HDRS := $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh $(CSRC)/sz_ws.cuh $(CSRC)/sz_batch.cuh $(CSRC)/capi_internal.h include/permlab_b200.h
 
 all: $(PKG)/libpermlab_b200.so $(PKG)/libpermlab_gen.so $(PKG)/libpermlab.so tests/cpp/test_permanent_device oracle
 
-$(PKG)/libpermlab_b200.so: $(CSRC)/capi.cu $(KERNEL_HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/capi.cu -lcudart
+BUILD := build
+
+$(BUILD)/capi.o: $(CSRC)/capi.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/capi.cu
+
+$(BUILD)/boson.o: $(CSRC)/boson.cu $(CSRC)/sz_boson.cuh $(CSRC)/capi_internal.h $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh include/permlab_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/boson.cu
+
+$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/boson.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c
 	gcc -O2 -fPIC -ffp-contract=off -std=gnu11 -Wall -shared -o $@ $< -lm
@@ -39,6 +49,7 @@ sass: $(PKG)/libpermlab_b200.so
 
 clean:
 	rm -f $(PKG)/*.so tests/cpp/test_permanent_device
+	rm -rf $(BUILD)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean sass

@@ -73,6 +73,7 @@ typedef struct pl_limits {
 
 /* Bits OR-ed into a caller-owned device status word by PL_FLAG_ASYNC calls. */
 #define PL_STATUS_BIT_OVERFLOW 0x1
+#define PL_STATUS_BIT_ROWS 0x2 /* boson: a malformed output row list (its probability is NaN) */
 
 const char* pl_version(void);
 const char* pl_last_error(void);
@@ -140,6 +141,50 @@ pl_status pl_sz_guard_i64(int32_t n, const int64_t* a_dev, int32_t* guard_dev, v
 /* Device scratch bytes a single-matrix run of order n needs (two layer
  * buffers of max_k C(n,k) entries). */
 uint64_t pl_sz_scratch_bytes(pl_dtype dtype, int32_t n);
+
+/* ---- boson sampling (reference proj/include/permlab/boson.hpp:67-99) ------
+ * An m-mode interferometer is its unitary U: m*m complex128 entries,
+ * row-major, interleaved (re, im) (reference Interferometer, boson.hpp:40-56;
+ * the unitarity check of its constructor stays with the host layer).
+ * `input_modes` (always host memory) are n distinct modes in [0, m): the
+ * submatrix columns. An output pattern with occupancy occ[0..m) is passed as
+ * its n ROWS: mode i repeated occ[i] times in ascending mode order, exactly
+ * the row list extract_submatrix builds (boson.cpp:213-219). The probability
+ * of a pattern is |per(U[rows, input_modes])|^2 / prod_i occ[i]!
+ * (outcome_probability, boson.cpp:229-240); in the default (non-FMA) mode it
+ * is bitwise the reference's. Probabilities are computed on the device with
+ * no submatrix in memory for n <= 6 (one fused kernel); larger n gathers the
+ * submatrices and runs the batched permanent kernels. */
+
+/* Number of output patterns of n photons over m modes, C(m+n-1, n)
+ * (reference enumerate_patterns, boson.cpp:185-205); 0 on overflow. */
+uint64_t pl_boson_pattern_count(int32_t m, int32_t n);
+
+/* Rows of pattern `index` in enumerate_patterns(m, n) order (ascending mode
+ * multisets: mode 0 takes the most photons first, boson.cpp:191-203) into
+ * rows[0..n). Host-side helper; the device enumerator uses the same search. */
+pl_status pl_boson_unrank_pattern(int32_t m, int32_t n, uint64_t index, int32_t* rows);
+
+/* Probabilities of `count` output patterns given as row lists (count x n
+ * int32, each nondecreasing in [0, m)). Replaces a loop over
+ * permlab::outcome_probability (boson.hpp:73-76, boson.cpp:229-240).
+ * Flags: PL_FLAG_DEVICE_PTRS (u, out_rows, probs are device pointers),
+ * PL_FLAG_FMA, PL_FLAG_ASYNC (device pointers; a malformed row list sets
+ * PL_STATUS_BIT_ROWS in *status_dev and gets a NaN probability; synchronous
+ * calls return PL_ERR_ARG instead). `limits` applies the subset-order cap. */
+pl_status pl_boson_probabilities(int32_t m, const void* u, int32_t n, const int32_t* input_modes, int64_t count,
+                                 const int32_t* out_rows, double* probs, uint32_t flags, const pl_limits* limits,
+                                 void* stream, int32_t* status_dev);
+
+/* Probabilities of patterns [first, first + count) of enumerate_patterns(m, n)
+ * order, the patterns enumerated on the device (nothing but U is read).
+ * Replaces the probability loop of permlab::full_distribution
+ * (boson.hpp:85-87, boson.cpp:250-269); n <= 6 as there (PL_ERR_LIMIT
+ * otherwise, the reference's message). The enumeration_cap check stays with
+ * the caller (the host layer applies Limits::enumeration_cap); a pattern
+ * range lets callers chunk or shard a distribution. Flags as above. */
+pl_status pl_boson_distribution(int32_t m, const void* u, int32_t n, const int32_t* input_modes, uint64_t first,
+                                int64_t count, double* probs, uint32_t flags, void* stream);
 
 #ifdef __cplusplus
 }

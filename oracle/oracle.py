@@ -83,6 +83,11 @@ def ref():
         R.ref_sz_batch_c128.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int]
         R.ref_sz_batch_f64.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int, C.c_uint64]
         R.ref_haar.argtypes = [C.c_int, C.c_uint64, _dp]
+        _ip = C.POINTER(C.c_int)
+        R.ref_outcome_probability.argtypes = [C.c_int, _dp, C.c_int, _ip, _ip, _dp]
+        R.ref_full_distribution.argtypes = [C.c_int, _dp, C.c_int, _ip, C.c_uint64, _i64p, _ip, _dp]
+        R.ref_sample.argtypes = [C.c_int, _dp, C.c_int, _ip, C.c_uint64, C.c_uint64, C.c_uint64, _ip]
+        R.ref_enumerate_patterns.argtypes = [C.c_int, C.c_int, _i64p, _ip]
         _ref = R
     return _ref
 
@@ -289,3 +294,70 @@ def ref_haar(m: int, seed: int) -> np.ndarray:
     if rc != 0:
         raise _ref_err(rc)
     return u
+
+
+# ----------------------------------------------------------------- boson sampling (reference)
+# Reference include/permlab/boson.hpp:67-99, src/boson.cpp:185-290. `u` is the
+# m x m unitary (complex128); occupancies are (count, m) int32 arrays.
+
+def _u_arg(u):
+    u = np.ascontiguousarray(u, dtype=np.complex128)
+    return u, _ptr(u.view(np.float64), _dp)
+
+
+def _modes_arg(modes):
+    a = np.ascontiguousarray(modes, dtype=np.int32)
+    return a, _ptr(a, C.POINTER(C.c_int))
+
+
+def ref_outcome_probability(u, input_modes, occupancy) -> float:
+    u, up = _u_arg(u)
+    im, imp = _modes_arg(input_modes)
+    oc, ocp = _modes_arg(occupancy)
+    p = C.c_double()
+    rc = ref().ref_outcome_probability(u.shape[0], up, len(im), imp, ocp, C.byref(p))
+    if rc != 0:
+        raise _ref_err(rc)
+    return p.value
+
+
+def ref_full_distribution(u, input_modes, enumeration_cap: int = 0):
+    """(occupancies (count, m) int32, probabilities (count,) float64)."""
+    u, up = _u_arg(u)
+    im, imp = _modes_arg(input_modes)
+    m = u.shape[0]
+    cnt = C.c_int64()
+    R = ref()
+    rc = R.ref_full_distribution(m, up, len(im), imp, enumeration_cap, C.byref(cnt), None, None)
+    if rc != 0:
+        raise _ref_err(rc)
+    occ = np.zeros((cnt.value, m), dtype=np.int32)
+    probs = np.zeros(cnt.value, dtype=np.float64)
+    rc = R.ref_full_distribution(m, up, len(im), imp, enumeration_cap, C.byref(cnt), _ptr(occ, C.POINTER(C.c_int)),
+                                 _ptr(probs, _dp))
+    if rc != 0:
+        raise _ref_err(rc)
+    return occ, probs
+
+
+def ref_sample(u, input_modes, count: int, seed: int, enumeration_cap: int = 0) -> np.ndarray:
+    u, up = _u_arg(u)
+    im, imp = _modes_arg(input_modes)
+    occ = np.zeros((count, u.shape[0]), dtype=np.int32)
+    rc = ref().ref_sample(u.shape[0], up, len(im), imp, count, seed, enumeration_cap, _ptr(occ, C.POINTER(C.c_int)))
+    if rc != 0:
+        raise _ref_err(rc)
+    return occ
+
+
+def ref_enumerate_patterns(m: int, n: int) -> np.ndarray:
+    cnt = C.c_int64()
+    R = ref()
+    rc = R.ref_enumerate_patterns(m, n, C.byref(cnt), None)
+    if rc != 0:
+        raise _ref_err(rc)
+    occ = np.zeros((cnt.value, m), dtype=np.int32)
+    rc = R.ref_enumerate_patterns(m, n, C.byref(cnt), _ptr(occ, C.POINTER(C.c_int)))
+    if rc != 0:
+        raise _ref_err(rc)
+    return occ

@@ -10,7 +10,8 @@
 //   permlab::store_zechin_permanent / store_zechin_run
 //       (reference include/permlab/permanent.hpp:90,96)
 //   permlab::naive_permanent / ryser_permanent   (permanent.hpp:77,84)
-//   permlab::haar_unitary                         (include/permlab/boson.hpp)
+//   permlab::haar_unitary, outcome_probability, full_distribution, sample,
+//   enumerate_patterns                            (include/permlab/boson.hpp)
 // Status codes: 0 ok, 1 DomainError (message via ref_last_error), 2 the value
 // (or an intermediate) left the shim's 128-bit range, 3 other exception.
 #include <algorithm>
@@ -200,6 +201,67 @@ int ref_haar(int m, std::uint64_t seed, double* u) {
         for (std::size_t i = 0; i < e.size(); ++i) {
             u[2 * i] = e[i].real();
             u[2 * i + 1] = e[i].imag();
+        }
+    });
+}
+
+// ---- boson sampling (reference include/permlab/boson.hpp:67-99) ----------
+// `u` is the m*m unitary, interleaved (re, im); occupancy vectors have length m.
+
+Interferometer make_itf(int m, const double* u) {
+    std::vector<Cplx> e(static_cast<std::size_t>(m) * m);
+    for (std::size_t i = 0; i < e.size(); ++i) e[i] = Cplx(u[2 * i], u[2 * i + 1]);
+    return Interferometer(m, Matrix<Cplx>(m, std::move(e)));
+}
+
+int ref_outcome_probability(int m, const double* u, int n, const int* input_modes, const int* occupancy,
+                            double* prob) {
+    return guarded([&] {
+        const Interferometer itf = make_itf(m, u);
+        OutputPattern out{std::vector<int>(occupancy, occupancy + m)};
+        *prob = outcome_probability(itf, std::vector<int>(input_modes, input_modes + n), out, make_limits(0, 0));
+    });
+}
+
+// Pattern count of full_distribution; with occupancy/probs non-null (sized by a
+// previous call) also the patterns and probabilities, enumeration order.
+int ref_full_distribution(int m, const double* u, int n, const int* input_modes, std::uint64_t enumeration_cap,
+                          std::int64_t* count, int* occupancy, double* probs) {
+    return guarded([&] {
+        const Interferometer itf = make_itf(m, u);
+        Limits lim = make_limits(0, 0);
+        if (enumeration_cap) lim.enumeration_cap = enumeration_cap;
+        const OutcomeDistribution d = full_distribution(itf, std::vector<int>(input_modes, input_modes + n), lim);
+        *count = static_cast<std::int64_t>(d.entries.size());
+        if (occupancy && probs) {
+            for (std::size_t i = 0; i < d.entries.size(); ++i) {
+                std::copy(d.entries[i].first.occupancy.begin(), d.entries[i].first.occupancy.end(),
+                          occupancy + i * static_cast<std::size_t>(m));
+                probs[i] = d.entries[i].second;
+            }
+        }
+    });
+}
+
+int ref_sample(int m, const double* u, int n, const int* input_modes, std::uint64_t count, std::uint64_t seed,
+               std::uint64_t enumeration_cap, int* occupancy) {
+    return guarded([&] {
+        const Interferometer itf = make_itf(m, u);
+        Limits lim = make_limits(0, 0);
+        if (enumeration_cap) lim.enumeration_cap = enumeration_cap;
+        const auto s = sample(itf, std::vector<int>(input_modes, input_modes + n), count, seed, lim);
+        for (std::size_t i = 0; i < s.size(); ++i)
+            std::copy(s[i].occupancy.begin(), s[i].occupancy.end(), occupancy + i * static_cast<std::size_t>(m));
+    });
+}
+
+int ref_enumerate_patterns(int m, int n, std::int64_t* count, int* occupancy) {
+    return guarded([&] {
+        const auto p = enumerate_patterns(m, n);
+        *count = static_cast<std::int64_t>(p.size());
+        if (occupancy) {
+            for (std::size_t i = 0; i < p.size(); ++i)
+                std::copy(p[i].occupancy.begin(), p[i].occupancy.end(), occupancy + i * static_cast<std::size_t>(m));
         }
     });
 }

@@ -21,6 +21,7 @@ PL_FLAG_DEVICE_PTRS = 0x1
 PL_FLAG_FMA = 0x2
 PL_FLAG_ASYNC = 0x4
 PL_STATUS_BIT_OVERFLOW = 0x1
+PL_STATUS_BIT_ROWS = 0x2
 PL_MAX_ORDER = 34
 
 STATUS_NAMES = {
@@ -50,6 +51,10 @@ EXPORTED_SYMBOLS = (
     "pl_sz_top",
     "pl_sz_guard_i64",
     "pl_sz_scratch_bytes",
+    "pl_boson_pattern_count",
+    "pl_boson_unrank_pattern",
+    "pl_boson_probabilities",
+    "pl_boson_distribution",
 )
 
 
@@ -92,6 +97,14 @@ def _load():
     L.pl_sz_guard_i64.restype = C.c_int
     L.pl_sz_scratch_bytes.argtypes = [C.c_int, i32]
     L.pl_sz_scratch_bytes.restype = u64
+    L.pl_boson_pattern_count.argtypes = [i32, i32]
+    L.pl_boson_pattern_count.restype = u64
+    L.pl_boson_unrank_pattern.argtypes = [i32, i32, u64, vp]
+    L.pl_boson_unrank_pattern.restype = C.c_int
+    L.pl_boson_probabilities.argtypes = [i32, vp, i32, vp, i64, vp, vp, u32, C.POINTER(pl_limits), vp, vp]
+    L.pl_boson_probabilities.restype = C.c_int
+    L.pl_boson_distribution.argtypes = [i32, vp, i32, vp, u64, i64, vp, u32, vp]
+    L.pl_boson_distribution.restype = C.c_int
     return L
 
 

@@ -22,6 +22,7 @@
 #include "sz_kernels.cuh"
 #include "sz_ws.cuh"
 #include "sz_batch.cuh"
+#include "capi_internal.h"
 
 namespace {
 
@@ -633,6 +634,20 @@ pl_status common_checks(pl_dtype dt, int n, int64_t count, const void* a, void* 
 }
 
 }  // namespace
+
+namespace plc {
+
+pl_status fail_msg(pl_status s, const char* msg) { return fail(s, "%s", msg); }
+pl_status cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+pl_status device_ready() { return have_device(); }
+int sm_count() { return num_sms(); }
+pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
+                        int32_t* status_dev, cudaStream_t st) {
+    return ::enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
+}
+pl_status check_order_limits(int n, const pl_limits* lim) { return check_order(n, lim); }
+
+}  // namespace plc
 
 extern "C" {
 

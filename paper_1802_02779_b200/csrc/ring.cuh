@@ -46,6 +46,7 @@ template <bool FMA>
 struct RF64 {
     using T = double;
     static constexpr bool kChecked = false;
+    static constexpr bool kFma = FMA;
     __device__ __forceinline__ static T mul(T a, T b, bool&) { return __dmul_rn(a, b); }
     __device__ __forceinline__ static T add(T a, T b, bool&) { return __dadd_rn(a, b); }
     __device__ __forceinline__ static T mac(T acc, T a, T b, bool&) {
@@ -58,6 +59,7 @@ template <bool FMA>
 struct RC128 {
     using T = double2;
     static constexpr bool kChecked = false;
+    static constexpr bool kFma = FMA;
     __device__ __forceinline__ static T mul(T a, T b, bool&) {
         T r;
         r.x = __dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y));

@@ -448,7 +448,7 @@ __global__ void sz_top_kernel(const typename R::T* __restrict__ a, int n, const 
     out[0] = total;
 }
 
-__global__ void sz_guard_i64_kernel(const long long* __restrict__ a, int n, int32_t* __restrict__ guard) {
+static __global__ void sz_guard_i64_kernel(const long long* __restrict__ a, int n, int32_t* __restrict__ guard) {
     if (threadIdx.x == 0 && blockIdx.x == 0) guard[0] = i64_guard_ok(a, n) ? 0 : 1;
 }
 
