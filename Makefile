@@ -34,11 +34,11 @@ $(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/boson.o
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c
 	gcc -O2 -fPIC -ffp-contract=off -std=gnu11 -Wall -shared -o $@ $< -lm
 
-$(PKG)/libpermlab.so: $(CSRC)/host/permanent.cpp $(wildcard include/permlab/*.hpp) include/permlab_b200.h $(PKG)/libpermlab_b200.so
-	g++ $(CXXFLAGS) -shared -o $@ $(CSRC)/host/permanent.cpp -L$(PKG) -lpermlab_b200 -Wl,-rpath,'$$ORIGIN'
+$(PKG)/libpermlab.so: $(CSRC)/host/permanent.cpp $(CSRC)/host/boson.cpp $(wildcard include/permlab/*.hpp) include/permlab_b200.h $(PKG)/libpermlab_b200.so $(PKG)/libpermlab_gen.so
+	g++ $(CXXFLAGS) -shared -o $@ $(CSRC)/host/permanent.cpp $(CSRC)/host/boson.cpp -L$(PKG) -lpermlab_b200 -lpermlab_gen -Wl,-rpath,'$$ORIGIN'
 
 tests/cpp/test_permanent_device: tests/cpp/test_permanent_device.cpp $(PKG)/libpermlab.so
-	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lpermlab -lpermlab_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lpermlab -lpermlab_b200 -lpermlab_gen -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle all

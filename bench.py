@@ -321,6 +321,111 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
     }
 
 
+BOSON = dict(m=25, modes=[0, 1, 2, 3, 4], seed=2,
+             desc="full outcome distribution of 5 photons in Haar(25) seed 2, input modes 0..4 "
+                  "(118,755 patterns; the collision-aware form of C2's submatrices)")
+FP64_PEAK = (18.518, "measured DMUL/DADD rate x 1 flop (profiles/microbench_b200.json; the non-FMA reference "
+                     "rounding mode issues no DFMA)")
+
+
+def boson_flops_per_pattern(n: int) -> int:
+    return flops_per_perm(n, "complex128") + 3  # + |z|^2 (2 mul, 1 add); the divide not counted
+
+
+def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False):
+    """The boson driver's fused kernel (pl_boson_distribution): every pattern
+    of the distribution enumerated, gathered, evaluated and normalised on the
+    device. value: device buffers, asynchronous calls, events; e2e: the
+    public host call (H2D of U, D2H of the probabilities)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1802_02779_b200 import boson as B
+
+    itf = B.haar_unitary(BOSON["m"], BOSON["seed"])
+    modes = BOSON["modes"]
+    count = B.pattern_count(BOSON["m"], len(modes))
+    stream = torch.cuda.current_stream(device)
+    out = torch.empty(count, dtype=torch.float64, device=device)
+    status = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def step():
+        B.distribution_probabilities(itf, modes, out=out, stream=stream, status=status, fma=fma)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    for _ in range(warmup):
+        step()
+    barrier()
+    evs = []
+    for _ in range(steps):
+        flush_buf[0].add_(1)
+        flush_buf[1].sum(dtype=torch.float32)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    barrier()
+    t_local = sum(a.elapsed_time(b) for a, b in evs) / 1000.0
+    t = torch.tensor([t_local], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = count * steps * world / float(t.item())
+    host = np.empty(count)
+    for _ in range(warmup):
+        B.distribution_probabilities(itf, modes, out=host, fma=fma)
+    barrier()
+    te = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        B.distribution_probabilities(itf, modes, out=host, fma=fma)
+        e1.record(stream)
+        e1.synchronize()
+        te.append(e0.elapsed_time(e1) / 1000.0)
+    tt = torch.tensor([sum(te)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e = count * steps * world / float(tt.item())
+    per_step = t_local / steps
+    achieved = boson_flops_per_pattern(len(modes)) * count / per_step / 1e12
+    return {
+        "value": value, "unit": "probabilities/s", "ms_per_step": 1000.0 * float(t.item()) / steps, "steps": steps,
+        "workload": BOSON["desc"], "patterns": count,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK[0], "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK[0], "peak_source": FP64_PEAK[1],
+                     "kernel": "sz_boson_kernel<RC128,5,VS=1> (enumerate + gather + DP + |per|^2/prod occ!)",
+                     "hbm_bytes_per_pattern": 8},
+        "e2e": {"value": e2e, "unit": "probabilities/s", "h2d_bytes_per_step": BOSON["m"] ** 2 * 16,
+                "d2h_bytes_per_step": count * 8},
+    }
+
+
+def boson_cpu_reference(budget_s: float):
+    """The reference's own full_distribution (oracle/_ref), single-threaded as
+    the reference is; bounded by repeating it until budget_s."""
+    from oracle import oracle as O
+
+    from paper_1802_02779_b200 import boson as B
+
+    if not O.ref_available():
+        return None
+    u = B.haar_unitary(BOSON["m"], BOSON["seed"]).unitary()
+    done, t0 = 0, time.perf_counter()
+    while True:
+        _, p = O.ref_full_distribution(u, BOSON["modes"], enumeration_cap=10 ** 6)
+        done += p.shape[0]
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": done / el, "unit": "probabilities/s", "cores": 1, "kind": "reference",
+            "sample": f"{done} patterns ({done // p.shape[0]} x full_distribution, {el:.1f} s, 1 thread)"}
+
+
 def roofline_of(res, peak, peak_src, traffic):
     achieved = res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9
     tr = traffic.get(res["name"])
@@ -377,6 +482,9 @@ def main():
                                "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"],
                                "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
                                             else "equal slices, all-gather") if r["sharded"] else None)}
+            suite["boson"] = measure_boson(10, 3, rank, world, device, flush_buf, args.fma)
+            if rank == 0 and world == 1 and not args.no_cpu:
+                suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

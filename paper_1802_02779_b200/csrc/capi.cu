@@ -350,7 +350,7 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int
 uint32_t ws_hints() {
     static const uint32_t h = [] {
         const char* e = std::getenv("PL_WS_HINTS");
-        return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0x905u;
+        return (e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0x905u) & 0x7fffffffu;  // bit 31: see loaded_dep
     }();
     return h;
 }
@@ -484,11 +484,15 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     cfg.blockDim = dim3(pl::WsGeom<(int)sizeof(T)>::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
+    static const bool pdl = [] {
+        const char* e = std::getenv("PL_WS_PDL");  // debug: 0 disables programmatic dependent launch
+        return !(e && e[0] == '0');
+    }();
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                static_cast<T*>(cur), r0, r1, sched, static_cast<const uint4*>(q.ltab),
                                static_cast<const uint32_t*>(q.offs), static_cast<const uint2*>(q.binom_pairs),

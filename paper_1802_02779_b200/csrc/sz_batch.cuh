@@ -104,8 +104,10 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads)
                 const T* src = buf + lane * Gm::kEnt;
 #pragma unroll
                 for (int e = 0; e < Gm::kEnt; ++e) m.v[e] = src[e];
+                // the refill may only be issued once every load has returned (loaded_dep)
+                const uint32_t dep = loaded_dep(m.v, Gm::kEnt, (uint32_t)((uint64_t)count >> 62));  // count < 2^62
                 __syncwarp();
-                if (b + stride < nfull) issue(b + stride, 0);
+                if (b + stride + dep < nfull) issue(b + stride + dep, 0);
                 v = batch_eval<R, N>(m.v, ov);
             }
         } else {

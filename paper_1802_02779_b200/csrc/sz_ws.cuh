@@ -379,6 +379,25 @@ __device__ __forceinline__ uint64_t warp_scan_u64(uint64_t v) {
     return v;
 }
 
+// Zero, computed from the bits of `n` loaded values: a mbarrier arrive whose
+// address adds it cannot issue before those loads have returned. An
+// mbarrier.arrive does not wait for the warp's outstanding shared-memory loads
+// (ptxas emits no scoreboard wait before SYNCS.ARRIVE), so a slot handed back
+// right after ld.shared can be refilled by the next TMA copy before a queued
+// load has read it (seen as wrong second outputs per thread in
+// profiles/archive_probe.py). `rt_zero` must be 0 at run time but unknown to
+// the compiler (a kernel argument), so the dependency survives ptxas.
+template <class T>
+__device__ __forceinline__ uint32_t loaded_dep(const T* v, int n, uint32_t rt_zero) {
+    uint32_t d = 0;
+    for (int i = 0; i < n; ++i) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[i]);
+#pragma unroll
+        for (int b = 0; b < (int)(sizeof(T) / 4); ++b) d ^= w[b];
+    }
+    return (uint32_t)(d == 0x9e3779b9u) & rt_zero;
+}
+
 // ---------------------------------------------------------------- debug trace
 // Event trace of CTA 0 for pipeline analysis (PL_WS_TRACE, see capi.cu):
 // region r holds (clock64, event | arg << 8) pairs; r = 0/1 first warp of
@@ -551,8 +570,9 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
                     for (int li = 0; li < FS; ++li)
                         xs[p][li] = li < nl ? st[p * LANES + li * WsSmem<T>::kSlot + pads[li]] : RR::zero();
             }
+            const uint32_t dep = loaded_dep(&xs[0][0], PER * FS, hints >> 31);  // hints bit 31 is never set
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s));
+            if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s) + dep);
             const bool init_first = M == 0 && l0 == 0;
 #pragma unroll
             for (int p = 0; p < PER; ++p) {
@@ -626,7 +646,10 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     // soon as SMs free up; this grid's prologue (engine tables, barriers)
     // overlaps the previous layer's tail, and nothing it reads or writes in the
     // layer buffers (or the matrix) is touched before griddepcontrol.wait.
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#ifndef PL_WS_TRIGGER
+#define PL_WS_TRIGGER 1
+#endif
+    if (PL_WS_TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     for (int e = threadIdx.x; e < kBinomDim * kBinomDim; e += blockDim.x) sm.B2[e] = __ldg(&binom_pairs[e]);
     for (int v = threadIdx.x; v <= D; v += blockDim.x) qoff_sh[v] = __ldg(qtab_off + v);
     if (threadIdx.x == 0) {
@@ -642,6 +665,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous layer is complete and visible
+#ifndef PL_WS_PROXY_FENCE
+#define PL_WS_PROXY_FENCE 1
+#endif
+    // The previous layer's outputs were written by generic-proxy stores and are
+    // read below by TMA bulk copies (async proxy): order the two proxies after
+    // the grid-dependency wait.
+    if (PL_WS_PROXY_FENCE) asm volatile("fence.proxy.async.global;\n" ::: "memory");
     for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
     for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
     __syncthreads();
@@ -886,6 +916,15 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             if (lane == 0) mbar_arrive(&sm.src_empty[ss]);
         }
         if (ov) atomicOr(status, 1);
+    }
+    if (PL_WS_TRIGGER == 2) {
+        // every output of this CTA stored and made visible device-wide, then
+        // let the next layer's grid start its prologue
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        }
     }
 }
 

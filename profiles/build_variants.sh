@@ -5,9 +5,11 @@
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p profiles/_variants
+make build/boson.o > /dev/null
 while [ $# -ge 2 ]; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
-       -Xptxas -warn-spills $2 -shared -o profiles/_variants/$1.so paper_1802_02779_b200/csrc/capi.cu -lcudart &
+  ( nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
+         -Xptxas -warn-spills $2 -c -o profiles/_variants/$1.o paper_1802_02779_b200/csrc/capi.cu &&
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o profiles/_variants/$1.so profiles/_variants/$1.o build/boson.o -lcudart ) &
   shift 2
 done
 wait

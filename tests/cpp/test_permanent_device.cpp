@@ -10,6 +10,7 @@
 //   error mapping when no device is present).
 #include <dlfcn.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -17,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "permlab/boson.hpp"
 #include "permlab/permanent.hpp"
 
 using namespace permlab;
@@ -255,11 +257,146 @@ void device_run_and_batch() {
     CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(20, 1)))) == 2432902008176640000LL);
 }
 
+// ---------------------------------------------------------------- boson sampling
+// mirrors reference tests/test_boson.cpp case by case
+
+Matrix<Cplx> balanced_coupler() {
+    const double s = 1.0 / std::sqrt(2.0);
+    return {2, {Cplx(s), Cplx(s), Cplx(s), Cplx(-s)}};
+}
+
+bool near(double a, double b, double eps) { return std::abs(a - b) <= eps * std::max(std::abs(a), std::abs(b)); }
+
+void host_boson() {
+    // reference test_boson.cpp:28-36
+    const Interferometer coupler(2, balanced_coupler());
+    CHECK(coupler.modes() == 2);
+    CHECK_THROWS_AS(Interferometer(2, Matrix<Cplx>::filled(2, Cplx(0.5))), DomainError);
+    CHECK_THROWS_AS(Interferometer(3, balanced_coupler()), DomainError);
+    CHECK_THROWS_AS(Interferometer(0, Matrix<Cplx>::identity(1)), DomainError);
+    // :38-63
+    for (int m : {1, 2, 5, 8}) {
+        const Interferometer itf = haar_unitary(m, 99);
+        CHECK(itf.modes() == m);
+    }
+    CHECK(haar_unitary(4, 5).unitary() == haar_unitary(4, 5).unitary());
+    CHECK(!(haar_unitary(4, 5).unitary() == haar_unitary(4, 6).unitary()));
+    // :65-72
+    const auto patterns = enumerate_patterns(2, 2);
+    CHECK(patterns.size() == 3);
+    CHECK(patterns[0].occupancy == (std::vector<int>{2, 0}));
+    CHECK(patterns[1].occupancy == (std::vector<int>{1, 1}));
+    CHECK(patterns[2].occupancy == (std::vector<int>{0, 2}));
+    CHECK(enumerate_patterns(6, 3).size() == 56);
+    // :74-99
+    const Interferometer itf = haar_unitary(3, 7);
+    CHECK(extract_submatrix(itf, {0, 1, 2}, {{1, 1, 1}}) == itf.unitary());
+    const auto one = extract_submatrix(itf, {1}, {{0, 0, 1}});
+    CHECK(one.order() == 1);
+    CHECK(one(0, 0) == itf.unitary()(2, 1));
+    const auto two = extract_submatrix(itf, {0, 1}, {{2, 0, 0}});
+    CHECK(two(0, 0) == two(1, 0));
+    CHECK(two(0, 1) == two(1, 1));
+    CHECK_THROWS_AS(extract_submatrix(itf, {0, 3}, {{1, 1, 0}}), DomainError);
+    CHECK_THROWS_AS(extract_submatrix(itf, {0, 0}, {{1, 1, 0}}), DomainError);
+    CHECK_THROWS_AS(extract_submatrix(itf, {0, 1}, {{1, 1, 1}}), DomainError);
+    CHECK_THROWS_AS(extract_submatrix(itf, {0, 1}, {{1, 1}}), DomainError);
+    CHECK_THROWS_AS(extract_submatrix(itf, {0, 1}, {{2, -1, 1}}), DomainError);
+    // :196-206 (all rejected before any device work)
+    const Interferometer itf8 = haar_unitary(8, 41);
+    CHECK_THROWS_AS(full_distribution(itf8, {0, 1, 2, 3, 4, 5, 6}), DomainError);
+    Limits tight;
+    tight.enumeration_cap = 10;
+    CHECK_THROWS_AS(full_distribution(itf8, {0, 1, 2}, tight), DomainError);
+    CHECK_THROWS_AS(full_distribution(itf8, {}), DomainError);
+    CHECK_THROWS_AS(full_distribution(itf8, {0, 8}), DomainError);
+}
+
+void device_boson() {
+    // :101-115 two-photon interference on the balanced coupler
+    const Interferometer coupler(2, balanced_coupler());
+    const std::vector<int> input{0, 1};
+    CHECK(outcome_probability(coupler, input, {{1, 1}}) <= 1e-12);
+    CHECK(near(outcome_probability(coupler, input, {{2, 0}}), 0.5, 1e-12));
+    CHECK(near(outcome_probability(coupler, input, {{0, 2}}), 0.5, 1e-12));
+    const OutcomeDistribution dist = full_distribution(coupler, input);
+    CHECK(dist.entries.size() == 3);
+    CHECK(near(dist.entries[0].second, 0.5, 1e-12));
+    CHECK(dist.entries[1].second <= 1e-12);
+    CHECK(near(dist.entries[2].second, 0.5, 1e-12));
+    CHECK(near(dist.total_probability(), 1.0, 1e-12));
+    // :117-128 single photons
+    const Interferometer itf4 = haar_unitary(4, 17);
+    double total = 0;
+    for (int j = 0; j < 4; ++j) {
+        OutputPattern out{std::vector<int>(4, 0)};
+        out.occupancy[static_cast<std::size_t>(j)] = 1;
+        const double p = outcome_probability(itf4, {2}, out);
+        CHECK(near(p, std::norm(itf4.unitary()(j, 2)), 1e-12));
+        total += p;
+    }
+    CHECK(near(total, 1.0, 1e-10));
+    // :140-163 the distribution against per-pattern Store-zechin on the device
+    const Interferometer itf6 = haar_unitary(6, 31);
+    const std::vector<int> in3{0, 1, 2};
+    const OutcomeDistribution d6 = full_distribution(itf6, in3);
+    CHECK(d6.entries.size() == 56);
+    CHECK(std::abs(d6.total_probability() - 1.0) <= 1e-9);
+    for (const auto& [pattern, p] : d6.entries) {
+        const Cplx per = std::get<Cplx>(store_zechin_permanent(SquareMatrix(extract_submatrix(itf6, in3, pattern))).value);
+        CHECK(per == oracle_cplx(extract_submatrix(itf6, in3, pattern)));
+        double divisor = 1;
+        for (int c : pattern.occupancy)
+            for (int i = 2; i <= c; ++i) divisor *= i;
+        CHECK(p == std::norm(per) / divisor);  // bitwise: same DP, same rounding
+    }
+    // batch entry point == singles; distribution chunks == the whole
+    std::vector<OutputPattern> pats;
+    for (const auto& e : d6.entries) pats.push_back(e.first);
+    const auto batch = outcome_probabilities(itf6, in3, pats);
+    const auto chunk = distribution_probabilities(itf6, in3, 10, 30);
+    for (std::size_t i = 0; i < pats.size(); ++i) CHECK(batch[i] == d6.entries[i].second);
+    for (std::size_t i = 0; i < chunk.size(); ++i) CHECK(chunk[i] == d6.entries[10 + i].second);
+    // :165-194 relabelling output modes permutes the distribution
+    const Interferometer itf = haar_unitary(4, 37);
+    const OutcomeDistribution base = full_distribution(itf, input);
+    const std::vector<int> perm{2, 0, 3, 1};
+    std::vector<int> inverse(perm.size());
+    for (std::size_t j = 0; j < perm.size(); ++j) inverse[static_cast<std::size_t>(perm[j])] = static_cast<int>(j);
+    const Interferometer relabeled(4, itf.unitary().permute(inverse, {0, 1, 2, 3}));
+    const OutcomeDistribution moved = full_distribution(relabeled, input);
+    for (const auto& [pattern, p] : base.entries) {
+        OutputPattern rp{std::vector<int>(4, 0)};
+        for (std::size_t j = 0; j < perm.size(); ++j) rp.occupancy[static_cast<std::size_t>(perm[j])] = pattern.occupancy[j];
+        bool found = false;
+        for (const auto& [q_pattern, q] : moved.entries) {
+            if (q_pattern == rp) {
+                CHECK(near(q, p, 1e-9));
+                found = true;
+            }
+        }
+        CHECK(found);
+    }
+    // :208-232 sampling
+    CHECK(sample(coupler, input, 0, 1).empty());
+    const auto draws = sample(coupler, input, 10000, 7);
+    CHECK(draws.size() == 10000);
+    std::size_t first = 0;
+    for (const auto& p : draws) {
+        CHECK(!(p.occupancy == std::vector<int>{1, 1}));
+        first += p.occupancy == std::vector<int>{2, 0} ? 1 : 0;
+    }
+    CHECK(first > 4500 && first < 5500);
+    CHECK(sample(coupler, input, 200, 99) == sample(coupler, input, 200, 99));
+    CHECK(!(sample(coupler, input, 200, 99) == sample(coupler, input, 200, 100)));
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     const bool host_only = argc > 1 && std::string(argv[1]) == "--host-only";
     host_closed_forms();
+    host_boson();
     if (!host_only) {
         if (!load_oracle(argv[0])) {
             std::fprintf(stderr, "cannot load oracle/liboracle.so\n");
@@ -269,6 +406,7 @@ int main(int argc, char** argv) {
         device_oracle_agreement();
         device_identities();
         device_run_and_batch();
+        device_boson();
     }
     std::printf("%d checks, %d failures\n", g_checks, g_failures);
     return g_failures == 0 ? 0 : 1;

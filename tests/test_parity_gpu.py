@@ -194,6 +194,17 @@ def test_c4_permutation_and_transpose_invariance():
     assert rel_err(pl.store_zechin_permanent(a.T.copy()).value, base) <= REL_TOL
 
 
+def test_c5_repeatable(goldens):
+    # every run of the layer DP is bitwise the same (regression: a missing
+    # generic -> async proxy fence after the PDL wait let ~1 in 8 runs read
+    # stale layer entries, sz_ws.cuh)
+    a = configs.c5()
+    want = complex(*goldens["c5"]["value"])
+    vals = {complex(pl.store_zechin_permanent(a).value) for _ in range(8)}
+    assert len(vals) == 1
+    assert abs(vals.pop() - want) <= REL_TOL * abs(want)
+
+
 def test_c5_row_linearity():
     a = configs.c5()
     x = configs.complex_uniform((32,), seed=77) * 1e-2
