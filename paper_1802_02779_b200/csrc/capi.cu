@@ -145,9 +145,34 @@ cudaError_t set_smem_once(K kern, size_t bytes) {
 
 constexpr int kRegsMaxOrder = 5;  // n = 6 spills in registers; it runs in the shared-memory kernel
 
+// Batch kernel choice for n <= 5: the pipelined kernel for inputs of 64 MiB
+// and more (1.6 M c128 5x5: 6.1 vs 5.5 TB/s), the per-warp TMA kernel below
+// that (equal at C2's 40 MB, faster for C1's int64) and for misaligned input.
+// PL_BATCH_KERNEL=warp|pipe forces one (A/B timing, profiles/batch_ab.py).
+bool use_pipe_kernel(size_t in_bytes) {
+    static const int force = [] {
+        const char* e = std::getenv("PL_BATCH_KERNEL");
+        if (e && std::string(e) == "warp") return 0;
+        if (e && std::string(e) == "pipe") return 1;
+        return -1;
+    }();
+    return force >= 0 ? force == 1 : in_bytes >= (size_t(64) << 20);
+}
+
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
+    if (use_pipe_kernel((size_t)count * N * N * sizeof(T)) && (reinterpret_cast<uintptr_t>(a) & 15u) == 0) {
+        using Pg = pl::PipeGeom<T, N>;
+        auto kern = pl::sz_batch_pipe_kernel<R, N>;
+        PL_CUDA(set_smem_once(kern, Pg::kSmem));
+        const int64_t nfull = count / 32;
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nfull, num_sms()));
+        kern<<<(unsigned)blocks, Pg::kThreads, Pg::kSmem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count,
+                                                              status);
+        PL_CUDA(cudaGetLastError());
+        return PL_OK;
+    }
     using Gm = pl::BatchGeom<T, N>;
     auto kern = pl::sz_batch_tma_kernel<R, N>;
     PL_CUDA(set_smem_once(kern, Gm::kSmem));

@@ -133,4 +133,89 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads)
     if (ov_any) atomicOr(status, 1);
 }
 
+// Pipelined batch kernel (n <= 5, 16-byte aligned input): one CTA per SM, an
+// even split of the batch's warp batches (32 matrices, one contiguous run)
+// across CTAs, and inside a CTA a producer warp that keeps a ring of S batches
+// in flight by TMA (enough bytes per SM to cover the HBM latency) while W
+// consumer warps take the landed batches round-robin (warp w owns slot w): matrix to registers, slot handed back (after the loads
+// have returned, loaded_dep), the order-n DP in registers, one coalesced store
+// per warp. A remainder of count % 32 matrices is read directly by the last CTA.
+template <class T, int N>
+struct PipeGeom {
+    static constexpr int kEnt = N * N;
+    static constexpr int W = (sizeof(T) == 16 && N == 5) || (sizeof(T) == 8 && N == 5) ? 10 : 12;  // consumer warps (N = 5 needs ~168 registers)
+    // ring slots = consumer warps: item i goes to warp i % W and slot i % S, so the
+    // uses of a slot are consumed in order by one warp (with S != W a fast warp
+    // could wait on a slot's parity two uses ahead and read a stale batch)
+    static constexpr int S = W;
+    static constexpr unsigned kBatchBytes = 32u * kEnt * sizeof(T);
+    static constexpr int kThreads = 32 * (W + 1);
+    static constexpr size_t kSmem = (size_t)S * kBatchBytes + 2 * S * sizeof(uint64_t);
+};
+
+template <class R, int N>
+__global__ void __launch_bounds__(PipeGeom<typename R::T, N>::kThreads, 1)
+    sz_batch_pipe_kernel(const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
+                         int32_t* __restrict__ status) {
+    using T = typename R::T;
+    using Gm = PipeGeom<T, N>;
+    constexpr int S = Gm::S, W = Gm::W, E = Gm::kEnt;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * Gm::kBatchBytes);
+    uint64_t* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nfull = count / 32;
+    const int64_t b0 = nfull * blockIdx.x / gridDim.x, b1 = nfull * (blockIdx.x + 1) / gridDim.x;
+    const int nb = (int)(b1 - b0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 32);  // every consumer thread, once its loads have returned
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    bool ov_any = false;
+    if (warp == W) {
+        // producer: one lane streams the CTA's batches into the ring
+        if (lane == 0) {
+            for (int i = 0; i < nb; ++i) {
+                const int s = i % S;
+                if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1u);
+                mbar_arrive_expect_tx(&full[s], Gm::kBatchBytes);
+                bulk_g2s(ring + (size_t)s * 32 * E, a + (b0 + i) * 32 * E, Gm::kBatchBytes, &full[s]);
+            }
+        }
+    } else {
+        for (int i = warp; i < nb; i += W) {
+            const int s = i % S;
+            mbar_wait(&full[s], (i / S) & 1u);
+            MatRegs<T, E> m;
+            const T* src = ring + (size_t)s * 32 * E + lane * E;
+#pragma unroll
+            for (int e = 0; e < E; ++e) m.v[e] = src[e];
+            mbar_arrive(&empty[s] + loaded_dep(m.v, E, (uint32_t)((uint64_t)count >> 62)));  // count < 2^62
+            bool ov = false;
+            T v = batch_eval<R, N>(m.v, ov);
+            if (ov) v = R::zero();
+            ov_any |= ov;
+            out[(b0 + i) * 32 + lane] = v;
+        }
+        if (blockIdx.x == gridDim.x - 1 && warp == 0) {
+            const int64_t mi = nfull * 32 + lane;
+            if (mi < count) {
+                MatRegs<T, E> m;
+                load_matrix<T, E>(a + mi * E, m);
+                bool ov = false;
+                T v = batch_eval<R, N>(m.v, ov);
+                if (ov) v = R::zero();
+                ov_any |= ov;
+                out[mi] = v;
+            }
+        }
+    }
+    if (ov_any) atomicOr(status, 1);
+}
+
 }  // namespace pl

@@ -379,22 +379,19 @@ __device__ __forceinline__ uint64_t warp_scan_u64(uint64_t v) {
     return v;
 }
 
-// Zero, computed from the bits of `n` loaded values: a mbarrier arrive whose
+// Zero, computed from `n` loaded values (one 32-bit word of each: a load
+// instruction's scoreboard covers its whole result): an mbarrier arrive whose
 // address adds it cannot issue before those loads have returned. An
-// mbarrier.arrive does not wait for the warp's outstanding shared-memory loads
-// (ptxas emits no scoreboard wait before SYNCS.ARRIVE), so a slot handed back
-// right after ld.shared can be refilled by the next TMA copy before a queued
-// load has read it (seen as wrong second outputs per thread in
+// mbarrier.arrive does not wait for the thread's outstanding shared-memory
+// loads (ptxas emits no scoreboard wait before SYNCS.ARRIVE), so a slot handed
+// back right after ld.shared can be refilled by the next TMA copy before a
+// queued load has read it (seen as wrong second outputs per thread in
 // profiles/archive_probe.py). `rt_zero` must be 0 at run time but unknown to
 // the compiler (a kernel argument), so the dependency survives ptxas.
 template <class T>
 __device__ __forceinline__ uint32_t loaded_dep(const T* v, int n, uint32_t rt_zero) {
     uint32_t d = 0;
-    for (int i = 0; i < n; ++i) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[i]);
-#pragma unroll
-        for (int b = 0; b < (int)(sizeof(T) / 4); ++b) d ^= w[b];
-    }
+    for (int i = 0; i < n; ++i) d ^= *reinterpret_cast<const uint32_t*>(&v[i]);
     return (uint32_t)(d == 0x9e3779b9u) & rt_zero;
 }
 
@@ -570,9 +567,9 @@ __device__ __forceinline__ void ws_consume_tile(const WsSmem<T>& sm, const WsHdr
                     for (int li = 0; li < FS; ++li)
                         xs[p][li] = li < nl ? st[p * LANES + li * WsSmem<T>::kSlot + pads[li]] : RR::zero();
             }
-            const uint32_t dep = loaded_dep(&xs[0][0], PER * FS, hints >> 31);  // hints bit 31 is never set
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(sm.empty_bar(g, s) + dep);
+            // every consumer thread hands the slot back once its own loads have
+            // returned (the empty barrier counts GW * 32 arrivals)
+            mbar_arrive(sm.empty_bar(g, s) + loaded_dep(&xs[0][0], PER * FS, hints >> 31));  // hints bit 31 is never set
             const bool init_first = M == 0 && l0 == 0;
 #pragma unroll
             for (int p = 0; p < PER; ++p) {
@@ -655,7 +652,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     if (threadIdx.x == 0) {
         for (int s = 0; s < G * NSG; ++s) {
             mbar_init(&sm.full[s], 1);               // the group's streamer: arrive.expect_tx
-            mbar_init(&sm.empty[s], GW);  // the group's consumer warps
+            mbar_init(&sm.empty[s], GW * 32);  // every thread of the group's consumer warps
         }
         for (int s = 0; s < NHDR; ++s) {
             mbar_init(&sm.src_full[s], 1);        // publisher: arrive.expect_tx

@@ -56,6 +56,19 @@ def test_c2_complex(goldens, fma):
         assert configs.sha256(out) == goldens["c2"]["output_sha256"]
 
 
+@pytest.mark.parametrize("dtype,count", [("c128", 200_003), ("i64", 350_017)])
+def test_pipelined_batch_kernel(dtype, count):
+    # inputs of >= 64 MiB take the pipelined n = 5 kernel (one CTA per SM, producer
+    # warp + ring); odd counts exercise the remainder path of the last CTA
+    if dtype == "c128":
+        a = configs.complex_uniform((count, 5, 5), seed=9)
+    else:
+        a = configs.int_matrices(5, count, seed=9)
+    assert a.nbytes >= 64 << 20
+    out = pl.store_zechin_permanent_batch(a)
+    assert np.array_equal(out, O.sz_batch(a))
+
+
 def test_c3_bit_exact(goldens):
     a = configs.c3()
     out = pl.store_zechin_permanent_batch(a)
