@@ -287,13 +287,53 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     return PL_OK;
 }
 
-// 6 <= n <= 14: the shared-memory kernel, specialised per order.
+// Warp-per-matrix kernel for 8-byte rings, 6 <= n <= 9 (PL_BATCH_SMEM=cta forces the CTA
+// kernel). Measured (profiles/c3_ab.py): n = 8 x 50k int64 104 -> 74 us; equal at n = 10;
+// slower at n = 12 (C3: 205 -> 293 us), where a matrix's layers take ~16 KB and a warp per
+// matrix leaves too few warps per SM, so n >= 10 keeps the CTA-per-matrix kernel.
+template <class R, int N>
+pl_status launch_warp_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st, const Ptab& pt) {
+    using T = typename R::T;
+    const size_t smem = (size_t)pl::kWarpKernelWarps * pl::warp_kernel_stride<N>() * sizeof(T);
+    auto kern = pl::sz_batch_warp_kernel<R, N>;
+    PL_CUDA(set_smem_once(kern, smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * pl::kWarpKernelWarps, smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t blocks = std::min<int64_t>((count + pl::kWarpKernelWarps - 1) / pl::kWarpKernelWarps,
+                                             (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, 32 * pl::kWarpKernelWarps, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out),
+                                                                   count, pt.tab, pt.off, status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
+bool use_warp_kernel() {
+    static const bool warp = [] {
+        const char* e = std::getenv("PL_BATCH_SMEM");
+        return !(e && std::string(e) == "cta");
+    }();
+    return warp;
+}
+
+// 6 <= n <= 14: the shared-memory kernels, specialised per order.
 template <class R>
 pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t count, int32_t* status,
                       cudaStream_t st) {
     Ptab pt;
     pl_status s = get_ptab(n, &pt);
     if (s != PL_OK) return s;
+    if constexpr (sizeof(typename R::T) == 8) {
+        if (use_warp_kernel()) {
+            switch (n) {
+#define PL_WARP_N(NN) \
+    case NN:          \
+        return launch_warp_n<R, NN>(a, out, count, status, st, pt);
+                PL_WARP_N(6) PL_WARP_N(7) PL_WARP_N(8) PL_WARP_N(9)
+#undef PL_WARP_N
+            }
+        }
+    }
     switch (n) {
 #define PL_SMEM_N(NN) \
     case NN:          \

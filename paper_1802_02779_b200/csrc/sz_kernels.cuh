@@ -289,18 +289,24 @@ __device__ __forceinline__ bool i64_fits_f64(const long long* a, int n) {
 
 // The layer DP of one matrix held in shared memory (see sz_batch_smem_kernel).
 // N > 0: the order is a compile-time constant (layer and term loops unroll).
-template <class RR, class TT, int N = 0>
+// WARP: the DP of one matrix by one warp (lane-strided outputs, __syncwarp
+// between layers) instead of the whole CTA.
+template <class RR, class TT, int N = 0, bool WARP = false>
 __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, int n_rt,
                                              const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff,
                                              bool& ov) {
     const int n = N > 0 ? N : n_rt;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x, nt = WARP ? 32 : (int)blockDim.x;
+    auto sync = [] {
+        if (WARP) __syncwarp();
+        else __syncthreads();
+    };
     const uint32_t c2 = poff[3] - poff[2];
     for (uint32_t r = tid; r < c2; r += nt) {
         const uint32_t e = __ldg(ptab + poff[2] + r);
         buf0[r] = base_pair<RR>(mat, n, (int)(e & 0xffu), (int)(e >> 8), ov);
     }
-    __syncthreads();
+    sync();
     TT* prev = buf0;
     TT* cur = buf1;
 #pragma unroll
@@ -326,7 +332,7 @@ __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, 
             }
             cur[r] = acc;
         }
-        __syncthreads();
+        sync();
         TT* t = prev;
         prev = cur;
         cur = t;
@@ -412,6 +418,103 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
         }
         __syncthreads();
     }
+}
+
+// Warp-per-matrix variant for 8-byte rings, 6 <= n <= 9 (the matrix and two
+// layers of one matrix fit a few KB, so many warps share an SM): no CTA barrier in
+// the layer loop, and the int64 exactness guard is computed by the warp (lane
+// i sums row i) instead of one thread.
+#ifndef PL_WARP_KERNEL_WARPS
+#define PL_WARP_KERNEL_WARPS 2
+#endif
+constexpr int kWarpKernelWarps = PL_WARP_KERNEL_WARPS;  // warps (matrices in flight) per CTA
+
+template <int N>
+__host__ __device__ constexpr int warp_kernel_stride() {
+    return ((N * N + 1) & ~1) + 2 * (((int)binom_u64(N, N / 2) + 1) & ~1);  // elements per warp
+}
+
+template <class R, int N>
+__global__ void __launch_bounds__(32 * kWarpKernelWarps) sz_batch_warp_kernel(
+    const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
+    const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, int32_t* __restrict__ status) {
+    using T = typename R::T;
+    static_assert(sizeof(T) == 8, "8-byte rings only");
+    constexpr int E = N * N;
+    constexpr int MAXC = (int)binom_u64(N, N / 2);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* mat = reinterpret_cast<T*>(smem_raw) + (size_t)warp * warp_kernel_stride<N>();
+    T* buf0 = mat + ((E + 1) & ~1);
+    T* buf1 = buf0 + ((MAXC + 1) & ~1);
+    bool ov_any = false;
+    for (int64_t b = (int64_t)blockIdx.x * kWarpKernelWarps + warp; b < count;
+         b += (int64_t)gridDim.x * kWarpKernelWarps) {
+        const T* g = a + b * E;
+        for (int e = lane; e < E; e += 32) mat[e] = g[e];
+        __syncwarp();
+        bool ov = false;
+        T total = R::zero();
+        if constexpr (R::kChecked) {
+            // guard of i64_guard_ok / i64_fits_f64, warp-parallel over rows
+            unsigned long long rs = 0;
+            double rd = 0.0;
+            bool ok = true;
+            if (lane < N) {
+                const long long* row = reinterpret_cast<const long long*>(mat) + lane * N;
+                for (int j = 0; j < N; ++j) {
+                    const long long v = row[j];
+                    ok &= v != (long long)0x8000000000000000ULL;
+                    const unsigned long long mg = v < 0 ? (unsigned long long)(-v) : (unsigned long long)v;
+                    const unsigned long long t = rs + mg;
+                    ok &= t >= rs;
+                    rs = t;
+                    rd += v < 0 ? -(double)v : (double)v;
+                }
+            }
+            unsigned long long prod = 1;
+            double pd = 1.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                unsigned long long r = __shfl_sync(0xffffffffu, rs, i);
+                const double d = __shfl_sync(0xffffffffu, rd, i);
+                r = r == 0 ? 1 : r;
+                ok &= __umul64hi(prod, r) == 0;
+                prod *= r;
+                ok &= prod < 0x8000000000000000ULL;
+                pd *= d < 1.0 ? 1.0 : d;
+            }
+            ok = __all_sync(0xffffffffu, ok);
+            if (pd < 9007199254740992.0) {
+                // exact in doubles: convert in place, FMA path
+                double* dm = reinterpret_cast<double*>(mat);
+                for (int e = lane; e < E; e += 32) dm[e] = (double)reinterpret_cast<const long long*>(mat)[e];
+                __syncwarp();
+                const double* last = smem_dp<RF64<true>, double, N, true>(dm, reinterpret_cast<double*>(buf0),
+                                                                          reinterpret_cast<double*>(buf1), N, ptab,
+                                                                          poff, ov);
+                if (lane == 0) total = (T)smem_top<RF64<true>, double, N>(dm, last, N, ov);
+            } else if (ok) {
+                const T* last = smem_dp<RI64<false>, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+                if (lane == 0) total = smem_top<RI64<false>, T, N>(mat, last, N, ov);
+            } else {
+                const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+                ov = __any_sync(0xffffffffu, ov);
+                if (lane == 0 && !ov) total = smem_top<R, T, N>(mat, last, N, ov);
+            }
+        } else {
+            const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+            if (lane == 0) total = smem_top<R, T, N>(mat, last, N, ov);
+        }
+        ov = __any_sync(0xffffffffu, ov);
+        if (lane == 0) {
+            if (ov) total = R::zero();
+            out[b] = total;
+        }
+        ov_any |= ov;
+        __syncwarp();
+    }
+    if (ov_any && lane == 0) atomicOr(status, 1);
 }
 
 // ---------------------------------------------------------------- layer 2

@@ -106,6 +106,16 @@ def test_int_orders_vs_oracle(n):
     assert np.array_equal(out, O.sz_batch(a))
 
 
+@pytest.mark.parametrize("n,h", [(6, 300), (8, 100), (9, 40), (11, 12)])
+def test_int_orders_checked_paths(n, h):
+    # entries up to +-h: the guard bound exceeds 2^53, so the batch kernels take
+    # the int64 / checked-int64 paths instead of exact doubles (every true value
+    # fits int64 for these seeds)
+    a = configs.int_matrices(n, 96, seed=4000 + n, lo=-h, hi=h)
+    out = pl.store_zechin_permanent_batch(a)
+    assert np.array_equal(out, O.sz_batch(a))
+
+
 @pytest.mark.parametrize("n", list(range(1, 21)) + [23, 24])
 def test_complex_orders_bitwise(n):
     count = 33 if n <= 12 else (3 if n <= 16 else 1)
