@@ -88,6 +88,15 @@ def ref():
         R.ref_full_distribution.argtypes = [C.c_int, _dp, C.c_int, _ip, C.c_uint64, _i64p, _ip, _dp]
         R.ref_sample.argtypes = [C.c_int, _dp, C.c_int, _ip, C.c_uint64, C.c_uint64, C.c_uint64, _ip]
         R.ref_enumerate_patterns.argtypes = [C.c_int, C.c_int, _i64p, _ip]
+        cp, sz = C.c_char_p, C.c_size_t
+        R.ref_fmt_value_text.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_double, cp, sz]
+        R.ref_fmt_perm_json.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_uint64,
+                                        cp, sz]
+        R.ref_fmt_dist_json.argtypes = [C.c_int, C.c_int, C.c_int64, _ip, _dp, cp, sz]
+        R.ref_fmt_sample_json.argtypes = [C.c_int, C.c_int64, _ip, cp, sz]
+        R.ref_fmt_itf_json.argtypes = [C.c_int, _dp, cp, sz]
+        R.ref_parse_matrix.argtypes = [cp, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _i64p, _dp,
+                                       C.c_int]
         _ref = R
     return _ref
 
@@ -361,3 +370,65 @@ def ref_enumerate_patterns(m: int, n: int) -> np.ndarray:
     if rc != 0:
         raise _ref_err(rc)
     return occ
+
+
+# ----------------------------------------------------------------- CLI formats (reference primitives)
+
+def _fmt_call(fn, *args) -> str:
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        rc = fn(*args, buf, cap)
+        if rc == 0:
+            return buf.value.decode()
+        if rc < 0:
+            raise _ref_err(-rc)
+        cap = max(cap * 2, rc)
+
+
+def ref_fmt_value_text(v) -> str:
+    if isinstance(v, (int, np.integer)):
+        return _fmt_call(ref().ref_fmt_value_text, 0, int(v), 0.0, 0.0)
+    z = complex(v)
+    return _fmt_call(ref().ref_fmt_value_text, 1, 0, z.real, z.imag)
+
+
+def ref_fmt_perm_json(v, order: int, mults: int, adds: int) -> str:
+    if isinstance(v, (int, np.integer)):
+        return _fmt_call(ref().ref_fmt_perm_json, 0, int(v), 0.0, 0.0, order, mults, adds)
+    z = complex(v)
+    return _fmt_call(ref().ref_fmt_perm_json, 1, 0, z.real, z.imag, order, mults, adds)
+
+
+def ref_fmt_dist_json(m: int, photons: int, occupancy: np.ndarray, probs: np.ndarray) -> str:
+    occ = np.ascontiguousarray(occupancy, dtype=np.int32)
+    pr = np.ascontiguousarray(probs, dtype=np.float64)
+    return _fmt_call(ref().ref_fmt_dist_json, m, photons, occ.shape[0], _ptr(occ, C.POINTER(C.c_int)), _ptr(pr, _dp))
+
+
+def ref_fmt_sample_json(occupancy: np.ndarray) -> str:
+    occ = np.ascontiguousarray(occupancy, dtype=np.int32)
+    return _fmt_call(ref().ref_fmt_sample_json, occ.shape[1], occ.shape[0], _ptr(occ, C.POINTER(C.c_int)))
+
+
+def ref_fmt_itf_json(u: np.ndarray) -> str:
+    u, up = _u_arg(u)
+    return _fmt_call(ref().ref_fmt_itf_json, u.shape[0], up)
+
+
+def ref_parse_matrix(text: str, csv: bool, csv_complex: bool = False):
+    """(order, ring 'int'|'complex'|'rational', entries) parsed by the reference."""
+    cap = 4096
+    ints = np.zeros(cap, dtype=np.int64)
+    cplx = np.zeros(2 * cap, dtype=np.float64)
+    order, ring = C.c_int(), C.c_int()
+    rc = ref().ref_parse_matrix(text.encode(), int(csv), int(csv_complex), C.byref(order), C.byref(ring),
+                                _ptr(ints, _i64p), _ptr(cplx, _dp), cap)
+    if rc != 0:
+        raise _ref_err(rc)
+    n = order.value
+    if ring.value == 0:
+        return n, "int", ints[:n * n].reshape(n, n).copy()
+    if ring.value == 1:
+        return n, "complex", cplx[:2 * n * n].view(np.complex128).reshape(n, n).copy()
+    return n, "rational", None

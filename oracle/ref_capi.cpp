@@ -23,7 +23,10 @@
 #include <thread>
 #include <vector>
 
+#include <json.hpp>
+
 #include "permlab/boson.hpp"
+#include "permlab/matrix.hpp"
 #include "permlab/permanent.hpp"
 
 using namespace permlab;
@@ -262,6 +265,100 @@ int ref_enumerate_patterns(int m, int n, std::int64_t* count, int* occupancy) {
         if (occupancy) {
             for (std::size_t i = 0; i < p.size(); ++i)
                 std::copy(p[i].occupancy.begin(), p[i].occupancy.end(), occupancy + i * static_cast<std::size_t>(m));
+        }
+    });
+}
+
+}  // extern "C"
+
+// ---- CLI output formats (test infrastructure for the device CLI,
+// paper_1802_02779_b200/cli.py): the reference's own formatting primitives
+// (permlab::to_string, Interferometer::to_json, parse_matrix/emit_matrix and
+// nlohmann::json's dump as the reference CLI uses it, tools/permlab_cli.cpp)
+// applied to given values, so the device CLI's bytes can be compared.
+
+namespace {
+
+int put_text(const std::string& t, char* buf, std::size_t cap) {
+    if (t.size() + 1 > cap) return static_cast<int>(t.size() + 1);
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+}
+
+nlohmann::json value_json(int ring, std::int64_t iv, double re, double im) {
+    if (ring == 0) return static_cast<long long>(iv);
+    return nlohmann::json::array({re, im});
+}
+
+}  // namespace
+
+extern "C" {
+
+// ring 0: int64 value iv; ring 1: complex (re, im)
+int ref_fmt_value_text(int ring, std::int64_t iv, double re, double im, char* buf, std::size_t cap) {
+    const RingElement v = ring == 0 ? RingElement(Int(static_cast<long long>(iv))) : RingElement(Cplx(re, im));
+    return put_text(to_string(v), buf, cap);
+}
+
+// the object run_perm prints for --format json
+int ref_fmt_perm_json(int ring, std::int64_t iv, double re, double im, int order, std::uint64_t mults,
+                      std::uint64_t adds, char* buf, std::size_t cap) {
+    const nlohmann::json j{{"algorithm", "store-zechin"},
+                           {"order", order},
+                           {"value", value_json(ring, iv, re, im)},
+                           {"counts", nlohmann::json{{"multiplications", mults}, {"additions", adds}}}};
+    return put_text(j.dump(2) + "\n", buf, cap);
+}
+
+// the object run_bs_dist prints for --format json: occupancy (count x m), probs (count)
+int ref_fmt_dist_json(int m, int photons, std::int64_t count, const int* occupancy, const double* probs, char* buf,
+                      std::size_t cap) {
+    nlohmann::json entries = nlohmann::json::array();
+    for (std::int64_t i = 0; i < count; ++i) {
+        std::vector<int> occ(occupancy + i * m, occupancy + (i + 1) * m);
+        entries.push_back(nlohmann::json{{"pattern", nlohmann::json(occ)}, {"probability", probs[i]}});
+    }
+    const nlohmann::json j{{"modes", m}, {"photons", photons}, {"entries", std::move(entries)}};
+    return put_text(j.dump(2) + "\n", buf, cap);
+}
+
+// compact dump of an array of occupancy arrays (run_bs_sample --format json)
+int ref_fmt_sample_json(int m, std::int64_t count, const int* occupancy, char* buf, std::size_t cap) {
+    nlohmann::json out = nlohmann::json::array();
+    for (std::int64_t i = 0; i < count; ++i) out.push_back(std::vector<int>(occupancy + i * m, occupancy + (i + 1) * m));
+    return put_text(out.dump() + "\n", buf, cap);
+}
+
+int ref_fmt_itf_json(int m, const double* u, char* buf, std::size_t cap) {
+    int rc = 0;
+    std::string t;
+    rc = guarded([&] { t = make_itf(m, u).to_json(); });
+    return rc ? -rc : put_text(t, buf, cap);
+}
+
+// parse a matrix file's text the reference way; out: order, ring (0 int, 1 complex), entries
+int ref_parse_matrix(const char* text, int csv, int csv_ring_complex, int* order, int* ring, std::int64_t* ints,
+                     double* cplx, int cap_entries) {
+    return guarded([&] {
+        const SquareMatrix m = parse_matrix(text, csv ? MatrixFormat::Csv : MatrixFormat::Json,
+                                            csv_ring_complex ? RingTag::Complex : RingTag::Int);
+        *order = m.order();
+        const int n = m.order();
+        if (n * n > cap_entries) throw DomainError("capacity");
+        if (m.ring() == RingTag::Int) {
+            *ring = 0;
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) ints[i * n + j] = static_cast<std::int64_t>(std::get<Int>(m.entry(i, j)).raw());
+        } else if (m.ring() == RingTag::Complex) {
+            *ring = 1;
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) {
+                    const Cplx z = std::get<Cplx>(m.entry(i, j));
+                    cplx[2 * (i * n + j)] = z.real();
+                    cplx[2 * (i * n + j) + 1] = z.imag();
+                }
+        } else {
+            *ring = 2;
         }
     });
 }
