@@ -213,6 +213,8 @@ bool smem_fits(pl_dtype dt, int n) { return n <= kSmemMaxOrder && smem_per_warp(
 struct Ptab {
     uint16_t* tab = nullptr;
     uint32_t* off = nullptr;
+    uint32_t* tab32[2] = {nullptr, nullptr};  // byte-offset entries for 8- and 16-byte elements
+    const uint32_t* t32(size_t es) const { return tab32[es == 16 ? 1 : 0]; }
 };
 
 // Predecessor table of order n (see sz_batch_smem_kernel), built once per
@@ -249,6 +251,16 @@ pl_status get_ptab(int n, Ptab* out) {
         }
     }
     Ptab p;
+    for (int w = 0; w < 2; ++w) {
+        // layers >= 3 as byte offsets: (rank * es) | (column * es) << 16 (es = 8, 16)
+        const uint32_t es = w == 0 ? 8u : 16u;
+        std::vector<uint32_t> t32(tab.size(), 0);
+        for (int k = 3; k < n; ++k)
+            for (uint32_t x = off[k]; x < off[k + 1]; ++x)
+                t32[x] = (uint32_t)(tab[x] & 0xfffu) * es | ((uint32_t)(tab[x] >> 12) * es) << 16;
+        PL_CUDA(cudaMalloc(&p.tab32[w], t32.size() * sizeof(uint32_t)));
+        PL_CUDA(cudaMemcpy(p.tab32[w], t32.data(), t32.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
     PL_CUDA(cudaMalloc(&p.tab, tab.size() * sizeof(uint16_t)));
     PL_CUDA(cudaMalloc(&p.off, off.size() * sizeof(uint32_t)));
     PL_CUDA(cudaMemcpy(p.tab, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
@@ -282,7 +294,7 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     per_sm = std::max(per_sm, 1);
     const int64_t blocks = std::min<int64_t>(count, (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, 128, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, N,
-                                              (int)max_layer(N), pt.tab, pt.off, status);
+                                              (int)max_layer(N), pt.tab, pt.off, pt.t32(sizeof(T)), status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
@@ -303,7 +315,7 @@ pl_status launch_warp_n(const void* a, void* out, int64_t count, int32_t* status
     const int64_t blocks = std::min<int64_t>((count + pl::kWarpKernelWarps - 1) / pl::kWarpKernelWarps,
                                              (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, 32 * pl::kWarpKernelWarps, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out),
-                                                                   count, pt.tab, pt.off, status);
+                                                                   count, pt.tab, pt.off, pt.t32(sizeof(T)), status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

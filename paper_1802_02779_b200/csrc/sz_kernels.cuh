@@ -291,10 +291,13 @@ __device__ __forceinline__ bool i64_fits_f64(const long long* a, int n) {
 // N > 0: the order is a compile-time constant (layer and term loops unroll).
 // WARP: the DP of one matrix by one warp (lane-strided outputs, __syncwarp
 // between layers) instead of the whole CTA.
+// ptab32 (layers >= 3) holds the same entries as byte offsets for this
+// element size: (rank(S \ {s_i}) * sizeof(TT)) | (s_i * sizeof(TT)) << 16, so a
+// term is one table load and two shared loads at (base + offset).
 template <class RR, class TT, int N = 0, bool WARP = false>
 __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, int n_rt,
                                              const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff,
-                                             bool& ov) {
+                                             const uint32_t* __restrict__ ptab32, bool& ov) {
     const int n = N > 0 ? N : n_rt;
     const int tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x, nt = WARP ? 32 : (int)blockDim.x;
     auto sync = [] {
@@ -312,23 +315,26 @@ __device__ __forceinline__ const TT* smem_dp(const TT* mat, TT* buf0, TT* buf1, 
 #pragma unroll
     for (int k = 3; k < n; ++k) {
         const uint32_t ck = N > 0 ? (uint32_t)binom_u64(N, k) : (poff[k + 1] - poff[k]) / (uint32_t)k;
-        const uint16_t* pt = ptab + poff[k];
-        const TT* row = mat + (k - 1) * n;
+        const uint32_t* pt = ptab32 + poff[k];
+        const char* row = reinterpret_cast<const char*>(mat + (k - 1) * n);
+        const char* pv = reinterpret_cast<const char*>(prev);
+        auto rowv = [&](uint32_t e) { return *reinterpret_cast<const TT*>(row + (e >> 16)); };
+        auto prevv = [&](uint32_t e) { return *reinterpret_cast<const TT*>(pv + (e & 0xffffu)); };
         for (uint32_t r = tid; r < ck; r += nt) {
             uint32_t e = __ldg(pt + r);
-            TT acc = RR::mul(row[e >> 12], prev[e & 0xfffu], ov);
+            TT acc = RR::mul(rowv(e), prevv(e), ov);
             int i = 1;
             for (; i + 4 <= k; i += 4) {
                 const uint32_t e0 = __ldg(pt + (i + 0) * ck + r), e1 = __ldg(pt + (i + 1) * ck + r);
                 const uint32_t e2 = __ldg(pt + (i + 2) * ck + r), e3 = __ldg(pt + (i + 3) * ck + r);
-                acc = RR::mac(acc, row[e0 >> 12], prev[e0 & 0xfffu], ov);
-                acc = RR::mac(acc, row[e1 >> 12], prev[e1 & 0xfffu], ov);
-                acc = RR::mac(acc, row[e2 >> 12], prev[e2 & 0xfffu], ov);
-                acc = RR::mac(acc, row[e3 >> 12], prev[e3 & 0xfffu], ov);
+                acc = RR::mac(acc, rowv(e0), prevv(e0), ov);
+                acc = RR::mac(acc, rowv(e1), prevv(e1), ov);
+                acc = RR::mac(acc, rowv(e2), prevv(e2), ov);
+                acc = RR::mac(acc, rowv(e3), prevv(e3), ov);
             }
             for (; i < k; ++i) {
                 e = __ldg(pt + i * ck + r);
-                acc = RR::mac(acc, row[e >> 12], prev[e & 0xfffu], ov);
+                acc = RR::mac(acc, rowv(e), prevv(e), ov);
             }
             cur[r] = acc;
         }
@@ -350,6 +356,43 @@ __device__ __forceinline__ TT smem_top(const TT* mat, const TT* last_layer, int 
     return total;
 }
 
+// Exact-path choice for one int64 matrix, computed by a whole warp (lane i
+// sums row i): 0 = exact in doubles (guard bound < 2^53, i64_fits_f64),
+// 1 = wrapping int64 (bound < 2^63, i64_guard_ok), 2 = checked int64.
+template <int N>
+__device__ __forceinline__ int warp_i64_mode(const long long* m) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long rs = 0;
+    double rd = 0.0;
+    bool ok = true;
+    if (lane < N) {
+        const long long* row = m + lane * N;
+        for (int j = 0; j < N; ++j) {
+            const long long v = row[j];
+            ok &= v != (long long)0x8000000000000000ULL;
+            const unsigned long long mg = v < 0 ? (unsigned long long)(-v) : (unsigned long long)v;
+            const unsigned long long t = rs + mg;
+            ok &= t >= rs;
+            rs = t;
+            rd += v < 0 ? -(double)v : (double)v;
+        }
+    }
+    unsigned long long prod = 1;
+    double pd = 1.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        unsigned long long r = __shfl_sync(0xffffffffu, rs, i);
+        const double d = __shfl_sync(0xffffffffu, rd, i);
+        r = r == 0 ? 1 : r;
+        ok &= __umul64hi(prod, r) == 0;
+        prod *= r;
+        ok &= prod < 0x8000000000000000ULL;
+        pd *= d < 1.0 ? 1.0 : d;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    return pd < 9007199254740992.0 ? 0 : (ok ? 1 : 2);
+}
+
 // One CTA per matrix at a time (persistent CTAs striding over the batch);
 // the matrix and two layer buffers live in the CTA's shared memory (16 KB at
 // n = 12, so ~14 CTAs share an SM). The predecessor structure is the same for
@@ -366,6 +409,7 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
                                                             typename R::T* __restrict__ out, int64_t count,
                                                             int n_rt, int maxc, const uint16_t* __restrict__ ptab,
                                                             const uint32_t* __restrict__ poff,
+                                                            const uint32_t* __restrict__ ptab32,
                                                             int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int n = N;
@@ -384,9 +428,9 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
         bool ov = false;
         T total = R::zero();
         if constexpr (R::kChecked) {
-            if (tid == 0) {
-                const long long* m = reinterpret_cast<const long long*>(mat);
-                mode = i64_fits_f64(m, n) ? 0 : (i64_guard_ok(m, n) ? 1 : 2);
+            if (tid < 32) {
+                const int md = warp_i64_mode<N>(reinterpret_cast<const long long*>(mat));
+                if (tid == 0) mode = md;
             }
             __syncthreads();
             if (mode == 0) {
@@ -394,19 +438,19 @@ __global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T*
                 for (int e = tid; e < n * n; e += nt) dm[e] = (double)mat[e];
                 __syncthreads();
                 const double* last = smem_dp<RF64<true>, double, N>(dm, reinterpret_cast<double*>(buf0),
-                                                         reinterpret_cast<double*>(buf1), n, ptab, poff, ov);
+                                                         reinterpret_cast<double*>(buf1), n, ptab, poff, ptab32, ov);
                 if (tid == 0) total = (T)smem_top<RF64<true>, double, N>(dm, last, n, ov);
             } else if (mode == 1) {
-                const T* last = smem_dp<RI64<false>, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
+                const T* last = smem_dp<RI64<false>, T, N>(mat, buf0, buf1, n, ptab, poff, ptab32, ov);
                 if (tid == 0) total = smem_top<RI64<false>, T, N>(mat, last, n, ov);
             } else {
-                const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
+                const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ptab32, ov);
                 if (ov) atomicOr(&flag, 1);
                 __syncthreads();
                 if (tid == 0 && !(flag & 1)) total = smem_top<R, T, N>(mat, last, n, ov);
             }
         } else {
-            const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ov);
+            const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ptab32, ov);
             if (tid == 0) total = smem_top<R, T, N>(mat, last, n, ov);
         }
         if (tid == 0) {
@@ -437,7 +481,8 @@ __host__ __device__ constexpr int warp_kernel_stride() {
 template <class R, int N>
 __global__ void __launch_bounds__(32 * kWarpKernelWarps) sz_batch_warp_kernel(
     const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
-    const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, int32_t* __restrict__ status) {
+    const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32,
+    int32_t* __restrict__ status) {
     using T = typename R::T;
     static_assert(sizeof(T) == 8, "8-byte rings only");
     constexpr int E = N * N;
@@ -456,54 +501,26 @@ __global__ void __launch_bounds__(32 * kWarpKernelWarps) sz_batch_warp_kernel(
         bool ov = false;
         T total = R::zero();
         if constexpr (R::kChecked) {
-            // guard of i64_guard_ok / i64_fits_f64, warp-parallel over rows
-            unsigned long long rs = 0;
-            double rd = 0.0;
-            bool ok = true;
-            if (lane < N) {
-                const long long* row = reinterpret_cast<const long long*>(mat) + lane * N;
-                for (int j = 0; j < N; ++j) {
-                    const long long v = row[j];
-                    ok &= v != (long long)0x8000000000000000ULL;
-                    const unsigned long long mg = v < 0 ? (unsigned long long)(-v) : (unsigned long long)v;
-                    const unsigned long long t = rs + mg;
-                    ok &= t >= rs;
-                    rs = t;
-                    rd += v < 0 ? -(double)v : (double)v;
-                }
-            }
-            unsigned long long prod = 1;
-            double pd = 1.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                unsigned long long r = __shfl_sync(0xffffffffu, rs, i);
-                const double d = __shfl_sync(0xffffffffu, rd, i);
-                r = r == 0 ? 1 : r;
-                ok &= __umul64hi(prod, r) == 0;
-                prod *= r;
-                ok &= prod < 0x8000000000000000ULL;
-                pd *= d < 1.0 ? 1.0 : d;
-            }
-            ok = __all_sync(0xffffffffu, ok);
-            if (pd < 9007199254740992.0) {
+            const int md = warp_i64_mode<N>(reinterpret_cast<const long long*>(mat));
+            if (md == 0) {
                 // exact in doubles: convert in place, FMA path
                 double* dm = reinterpret_cast<double*>(mat);
                 for (int e = lane; e < E; e += 32) dm[e] = (double)reinterpret_cast<const long long*>(mat)[e];
                 __syncwarp();
                 const double* last = smem_dp<RF64<true>, double, N, true>(dm, reinterpret_cast<double*>(buf0),
                                                                           reinterpret_cast<double*>(buf1), N, ptab,
-                                                                          poff, ov);
+                                                                          poff, ptab32, ov);
                 if (lane == 0) total = (T)smem_top<RF64<true>, double, N>(dm, last, N, ov);
-            } else if (ok) {
-                const T* last = smem_dp<RI64<false>, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+            } else if (md == 1) {
+                const T* last = smem_dp<RI64<false>, T, N, true>(mat, buf0, buf1, N, ptab, poff, ptab32, ov);
                 if (lane == 0) total = smem_top<RI64<false>, T, N>(mat, last, N, ov);
             } else {
-                const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+                const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ptab32, ov);
                 ov = __any_sync(0xffffffffu, ov);
                 if (lane == 0 && !ov) total = smem_top<R, T, N>(mat, last, N, ov);
             }
         } else {
-            const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ov);
+            const T* last = smem_dp<R, T, N, true>(mat, buf0, buf1, N, ptab, poff, ptab32, ov);
             if (lane == 0) total = smem_top<R, T, N>(mat, last, N, ov);
         }
         ov = __any_sync(0xffffffffu, ov);
