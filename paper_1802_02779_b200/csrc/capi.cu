@@ -46,6 +46,8 @@ pl_status cuda_fail(cudaError_t e, const char* what) {
     return fail(PL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+pl_status cuda_fail_if(cudaError_t e, const char* what) { return e == cudaSuccess ? PL_OK : cuda_fail(e, what); }
+
 #define PL_CUDA(expr)                                        \
     do {                                                     \
         cudaError_t _e = (expr);                             \
@@ -654,6 +656,84 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     return s;
 }
 
+// Host-pointer batches of batched orders: the batch moves in chunks so that the
+// upload of chunk i + 1 (copy stream), the kernel of chunk i (the caller's
+// stream) and the download of chunk i - 1 (second copy stream, the other PCIe
+// direction) overlap; the call then costs about the upload alone.
+constexpr size_t kPipeMinBytes = size_t(8) << 20;
+constexpr size_t kPipeChunkBytes = size_t(8) << 20;
+
+struct CopyStreams {
+    cudaStream_t up = nullptr, down = nullptr;
+};
+
+pl_status copy_streams(CopyStreams* out) {
+    static thread_local std::map<int, CopyStreams> cache;  // per thread and device
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    auto it = cache.find(dev);
+    if (it == cache.end()) {
+        CopyStreams cs;
+        PL_CUDA(cudaStreamCreateWithFlags(&cs.up, cudaStreamNonBlocking));
+        PL_CUDA(cudaStreamCreateWithFlags(&cs.down, cudaStreamNonBlocking));
+        it = cache.emplace(dev, cs).first;
+    }
+    *out = it->second;
+    return PL_OK;
+}
+
+pl_status pipelined_host_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out, void* a_dev,
+                               void* out_dev, bool fma, int32_t* status_dev, cudaStream_t st) {
+    CopyStreams cs;
+    pl_status s = copy_streams(&cs);
+    if (s != PL_OK) return s;
+    const size_t es = elem_size(dt);
+    const size_t mat_bytes = (size_t)n * n * es;
+    const int64_t per = std::max<int64_t>(32, (int64_t)(kPipeChunkBytes / mat_bytes) / 32 * 32);
+    const int64_t nchunks = (count + per - 1) / per;
+    std::vector<cudaEvent_t> evs;
+    auto make_event = [&](cudaEvent_t* e) -> pl_status {
+        PL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        evs.push_back(*e);
+        return PL_OK;
+    };
+    cudaEvent_t start;
+    s = make_event(&start);
+    if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(start, st), "cudaEventRecord");
+    if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(cs.up, start, 0), "cudaStreamWaitEvent");
+    if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(cs.down, start, 0), "cudaStreamWaitEvent");
+    for (int64_t c = 0; c < nchunks && s == PL_OK; ++c) {
+        const int64_t b0 = c * per, b1 = std::min<int64_t>(count, b0 + per);
+        const size_t off_in = (size_t)b0 * mat_bytes, len_in = (size_t)(b1 - b0) * mat_bytes;
+        cudaEvent_t up_done, k_done;
+        if ((s = make_event(&up_done)) != PL_OK || (s = make_event(&k_done)) != PL_OK) break;
+        s = cuda_fail_if(cudaMemcpyAsync(static_cast<char*>(a_dev) + off_in, static_cast<const char*>(a) + off_in,
+                                         len_in, cudaMemcpyHostToDevice, cs.up), "cudaMemcpyAsync(in)");
+        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(up_done, cs.up), "cudaEventRecord");
+        if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, up_done, 0), "cudaStreamWaitEvent");
+        if (s == PL_OK)
+            s = enqueue_batch(dt, n, b1 - b0, static_cast<const char*>(a_dev) + off_in,
+                              static_cast<char*>(out_dev) + (size_t)b0 * es, fma, status_dev, st);
+        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(k_done, st), "cudaEventRecord");
+        if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(cs.down, k_done, 0), "cudaStreamWaitEvent");
+        if (s == PL_OK)
+            s = cuda_fail_if(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)b0 * es,
+                                             static_cast<char*>(out_dev) + (size_t)b0 * es, (size_t)(b1 - b0) * es,
+                                             cudaMemcpyDeviceToHost, cs.down),
+                             "cudaMemcpyAsync(out)");
+    }
+    // the caller's stream continues after every download (and every upload)
+    cudaEvent_t up_all, down_all;
+    if (s == PL_OK && (s = make_event(&up_all)) == PL_OK && (s = make_event(&down_all)) == PL_OK) {
+        s = cuda_fail_if(cudaEventRecord(up_all, cs.up), "cudaEventRecord");
+        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(down_all, cs.down), "cudaEventRecord");
+        if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, up_all, 0), "cudaStreamWaitEvent");
+        if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, down_all, 0), "cudaStreamWaitEvent");
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);  // destruction is deferred until the event completes
+    return s;
+}
+
 // Synchronous wrapper: owns device copies for host pointers and a status
 // word; waits and maps the status word to PL_ERR_OVERFLOW.
 pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,
@@ -677,12 +757,23 @@ pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out,
     if (!dev_ptrs) {
         PL_CUDA(cudaMallocAsync(&a_dev, std::max<size_t>(in_bytes, 16), st));
         PL_CUDA(cudaMallocAsync(&out_dev, std::max<size_t>(out_bytes, 16), st));
-        PL_CUDA(cudaMemcpyAsync(a_dev, a, in_bytes, cudaMemcpyHostToDevice, st));
     }
-    pl_status s = enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
+    pl_status s = PL_OK;
+    bool out_copied = false;
+    static const bool host_pipe = [] {
+        const char* e = std::getenv("PL_HOST_PIPE");  // 0: one upload, one kernel, one download (A/B)
+        return !(e && e[0] == '0');
+    }();
+    if (!dev_ptrs && host_pipe && n <= kSmemMaxOrder && in_bytes >= kPipeMinBytes) {
+        s = pipelined_host_batch(dt, n, count, a, out, a_dev, out_dev, fma, status_dev, st);
+        out_copied = true;
+    } else {
+        if (!dev_ptrs) PL_CUDA(cudaMemcpyAsync(a_dev, a, in_bytes, cudaMemcpyHostToDevice, st));
+        s = enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
+    }
     int32_t status_host = 0;
     if (s == PL_OK) {
-        if (!dev_ptrs) {
+        if (!dev_ptrs && !out_copied) {
             const cudaError_t e = cudaMemcpyAsync(out, out_dev, out_bytes, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(out)");
         }
