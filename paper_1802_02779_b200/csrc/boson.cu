@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/permlab_b200.h"
@@ -47,10 +48,15 @@ template <class R, int N, bool VS>
 pl_status launch_fused(const pl::BosonParams& p, bool enumerate, cudaStream_t st) {
     const size_t smem = (enumerate ? table_bytes(p.m, N) : 0) + (VS ? (size_t)p.m * N * sizeof(double2) : 0);
     auto kern = pl::sz_boson_kernel<R, N, VS>;
-    static size_t have = 0;  // per instantiation; raised monotonically
-    if (smem > have) {
-        PLC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        have = smem;
+    {
+        // the attribute is a per-kernel maximum: raise it monotonically, under a lock
+        static std::mutex mu;
+        static size_t have = 0;  // per instantiation
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > have) {
+            PLC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            have = smem;
+        }
     }
     int per_sm = 1;
     PLC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kBosonThreads, smem));

@@ -178,11 +178,15 @@ pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status
     using Gm = pl::BatchGeom<T, N>;
     auto kern = pl::sz_batch_tma_kernel<R, N>;
     PL_CUDA(set_smem_once(kern, Gm::kSmem));
-    static int per_sm = 0;  // resident CTAs per SM (per instantiation)
-    if (per_sm == 0) {
-        PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Gm::kThreads, Gm::kSmem));
-        per_sm = std::max(per_sm, 1);
-    }
+    // resident CTAs per SM (per instantiation; thread-safe static initialisation)
+    static const int per_sm = [kern] {
+        int v = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, Gm::kThreads, Gm::kSmem) != cudaSuccess) {
+            cudaGetLastError();
+            v = 1;
+        }
+        return std::max(v, 1);
+    }();
     const int64_t batches = (count + Gm::kBatch - 1) / Gm::kBatch;
     const int64_t blocks = std::min<int64_t>((batches + Gm::kWarps - 1) / Gm::kWarps, (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, Gm::kThreads, Gm::kSmem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count,
