@@ -42,7 +42,9 @@
 //                          then the math), coalesced stores. The chunk loop is
 //                          specialised per low count m.
 // Geometry per element size (WsGeom): complex 3 groups x 4 warps, D = 14,
-// FS = 4; 8-byte 3 groups x 8 warps, D = 14, FS = 4.
+// FS = 2 segments per stage, 4 stages per group ring (C5 114 -> 108.5 ms against
+// FS = 4 x 2 stages in the same shared memory); 8-byte 3 groups x 8 warps, D = 14,
+// FS = 4, 2 stages.
 #pragma once
 
 #include <cstdint>
@@ -78,13 +80,13 @@ constexpr unsigned kPubSleepNs = PL_WS_PUBSLEEP;    // max poll sleep of publish
 #define PL_WS_D8 14
 #endif
 #ifndef PL_WS_NSG16
-#define PL_WS_NSG16 2
+#define PL_WS_NSG16 4
 #endif
 #ifndef PL_WS_NSG8
 #define PL_WS_NSG8 2
 #endif
 #ifndef PL_WS_FS16
-#define PL_WS_FS16 4
+#define PL_WS_FS16 2
 #endif
 #ifndef PL_WS_FS8
 #define PL_WS_FS8 4

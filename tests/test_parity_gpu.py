@@ -378,3 +378,32 @@ def test_cpp_device_suite():
     exe = ROOT / "tests" / "cpp" / "test_permanent_device"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_concurrent_host_threads():
+    # the entry points are reentrant (reference SPEC: pure, no global state): host
+    # threads calling at once get the same results as serial calls
+    import threading
+
+    jobs = [configs.c1(3000, seed=s) for s in (11, 12)] + [configs.complex_uniform((64, 9, 9), seed=13),
+                                                           configs.complex_uniform((1, 21, 21), seed=14)]
+    want = [O.sz_batch(a) for a in jobs]
+    got = [None] * len(jobs)
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                got[i] = pl.store_zechin_permanent_batch(jobs[i])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs
+    for g, w in zip(got, want):
+        assert np.array_equal(g.view(np.uint64) if g.dtype == np.complex128 else g,
+                              w.view(np.uint64) if w.dtype == np.complex128 else w)
