@@ -45,14 +45,15 @@ __device__ __forceinline__ typename R::T batch_eval(const typename R::T* local, 
         // int64, warp-uniform choice: exact doubles with FMA when every lane's
         // guard bound is below 2^53 (see i64_fits_f64), wrapping int64 below
         // 2^63, checked int64 otherwise.
-        const bool ok = i64_guard_ok_n<N>(local);
+        // the double bound (< 2^53) implies the int64 one (< 2^63, no INT64_MIN entry),
+        // so the int64 guard is only evaluated when some lane fails the double bound
         const unsigned act = __activemask();
-        if (__all_sync(act, ok && i64_fits_f64_n<N>(local))) {
+        if (__all_sync(act, i64_fits_f64_n<N>(local))) {
             double dv[kEnt];
 #pragma unroll
             for (int e = 0; e < kEnt; ++e) dv[e] = (double)local[e];
             return (T)perm_in_registers<RF64<true>, N>(dv, ov);
-        } else if (__all_sync(act, ok)) {
+        } else if (__all_sync(act, i64_guard_ok_n<N>(local))) {
             return perm_in_registers<RI64<false>, N>(local, ov);
         }
         return perm_in_registers<R, N>(local, ov);
