@@ -356,6 +356,9 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
 BOSON = dict(m=25, modes=[0, 1, 2, 3, 4], seed=2,
              desc="full outcome distribution of 5 photons in Haar(25) seed 2, input modes 0..4 "
                   "(118,755 patterns; the collision-aware form of C2's submatrices)")
+BOSON_LARGE = dict(m=40, modes=[0, 1, 2, 3, 4, 5], seed=6,
+                   desc="full outcome distribution of 6 photons in Haar(40) seed 6, input modes 0..5 "
+                        "(8,145,060 patterns: a launch long enough to reach the FP64 roofline)")
 FP64_PEAK = (18.518, "measured DMUL/DADD rate x 1 flop (profiles/microbench_b200.json; the non-FMA reference "
                      "rounding mode issues no DFMA)")
 
@@ -364,7 +367,7 @@ def boson_flops_per_pattern(n: int) -> int:
     return flops_per_perm(n, "complex128") + 3  # + |z|^2 (2 mul, 1 add); the divide not counted
 
 
-def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False):
+def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False, spec=None):
     """The boson driver's fused kernel (pl_boson_distribution): every pattern
     of the distribution enumerated, gathered, evaluated and normalised on the
     device. value: device buffers, asynchronous calls, events; e2e: the
@@ -374,9 +377,10 @@ def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False):
 
     from paper_1802_02779_b200 import boson as B
 
-    itf = B.haar_unitary(BOSON["m"], BOSON["seed"])
-    modes = BOSON["modes"]
-    count = B.pattern_count(BOSON["m"], len(modes))
+    spec = spec or BOSON
+    itf = B.haar_unitary(spec["m"], spec["seed"])
+    modes = spec["modes"]
+    count = B.pattern_count(spec["m"], len(modes))
     stream = torch.cuda.current_stream(device)
     out = torch.empty(count, dtype=torch.float64, device=device)
     status = torch.zeros(1, dtype=torch.int32, device=device)
@@ -432,12 +436,12 @@ def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False):
     achieved = boson_flops_per_pattern(len(modes)) * count / per_step / 1e12
     return {
         "value": value, "unit": "probabilities/s", "ms_per_step": 1000.0 * float(t.item()) / steps, "steps": steps,
-        "workload": BOSON["desc"], "patterns": count,
+        "workload": spec["desc"], "patterns": count,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK[0], "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK[0], "peak_source": FP64_PEAK[1],
-                     "kernel": "sz_boson_kernel<RC128,5,VS=1> (enumerate + gather + DP + |per|^2/prod occ!)",
+                     "kernel": f"sz_boson_kernel<RC128,{len(modes)},VS=1> (enumerate + gather + DP + |per|^2/prod occ!)",
                      "hbm_bytes_per_pattern": 8},
-        "e2e": {"value": e2e, "unit": "probabilities/s", "h2d_bytes_per_step": BOSON["m"] ** 2 * 16,
+        "e2e": {"value": e2e, "unit": "probabilities/s", "h2d_bytes_per_step": spec["m"] ** 2 * 16,
                 "d2h_bytes_per_step": count * 8},
     }
 
@@ -521,6 +525,7 @@ def main():
                                "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
                                             else "equal slices, all-gather") if r["sharded"] else None)}
             suite["boson"] = measure_boson(10, 3, rank, world, device, flush_buf, args.fma)
+            suite["boson_large"] = measure_boson(3, 3, rank, world, device, flush_buf, args.fma, BOSON_LARGE)
             if rank == 0 and world == 1 and not args.no_cpu:
                 suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
 
