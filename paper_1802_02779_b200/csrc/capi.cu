@@ -693,7 +693,11 @@ pl_status pipelined_host_batch(pl_dtype dt, int n, int64_t count, const void* a,
     if (s != PL_OK) return s;
     const size_t es = elem_size(dt);
     const size_t mat_bytes = (size_t)n * n * es;
-    const int64_t per = std::max<int64_t>(32, (int64_t)(kPipeChunkBytes / mat_bytes) / 32 * 32);
+    static const size_t chunk_bytes = [] {
+        const char* e = std::getenv("PL_HOST_CHUNK_MB");  // tuning: chunk size of the host pipeline
+        return e ? std::max<size_t>(1, (size_t)atoi(e)) << 20 : kPipeChunkBytes;
+    }();
+    const int64_t per = std::max<int64_t>(32, (int64_t)(chunk_bytes / mat_bytes) / 32 * 32);
     const int64_t nchunks = (count + per - 1) / per;
     std::vector<cudaEvent_t> evs;
     auto make_event = [&](cudaEvent_t* e) -> pl_status {
