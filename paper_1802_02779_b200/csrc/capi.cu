@@ -296,10 +296,10 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     auto kern = pl::sz_batch_smem_kernel<R, N>;
     PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;
-    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kSmemThreads, smem));
     per_sm = std::max(per_sm, 1);
     const int64_t blocks = std::min<int64_t>(count, (int64_t)num_sms() * per_sm);
-    kern<<<(unsigned)blocks, 128, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, N,
+    kern<<<(unsigned)blocks, pl::kSmemThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, N,
                                               (int)max_layer(N), pt.tab, pt.off, pt.t32(sizeof(T)), status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;

@@ -28,7 +28,10 @@ struct BatchGeom {
     static constexpr int kBatch = 32;                                   // matrices per warp batch
     static constexpr int kBatchElems = kBatch * kEnt;                   // entries per batch
     static constexpr unsigned kBatchBytes = kBatchElems * sizeof(T);    // a multiple of 16 (kBatch = 32)
-    static constexpr int kWarps = 4;                                    // warps per CTA
+#ifndef PL_BATCH_WARPS
+#define PL_BATCH_WARPS 4
+#endif
+    static constexpr int kWarps = PL_BATCH_WARPS;                       // warps per CTA
     static constexpr int kThreads = 32 * kWarps;
 #ifndef PL_BATCH_NBUF
 #define PL_BATCH_NBUF 1

@@ -404,8 +404,13 @@ __device__ __forceinline__ int warp_i64_mode(const long long* m) {
 // Integer matrices take one of three exact paths per matrix: doubles with FMA
 // when the guard bound is below 2^53, wrapping int64 below 2^63, checked int64
 // otherwise.
+#ifndef PL_SMEM_THREADS
+#define PL_SMEM_THREADS 128
+#endif
+constexpr int kSmemThreads = PL_SMEM_THREADS;  // threads per matrix (CTA) of the shared-memory kernel
+
 template <class R, int N>
-__global__ void __launch_bounds__(128) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
+__global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typename R::T* __restrict__ a,
                                                             typename R::T* __restrict__ out, int64_t count,
                                                             int n_rt, int maxc, const uint16_t* __restrict__ ptab,
                                                             const uint32_t* __restrict__ poff,
