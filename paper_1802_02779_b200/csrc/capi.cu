@@ -383,10 +383,16 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int
     const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
     const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
     std::vector<std::vector<uint32_t>> lists(grid);
-    std::vector<std::pair<uint64_t, int>> heap;  // (load, cta), min-heap
-    for (int b = 0; b < grid; ++b) heap.push_back({0, b});
-    auto cmp = [](const std::pair<uint64_t, int>& x, const std::pair<uint64_t, int>& y) { return x > y; };
-    std::make_heap(heap.begin(), heap.end(), cmp);
+    // least-loaded CTA, lowest index among equals: a bucket queue over loads (loads only
+    // grow, so the minimum moves forward), each bucket a bitset of CTAs -- O(1) per tile
+    const int words = (grid + 63) / 64;
+    std::vector<uint64_t> bits((size_t)words * 64, 0);  // bucket b at [b * words, (b + 1) * words)
+    auto bucket = [&](uint64_t b) -> uint64_t* {
+        if ((b + 1) * (uint64_t)words > bits.size()) bits.resize(std::max<size_t>(bits.size() * 2, (b + 1) * words), 0);
+        return bits.data() + b * (uint64_t)words;
+    };
+    for (int c = 0; c < grid; ++c) bucket(0)[c / 64] |= 1ull << (c % 64);
+    uint64_t min_load = 0;
     static const auto C = [] {
         std::vector<uint64_t> c(pl::kBinomDim * pl::kBinomDim);
         for (int a = 0; a < pl::kBinomDim; ++a)
@@ -409,11 +415,24 @@ pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int
         }
         if (hi <= lo) continue;
         const uint64_t chunks = (hi - lo + chunk - 1) / chunk;
-        std::pop_heap(heap.begin(), heap.end(), cmp);
-        auto& top = heap.back();
-        lists[top.second].push_back(F);
-        top.first += chunks;
-        std::push_heap(heap.begin(), heap.end(), cmp);
+        for (;;) {
+            uint64_t* w = bucket(min_load);
+            int c = -1;
+            for (int i = 0; i < words; ++i) {
+                if (w[i]) {
+                    c = i * 64 + __builtin_ctzll(w[i]);
+                    break;
+                }
+            }
+            if (c < 0) {
+                ++min_load;
+                continue;
+            }
+            w[c / 64] &= ~(1ull << (c % 64));
+            lists[c].push_back(F);
+            bucket(min_load + chunks)[c / 64] |= 1ull << (c % 64);
+            break;
+        }
     }
     std::vector<uint32_t> flat(grid + 1, 0);
     for (int b = 0; b < grid; ++b) flat[b + 1] = flat[b] + (uint32_t)lists[b].size();
