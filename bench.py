@@ -533,9 +533,13 @@ def main():
                                "timing": r["timing"],
                                "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
                                             else "equal slices, all-gather") if r["sharded"] else None)}
-            suite["boson"] = measure_boson(10, 3, rank, world, device, flush_buf, args.fma)
-            suite["boson_large"] = measure_boson(3, 3, rank, world, device, flush_buf, args.fma, BOSON_LARGE)
-            if rank == 0 and world == 1 and not args.no_cpu:
+            for key, steps_b, spec_b in (("boson", 10, BOSON), ("boson_large", 3, BOSON_LARGE)):
+                try:
+                    suite[key] = measure_boson(steps_b, 3, rank, world, device, flush_buf, args.fma, spec_b)
+                except Exception as e:
+                    print(f"bench: suite entry {key} failed: {e!r}", file=sys.stderr, flush=True)
+                    suite[key] = {"error": repr(e)[:300]}
+            if rank == 0 and world == 1 and not args.no_cpu and "error" not in suite["boson"]:
                 suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
 
     cpu = None
@@ -566,8 +570,11 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        try:
+            dist.barrier()
+            dist.destroy_process_group()
+        except Exception as e:  # the JSON line is already out
+            print(f"bench: teardown: {e!r}", file=sys.stderr, flush=True)
     return 0
 
 
