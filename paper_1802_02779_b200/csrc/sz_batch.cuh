@@ -2,14 +2,16 @@
 // registers (perm_in_registers, compile-time subset masks), inputs staged per
 // warp through shared memory.
 //
-// Each warp owns batches of 32 consecutive matrices (32 * n^2 entries, one
-// contiguous run) and two shared-memory buffers. One lane issues a single
-// cp.async.bulk (TMA) for the warp's next batch while the warp computes the
-// current one, so HBM reads are whole-batch bulk transfers that overlap the
-// FP64/INT64 arithmetic; thread `lane` then reads its own matrix from shared
-// memory (stride n^2 elements: conflict-free for 8- and 16-byte entries).
-// A trailing partial batch, or an input pointer that is not 16-byte aligned,
-// is read directly from global memory.
+// sz_batch_tma_kernel: each warp owns batches of 32 consecutive matrices
+// (32 * n^2 entries, one contiguous run) and a shared-memory buffer. Thread
+// `lane` copies its matrix to registers (stride n^2 elements: conflict-free for
+// 8- and 16-byte entries), then one lane refills the buffer with the warp's next
+// batch by a single cp.async.bulk (TMA) -- only once every lane's loads have
+// returned (loaded_dep) -- while the warp computes, so HBM reads are whole-batch
+// bulk transfers that overlap the FP64/INT64 arithmetic. A trailing partial
+// batch, or an input pointer that is not 16-byte aligned, is read directly from
+// global memory. sz_batch_pipe_kernel (below, inputs >= 64 MiB): one CTA per SM,
+// a producer warp and a ring of batches.
 //
 // Reference: the per-matrix recurrence is proj/src/permanent.cpp:254-302
 // (see sz_kernels.cuh for the evaluation order).

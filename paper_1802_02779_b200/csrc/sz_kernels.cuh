@@ -15,11 +15,13 @@
 // term), visiting the terms in the reference's ascending-j order.
 //
 // Kernels here:
-//   (n <= 5: sz_batch_tma_kernel in sz_batch.cuh, one thread per matrix with
-//                         the whole DP in registers, warp batches staged by TMA.)
-//   sz_batch_smem_kernel  6 <= n <= 14: one CTA per matrix, ping-pong
+//   (n <= 5: sz_batch_tma_kernel / sz_batch_pipe_kernel in sz_batch.cuh, one
+//                         thread per matrix with the whole DP in registers,
+//                         batches staged by TMA.)
+//   sz_batch_warp_kernel  6 <= n <= 9, 8-byte rings: one warp per matrix.
+//   sz_batch_smem_kernel  otherwise up to n = 14: one CTA per matrix, ping-pong
 //                         layers and the matrix in shared memory, predecessor
-//                         ranks from a host-built table shared by the batch.
+//                         offsets from a host-built table shared by the batch.
 //   sz_base_layer_kernel  layer 2 (order-2 base case) of a single large matrix;
 //                         layers >= 3 run in the warp-specialised kernel (sz_ws.cuh).
 //   sz_top_kernel         the final n-term development.
