@@ -38,9 +38,10 @@
 //                          cp.async.bulk per segment, mbarrier tx counts.
 //   consumers (G groups    take alternate chunks, PER outputs per thread: low
 //   of GW warps)           terms from the source ring, high terms from the
-//                          group's ring (read to registers, slot handed back,
-//                          then the math), coalesced stores. The chunk loop is
-//                          specialised per low count m.
+//                          group's ring (read to registers; every thread hands
+//                          the slot back once its own loads have returned,
+//                          loaded_dep; then the math), coalesced stores. The
+//                          chunk loop is specialised per low count m.
 // Geometry per element size (WsGeom): complex 3 groups x 4 warps, D = 14,
 // FS = 2 segments per stage, 4 stages per group ring (C5 114 -> 108.5 ms against
 // FS = 4 x 2 stages in the same shared memory); 8-byte 3 groups x 8 warps, D = 14,
