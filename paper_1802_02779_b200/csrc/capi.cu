@@ -305,6 +305,33 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     return PL_OK;
 }
 
+// Pair kernel for 8-byte rings, 10 <= n <= 14 (PL_BATCH_PAIR=0 disables).
+bool use_pair_kernel() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_BATCH_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <class R, int N>
+pl_status launch_pair_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st, const Ptab& pt) {
+    using T = typename R::T;
+    const int maxc = (int)max_layer(N);
+    const size_t smem = (size_t)(N * N + 2 * maxc) * 16 + 64;  // pair layout (the single layout fits inside)
+    auto kern = pl::sz_batch_smem_pair_kernel<R, N>;
+    PL_CUDA(set_smem_once(kern, smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kSmemThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t pairs = (count + 1) / 2;
+    const int64_t blocks = std::min<int64_t>(pairs, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, pl::kSmemThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, maxc,
+                                                          pt.tab, pt.off, pt.t32(8), pt.t32(16), status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
 // Warp-per-matrix kernel for 8-byte rings, 6 <= n <= 9 (PL_BATCH_SMEM=cta forces the CTA
 // kernel). Measured (profiles/c3_ab.py): n = 8 x 50k int64 104 -> 74 us; equal at n = 10;
 // slower at n = 12 (C3: 205 -> 293 us), where a matrix's layers take ~16 KB and a warp per
@@ -349,6 +376,15 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
         return launch_warp_n<R, NN>(a, out, count, status, st, pt);
                 PL_WARP_N(6) PL_WARP_N(7) PL_WARP_N(8) PL_WARP_N(9)
 #undef PL_WARP_N
+            }
+        }
+        if (use_pair_kernel() && count >= 2) {
+            switch (n) {
+#define PL_PAIR_N(NN) \
+    case NN:          \
+        return launch_pair_n<R, NN>(a, out, count, status, st, pt);
+                PL_PAIR_N(10) PL_PAIR_N(11) PL_PAIR_N(12) PL_PAIR_N(13) PL_PAIR_N(14)
+#undef PL_PAIR_N
             }
         }
     }

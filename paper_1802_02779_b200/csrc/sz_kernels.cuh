@@ -471,6 +471,156 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
     }
 }
 
+// Two matrices evaluated in lockstep (8-byte rings): every value is a pair
+// {matrix A, matrix B} stored as one 16-byte word, so each term is one table
+// load, two 16-byte shared loads and two products -- the predecessor table and
+// the barriers are shared by the pair. Operations apply to both halves in the
+// same order, so each half is bitwise what the single-matrix DP computes.
+template <class RR>
+struct PairRing {
+    struct __align__(16) T {
+        typename RR::T a, b;
+    };
+    static constexpr bool kChecked = RR::kChecked;
+    __device__ __forceinline__ static T mul(T x, T y, bool& ov) { return {RR::mul(x.a, y.a, ov), RR::mul(x.b, y.b, ov)}; }
+    __device__ __forceinline__ static T add(T x, T y, bool& ov) { return {RR::add(x.a, y.a, ov), RR::add(x.b, y.b, ov)}; }
+    __device__ __forceinline__ static T mac(T acc, T x, T y, bool& ov) {
+        return {RR::mac(acc.a, x.a, y.a, ov), RR::mac(acc.b, x.b, y.b, ov)};
+    }
+    __device__ __forceinline__ static T zero() { return {RR::zero(), RR::zero()}; }
+};
+
+// The ring a pair runs in: the ring itself for doubles, exact doubles (FMA) for
+// int64 matrices whose guard bound is below 2^53.
+template <class R>
+struct PairBase {
+    using type = R;
+};
+template <>
+struct PairBase<RI64<true>> {
+    using type = RF64<true>;
+};
+
+// CTA per pair of matrices (8-byte rings, 10 <= n <= 14): the pair DP when both
+// matrices take the same exact path, else each matrix on its own (contiguous
+// layout in the same shared memory).
+template <class R, int N>
+__global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_pair_kernel(
+    const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count, int maxc,
+    const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
+    const uint32_t* __restrict__ ptab32_16, int32_t* __restrict__ status) {
+    using T = typename R::T;
+    static_assert(sizeof(T) == 8, "8-byte rings only");
+    constexpr int n = N, E = N * N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int mode[2], flag;
+    const int tid = threadIdx.x;
+    const int64_t npairs = (count + 1) / 2;
+    for (int64_t pb = blockIdx.x; pb < npairs; pb += gridDim.x) {
+        const int64_t b0 = 2 * pb;
+        const bool two = b0 + 1 < count;
+        const T* g0 = a + b0 * E;
+        const T* g1 = a + (b0 + 1) * E;
+        if (tid == 0) flag = 0;
+        if constexpr (R::kChecked) {
+            const int w = tid >> 5;
+            if (w < 2 && (w == 0 || two)) {
+                const int md = warp_i64_mode<N>(reinterpret_cast<const long long*>(w == 0 ? g0 : g1));
+                if ((tid & 31) == 0) mode[w] = md;
+            }
+        }
+        __syncthreads();
+        const int m0 = R::kChecked ? mode[0] : 0;
+        const bool joint = two && (!R::kChecked || (m0 == mode[1] && m0 < 2));
+        if (joint) {
+            // interleaved pairs: mat[e] = {A[e], B[e]}; layers likewise
+            if (!R::kChecked || m0 == 0) {
+                using PR = PairRing<typename PairBase<R>::type>;  // doubles (exact for int64 here)
+                using PT = typename PR::T;
+                PT* mat = reinterpret_cast<PT*>(smem_raw);
+                PT* buf0 = mat + E;
+                PT* buf1 = buf0 + maxc;
+                for (int e = tid; e < E; e += blockDim.x) {
+                    if constexpr (R::kChecked) {
+                        mat[e] = {(double)reinterpret_cast<const long long*>(g0)[e],
+                                  (double)reinterpret_cast<const long long*>(g1)[e]};
+                    } else {
+                        mat[e] = {reinterpret_cast<const double*>(g0)[e], reinterpret_cast<const double*>(g1)[e]};
+                    }
+                }
+                __syncthreads();
+                bool ov = false;
+                const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
+                if (tid == 0) {
+                    const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
+                    out[b0] = (T)t.a;  // exact: integer-valued doubles for the int64 ring
+                    out[b0 + 1] = (T)t.b;
+                }
+            } else if constexpr (R::kChecked) {
+                using PR = PairRing<RI64<false>>;
+                using PT = typename PR::T;
+                PT* mat = reinterpret_cast<PT*>(smem_raw);
+                PT* buf0 = mat + E;
+                PT* buf1 = buf0 + maxc;
+                for (int e = tid; e < E; e += blockDim.x)
+                    mat[e] = {reinterpret_cast<const long long*>(g0)[e], reinterpret_cast<const long long*>(g1)[e]};
+                __syncthreads();
+                bool ov = false;
+                const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
+                if (tid == 0) {
+                    const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
+                    out[b0] = (T)t.a;
+                    out[b0 + 1] = (T)t.b;
+                }
+            }
+        } else {
+            // one matrix at a time, contiguous layout (the single-matrix kernel's path)
+            for (int h = 0; h < (two ? 2 : 1); ++h) {
+                const T* g = h == 0 ? g0 : g1;
+                T* mat = reinterpret_cast<T*>(smem_raw);
+                T* buf0 = mat + ((E + 1) & ~1);
+                T* buf1 = buf0 + ((maxc + 1) & ~1);
+                for (int e = tid; e < E; e += blockDim.x) mat[e] = g[e];
+                if (tid == 0) flag = 0;
+                __syncthreads();
+                bool ov = false;
+                T total = R::zero();
+                const int md = R::kChecked ? mode[h] : 2;
+                if constexpr (R::kChecked) {
+                    if (md == 0) {
+                        double* dm = reinterpret_cast<double*>(mat);
+                        for (int e = tid; e < E; e += blockDim.x)
+                            dm[e] = (double)reinterpret_cast<const long long*>(mat)[e];
+                        __syncthreads();
+                        const double* last = smem_dp<RF64<true>, double, N>(
+                            dm, reinterpret_cast<double*>(buf0), reinterpret_cast<double*>(buf1), n, ptab, poff,
+                            ptab32_8, ov);
+                        if (tid == 0) total = (T)smem_top<RF64<true>, double, N>(dm, last, n, ov);
+                    } else if (md == 1) {
+                        const T* last = smem_dp<RI64<false>, T, N>(mat, buf0, buf1, n, ptab, poff, ptab32_8, ov);
+                        if (tid == 0) total = smem_top<RI64<false>, T, N>(mat, last, n, ov);
+                    }
+                }
+                if (md == 2) {
+                    const T* last = smem_dp<R, T, N>(mat, buf0, buf1, n, ptab, poff, ptab32_8, ov);
+                    if (ov) atomicOr(&flag, 1);
+                    __syncthreads();
+                    if (tid == 0 && !(flag & 1)) total = smem_top<R, T, N>(mat, last, n, ov);
+                }
+                if (tid == 0) {
+                    if ((flag & 1) || ov) {
+                        atomicOr(status, 1);
+                        total = R::zero();
+                    }
+                    out[b0 + h] = total;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Warp-per-matrix variant for 8-byte rings, 6 <= n <= 9 (the matrix and two
 // layers of one matrix fit a few KB, so many warps share an SM): no CTA barrier in
 // the layer loop, and the int64 exactness guard is computed by the warp (lane
