@@ -407,3 +407,24 @@ def test_concurrent_host_threads():
     for g, w in zip(got, want):
         assert np.array_equal(g.view(np.uint64) if g.dtype == np.complex128 else g,
                               w.view(np.uint64) if w.dtype == np.complex128 else w)
+
+
+@pytest.mark.parametrize("n", [10, 12, 14])
+def test_pair_kernel_mixed_modes_and_odd_counts(n):
+    # the pair kernel runs two matrices in lockstep when their int64 guards agree and
+    # one at a time otherwise; alternate small (exact-in-double) and larger entries
+    # (int64 / checked paths) and leave an odd matrix at the end
+    small = configs.int_matrices(n, 9, seed=5000 + n, lo=0, hi=1)
+    h = {10: 20, 12: 15, 14: 8}[n]  # guard bounds above 2^53: the int64 / checked-int64 paths
+    big = configs.int_matrices(n, 8, seed=6000 + n, lo=-h, hi=h)
+    a = np.empty((17, n, n), dtype=np.int64)
+    a[0::2], a[1::2] = small, big
+    try:
+        want = O.sz_batch(a)
+    except Exception:  # pragma: no cover
+        pytest.skip("oracle overflow")
+    if np.any(np.abs(want.astype(object)) >= 2 ** 63):  # pragma: no cover
+        pytest.skip("values beyond int64")
+    assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
+    f = configs.uniform((17, n, n), seed=7000 + n)
+    assert np.array_equal(pl.store_zechin_permanent_batch(f).view(np.uint64), O.sz_batch(f).view(np.uint64))
