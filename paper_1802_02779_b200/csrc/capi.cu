@@ -219,8 +219,8 @@ bool smem_fits(pl_dtype dt, int n) { return n <= kSmemMaxOrder && smem_per_warp(
 struct Ptab {
     uint16_t* tab = nullptr;
     uint32_t* off = nullptr;
-    uint32_t* tab32[2] = {nullptr, nullptr};  // byte-offset entries for 8- and 16-byte elements
-    const uint32_t* t32(size_t es) const { return tab32[es == 16 ? 1 : 0]; }
+    uint32_t* tab32[3] = {nullptr, nullptr, nullptr};  // byte-offset entries for 8-, 16- and 32-byte elements
+    const uint32_t* t32(size_t es) const { return tab32[es == 32 ? 2 : es == 16 ? 1 : 0]; }
 };
 
 // Predecessor table of order n (see sz_batch_smem_kernel), built once per
@@ -257,9 +257,11 @@ pl_status get_ptab(int n, Ptab* out) {
         }
     }
     Ptab p;
-    for (int w = 0; w < 2; ++w) {
-        // layers >= 3 as byte offsets: (rank * es) | (column * es) << 16 (es = 8, 16)
-        const uint32_t es = w == 0 ? 8u : 16u;
+    for (int w = 0; w < 3; ++w) {
+        // layers >= 3 as byte offsets: (rank * es) | (column * es) << 16 (es = 8, 16, 32;
+        // 32 only where the largest rank * 32 fits 16 bits, n <= 13)
+        const uint32_t es = w == 0 ? 8u : w == 1 ? 16u : 32u;
+        if (es * (uint32_t)max_layer(n) >= 65536u) continue;
         std::vector<uint32_t> t32(tab.size(), 0);
         for (int k = 3; k < n; ++k)
             for (uint32_t x = off[k]; x < off[k + 1]; ++x)
@@ -305,29 +307,34 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     return PL_OK;
 }
 
-// Pair kernel for 8-byte rings, 10 <= n <= 14 (PL_BATCH_PAIR=0 disables).
-bool use_pair_kernel() {
-    static const bool on = [] {
-        const char* e = std::getenv("PL_BATCH_PAIR");
-        return !(e && e[0] == '0');
+// Pack kernel for 8-byte rings, 10 <= n <= 14: P matrices per CTA in lockstep.
+// P = 2 by default (C3 197 -> 182 us); P = 4 (PL_BATCH_PACK=4, n <= 13, where 16-bit
+// byte offsets of 32-byte packs fit) measured slower (233 us: fewer packs per SM);
+// PL_BATCH_PACK=1 runs the one-matrix kernel.
+int pack_width(int n) {
+    static const int force = [] {
+        const char* e = std::getenv("PL_BATCH_PACK");
+        return e ? atoi(e) : 0;
     }();
-    return on;
+    if (force == 1) return 1;
+    if (force == 4 && n <= 13) return 4;
+    return 2;
 }
 
-template <class R, int N>
-pl_status launch_pair_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st, const Ptab& pt) {
+template <class R, int N, int P>
+pl_status launch_pack_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st, const Ptab& pt) {
     using T = typename R::T;
     const int maxc = (int)max_layer(N);
-    const size_t smem = (size_t)(N * N + 2 * maxc) * 16 + 64;  // pair layout (the single layout fits inside)
-    auto kern = pl::sz_batch_smem_pair_kernel<R, N>;
+    const size_t smem = (size_t)(N * N + 2 * maxc) * 8 * P + 64;  // pack layout (the single layout fits inside)
+    auto kern = pl::sz_batch_smem_pack_kernel<R, N, P>;
     PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;
     PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kSmemThreads, smem));
     per_sm = std::max(per_sm, 1);
-    const int64_t pairs = (count + 1) / 2;
-    const int64_t blocks = std::min<int64_t>(pairs, (int64_t)num_sms() * per_sm);
+    const int64_t packs = (count + P - 1) / P;
+    const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, pl::kSmemThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, maxc,
-                                                          pt.tab, pt.off, pt.t32(8), pt.t32(16), status);
+                                                          pt.tab, pt.off, pt.t32(8), pt.t32(8 * P), status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
@@ -378,13 +385,15 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
 #undef PL_WARP_N
             }
         }
-        if (use_pair_kernel() && count >= 2) {
-            switch (n) {
-#define PL_PAIR_N(NN) \
-    case NN:          \
-        return launch_pair_n<R, NN>(a, out, count, status, st, pt);
-                PL_PAIR_N(10) PL_PAIR_N(11) PL_PAIR_N(12) PL_PAIR_N(13) PL_PAIR_N(14)
-#undef PL_PAIR_N
+        const int P = n >= 10 && n <= 14 ? pack_width(n) : 1;
+        if (P > 1 && count >= 2) {
+            switch (n * 8 + P) {
+#define PL_PACK_N(NN, PP) \
+    case NN * 8 + PP:     \
+        return launch_pack_n<R, NN, PP>(a, out, count, status, st, pt);
+                PL_PACK_N(10, 2) PL_PACK_N(11, 2) PL_PACK_N(12, 2) PL_PACK_N(13, 2) PL_PACK_N(14, 2)
+                PL_PACK_N(10, 4) PL_PACK_N(11, 4) PL_PACK_N(12, 4) PL_PACK_N(13, 4)
+#undef PL_PACK_N
             }
         }
     }

@@ -471,116 +471,127 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
     }
 }
 
-// Two matrices evaluated in lockstep (8-byte rings): every value is a pair
-// {matrix A, matrix B} stored as one 16-byte word, so each term is one table
-// load, two 16-byte shared loads and two products -- the predecessor table and
-// the barriers are shared by the pair. Operations apply to both halves in the
-// same order, so each half is bitwise what the single-matrix DP computes.
-template <class RR>
-struct PairRing {
-    struct __align__(16) T {
-        typename RR::T a, b;
+// P matrices evaluated in lockstep (8-byte rings): every value is a pack
+// {matrix 0, ..., matrix P-1} of P * 8 bytes, so each term is one table load,
+// two P * 8-byte shared loads and P products -- the predecessor table and the
+// barriers are shared by the pack. Operations apply to every member in the same
+// order, so each member is bitwise what the single-matrix DP computes.
+template <class RR, int P>
+struct PackRing {
+    struct __align__(8 * P) T {
+        typename RR::T v[P];
     };
     static constexpr bool kChecked = RR::kChecked;
-    __device__ __forceinline__ static T mul(T x, T y, bool& ov) { return {RR::mul(x.a, y.a, ov), RR::mul(x.b, y.b, ov)}; }
-    __device__ __forceinline__ static T add(T x, T y, bool& ov) { return {RR::add(x.a, y.a, ov), RR::add(x.b, y.b, ov)}; }
-    __device__ __forceinline__ static T mac(T acc, T x, T y, bool& ov) {
-        return {RR::mac(acc.a, x.a, y.a, ov), RR::mac(acc.b, x.b, y.b, ov)};
+    __device__ __forceinline__ static T mul(T x, T y, bool& ov) {
+        T r;
+#pragma unroll
+        for (int i = 0; i < P; ++i) r.v[i] = RR::mul(x.v[i], y.v[i], ov);
+        return r;
     }
-    __device__ __forceinline__ static T zero() { return {RR::zero(), RR::zero()}; }
+    __device__ __forceinline__ static T add(T x, T y, bool& ov) {
+        T r;
+#pragma unroll
+        for (int i = 0; i < P; ++i) r.v[i] = RR::add(x.v[i], y.v[i], ov);
+        return r;
+    }
+    __device__ __forceinline__ static T mac(T acc, T x, T y, bool& ov) {
+        T r;
+#pragma unroll
+        for (int i = 0; i < P; ++i) r.v[i] = RR::mac(acc.v[i], x.v[i], y.v[i], ov);
+        return r;
+    }
+    __device__ __forceinline__ static T zero() {
+        T r;
+#pragma unroll
+        for (int i = 0; i < P; ++i) r.v[i] = RR::zero();
+        return r;
+    }
 };
 
-// The ring a pair runs in: the ring itself for doubles, exact doubles (FMA) for
+// The ring a pack runs in: the ring itself for doubles, exact doubles (FMA) for
 // int64 matrices whose guard bound is below 2^53.
 template <class R>
-struct PairBase {
+struct PackBase {
     using type = R;
 };
 template <>
-struct PairBase<RI64<true>> {
+struct PackBase<RI64<true>> {
     using type = RF64<true>;
 };
 
-// CTA per pair of matrices (8-byte rings, 10 <= n <= 14): the pair DP when both
-// matrices take the same exact path, else each matrix on its own (contiguous
-// layout in the same shared memory).
-template <class R, int N>
-__global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_pair_kernel(
+// CTA per pack of P matrices (8-byte rings, 10 <= n <= 14): the pack DP when every
+// member takes the same exact path, else each matrix on its own (contiguous
+// layout in the same shared memory). ptab32p: byte offsets for 8 * P-byte packs.
+template <class R, int N, int P>
+__global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_pack_kernel(
     const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count, int maxc,
     const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
-    const uint32_t* __restrict__ ptab32_16, int32_t* __restrict__ status) {
+    const uint32_t* __restrict__ ptab32p, int32_t* __restrict__ status) {
     using T = typename R::T;
     static_assert(sizeof(T) == 8, "8-byte rings only");
+    static_assert(kSmemThreads / 32 >= P, "one warp per member for the guards");
     constexpr int n = N, E = N * N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int mode[2], flag;
+    __shared__ int mode[P], flag;
     const int tid = threadIdx.x;
-    const int64_t npairs = (count + 1) / 2;
-    for (int64_t pb = blockIdx.x; pb < npairs; pb += gridDim.x) {
-        const int64_t b0 = 2 * pb;
-        const bool two = b0 + 1 < count;
-        const T* g0 = a + b0 * E;
-        const T* g1 = a + (b0 + 1) * E;
+    const int64_t npacks = (count + P - 1) / P;
+    for (int64_t pb = blockIdx.x; pb < npacks; pb += gridDim.x) {
+        const int64_t b0 = P * pb;
+        const int have = count - b0 < P ? (int)(count - b0) : P;
+        const T* g = a + b0 * E;
         if (tid == 0) flag = 0;
         if constexpr (R::kChecked) {
             const int w = tid >> 5;
-            if (w < 2 && (w == 0 || two)) {
-                const int md = warp_i64_mode<N>(reinterpret_cast<const long long*>(w == 0 ? g0 : g1));
+            if (w < have) {
+                const int md = warp_i64_mode<N>(reinterpret_cast<const long long*>(g + (size_t)w * E));
                 if ((tid & 31) == 0) mode[w] = md;
             }
         }
         __syncthreads();
-        const int m0 = R::kChecked ? mode[0] : 0;
-        const bool joint = two && (!R::kChecked || (m0 == mode[1] && m0 < 2));
+        bool joint = have == P;
+        int m0 = 0;
+        if constexpr (R::kChecked) {
+            m0 = mode[0];
+#pragma unroll
+            for (int i = 1; i < P; ++i) joint &= mode[i] == m0;
+            joint &= m0 < 2;
+        }
         if (joint) {
-            // interleaved pairs: mat[e] = {A[e], B[e]}; layers likewise
-            if (!R::kChecked || m0 == 0) {
-                using PR = PairRing<typename PairBase<R>::type>;  // doubles (exact for int64 here)
+            // interleaved packs: mat[e] = {M0[e], ..., M(P-1)[e]}; layers likewise
+            auto run = [&](auto ring_tag, auto conv) {
+                using PR = decltype(ring_tag);
                 using PT = typename PR::T;
                 PT* mat = reinterpret_cast<PT*>(smem_raw);
                 PT* buf0 = mat + E;
                 PT* buf1 = buf0 + maxc;
                 for (int e = tid; e < E; e += blockDim.x) {
-                    if constexpr (R::kChecked) {
-                        mat[e] = {(double)reinterpret_cast<const long long*>(g0)[e],
-                                  (double)reinterpret_cast<const long long*>(g1)[e]};
-                    } else {
-                        mat[e] = {reinterpret_cast<const double*>(g0)[e], reinterpret_cast<const double*>(g1)[e]};
-                    }
+                    PT x;
+#pragma unroll
+                    for (int i = 0; i < P; ++i) x.v[i] = conv(g[(size_t)i * E + e]);
+                    mat[e] = x;
                 }
                 __syncthreads();
                 bool ov = false;
-                const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
+                const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32p, ov);
                 if (tid == 0) {
                     const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
-                    out[b0] = (T)t.a;  // exact: integer-valued doubles for the int64 ring
-                    out[b0 + 1] = (T)t.b;
+#pragma unroll
+                    for (int i = 0; i < P; ++i) out[b0 + i] = (T)t.v[i];  // exact for the int64 ring
                 }
+            };
+            if (!R::kChecked || m0 == 0) {
+                run(PackRing<typename PackBase<R>::type, P>{}, [](T v) { return (double)v; });
             } else if constexpr (R::kChecked) {
-                using PR = PairRing<RI64<false>>;
-                using PT = typename PR::T;
-                PT* mat = reinterpret_cast<PT*>(smem_raw);
-                PT* buf0 = mat + E;
-                PT* buf1 = buf0 + maxc;
-                for (int e = tid; e < E; e += blockDim.x)
-                    mat[e] = {reinterpret_cast<const long long*>(g0)[e], reinterpret_cast<const long long*>(g1)[e]};
-                __syncthreads();
-                bool ov = false;
-                const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
-                if (tid == 0) {
-                    const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
-                    out[b0] = (T)t.a;
-                    out[b0 + 1] = (T)t.b;
-                }
+                run(PackRing<RI64<false>, P>{}, [](T v) { return (long long)v; });
             }
         } else {
             // one matrix at a time, contiguous layout (the single-matrix kernel's path)
-            for (int h = 0; h < (two ? 2 : 1); ++h) {
-                const T* g = h == 0 ? g0 : g1;
+            for (int h = 0; h < have; ++h) {
+                const T* gh = g + (size_t)h * E;
                 T* mat = reinterpret_cast<T*>(smem_raw);
                 T* buf0 = mat + ((E + 1) & ~1);
                 T* buf1 = buf0 + ((maxc + 1) & ~1);
-                for (int e = tid; e < E; e += blockDim.x) mat[e] = g[e];
+                for (int e = tid; e < E; e += blockDim.x) mat[e] = gh[e];
                 if (tid == 0) flag = 0;
                 __syncthreads();
                 bool ov = false;
