@@ -736,9 +736,13 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 x = b.x;
                 y = b.y;
             }
-            const uint64_t ix = warp_scan_u64(x), iy = warp_scan_u64(y);
-            const uint64_t cur_base = __shfl_sync(0xffffffffu, ix, 31);
-            const uint64_t src_base = __shfl_sync(0xffffffffu, iy, 31);
+            // both prefix sums in one 64-bit scan: every partial sum is a colex rank
+            // below C(34, 17) < 2^32, so the low half never carries into the high one
+            const uint64_t ixy = warp_scan_u64(x | y << 32);
+            const uint64_t ix = ixy & 0xffffffffull, iy = ixy >> 32;
+            const uint64_t last = __shfl_sync(0xffffffffu, ixy, 31);
+            const uint64_t cur_base = last & 0xffffffffull;
+            const uint64_t src_base = last >> 32;
             // stream tile (F \ {F_idx}, k-1): elements below keep their position,
             // elements above shift down one
             const uint64_t sbase = (ix - x) + (src_base - iy);
