@@ -329,11 +329,11 @@ pl_status launch_pack_n(const void* a, void* out, int64_t count, int32_t* status
     auto kern = pl::sz_batch_smem_pack_kernel<R, N, P>;
     PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;
-    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kSmemThreads, smem));
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::pack_threads<N>(), smem));
     per_sm = std::max(per_sm, 1);
     const int64_t packs = (count + P - 1) / P;
     const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
-    kern<<<(unsigned)blocks, pl::kSmemThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, maxc,
+    kern<<<(unsigned)blocks, pl::pack_threads<N>(), smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, maxc,
                                                           pt.tab, pt.off, pt.t32(8), pt.t32(8 * P), status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;

@@ -522,14 +522,21 @@ struct PackBase<RI64<true>> {
 // CTA per pack of P matrices (8-byte rings, 10 <= n <= 14): the pack DP when every
 // member takes the same exact path, else each matrix on its own (contiguous
 // layout in the same shared memory). ptab32p: byte offsets for 8 * P-byte packs.
+// threads per pack CTA: 256 from n = 12 on (C3 182 -> 177 us), 128 below (n = 10 f64
+// is ~3 % faster with 128)
+template <int N>
+__host__ __device__ constexpr int pack_threads() {
+    return N >= 12 ? 256 : 128;
+}
+
 template <class R, int N, int P>
-__global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_pack_kernel(
+__global__ void __launch_bounds__(pack_threads<N>()) sz_batch_smem_pack_kernel(
     const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count, int maxc,
     const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
     const uint32_t* __restrict__ ptab32p, int32_t* __restrict__ status) {
     using T = typename R::T;
     static_assert(sizeof(T) == 8, "8-byte rings only");
-    static_assert(kSmemThreads / 32 >= P, "one warp per member for the guards");
+    static_assert(pack_threads<N>() / 32 >= P, "one warp per member for the guards");
     constexpr int n = N, E = N * N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int mode[P], flag;
