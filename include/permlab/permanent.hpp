@@ -6,7 +6,9 @@
 // include/permlab_b200.h. Deviations, all documented in DESIGN.md:
 //   * Int is int64_t with a guard (DomainError when an intermediate could
 //     reach 2^63) instead of arbitrary precision (reference ring.hpp:31);
-//   * a Real (double) ring is added; Rational is not offered on the device;
+//   * a Real (double) ring is added next to the reference's tags; the
+//     Rational tag is kept (ring_name / ring_from_name) but has no device
+//     arithmetic: a Rational batch call throws DomainError;
 //   * Limits.subset_order_limit defaults to the device cap 34 (reference 30)
 //     and memo_budget_bytes caps device layer scratch (0 = uncapped);
 //   * StoreZechinRun.attribution is computed by a host-side replay of the
@@ -58,10 +60,13 @@ using Int = std::int64_t;
 using Real = double;
 using Cplx = std::complex<double>;
 
-enum class RingTag { Int, Real, Complex };
+/// The reference's tags keep their values (reference ring.hpp:39); Real is
+/// the added double ring.
+enum class RingTag { Int = 0, Rational = 1, Complex = 2, Real = 3 };
 using RingElement = std::variant<Int, Real, Cplx>;
 
-std::string_view ring_name(RingTag tag);  // "int" | "real" | "complex"
+std::string_view ring_name(RingTag tag);          // "int" | "rational" | "complex" | "real"
+RingTag ring_from_name(std::string_view name);    // reference ring.cpp:34-45, plus "real"
 RingTag ring_of(const RingElement& v);
 
 inline constexpr double kComplexRelTol = 1e-9;  // reference ring.hpp:49-50
@@ -98,12 +103,15 @@ class Matrix {
             for (int j = 0; j < order_; ++j) out[static_cast<std::size_t>(j) * order_ + i] = (*this)(i, j);
         return Matrix(order_, std::move(out));
     }
-    /// Entry (i, j) of the result is entry (row_perm[i], col_perm[j]).
+    /// Entry (i, j) of the result is entry (row_perm[i], col_perm[j]); both
+    /// must be permutations of 0..order-1 (reference matrix.hpp:133-146).
     Matrix permute(const std::vector<int>& row_perm, const std::vector<int>& col_perm) const {
+        check_permutation(row_perm, "row");
+        check_permutation(col_perm, "column");
         std::vector<T> out;
         out.reserve(entries_.size());
         for (int i = 0; i < order_; ++i)
-            for (int j = 0; j < order_; ++j) out.push_back((*this)(row_perm.at(i), col_perm.at(j)));
+            for (int j = 0; j < order_; ++j) out.push_back((*this)(row_perm[i], col_perm[j]));
         return Matrix(order_, std::move(out));
     }
     Matrix scale_row(int row, const T& s) const {
@@ -112,13 +120,14 @@ class Matrix {
         for (int j = 0; j < order_; ++j) out[static_cast<std::size_t>(row) * order_ + j] = (*this)(row, j) * s;
         return Matrix(order_, std::move(out));
     }
-    /// Minor with the listed rows and columns removed (|rows| == |cols| < order).
+    /// Minor with the listed rows and columns removed (|rows| == |cols| < order;
+    /// indices in range and distinct, reference matrix.hpp:93-120).
     Matrix remove_rows_cols(const std::vector<int>& rows, const std::vector<int>& cols) const {
         if (rows.size() != cols.size()) throw DomainError("row and column removal sets must have equal size");
         if (static_cast<int>(rows.size()) >= order_) throw DomainError("cannot remove all rows of a matrix");
         std::vector<char> dr(order_, 0), dc(order_, 0);
-        for (int r : rows) dr.at(r) = 1;
-        for (int c : cols) dc.at(c) = 1;
+        mark(rows, dr, "row");
+        mark(cols, dc, "column");
         const int k = order_ - static_cast<int>(rows.size());
         std::vector<T> out;
         for (int i = 0; i < order_; ++i)
@@ -129,6 +138,23 @@ class Matrix {
     bool operator==(const Matrix&) const = default;
 
   private:
+    // The reference's index checks and messages (matrix.hpp:164-184).
+    void mark(const std::vector<int>& idx, std::vector<char>& flags, const char* what) const {
+        for (int i : idx) {
+            if (i < 0 || i >= order_) throw DomainError(std::string(what) + " index out of range");
+            if (flags[i]) throw DomainError(std::string("duplicate ") + what + " index");
+            flags[i] = 1;
+        }
+    }
+    void check_permutation(const std::vector<int>& p, const char* what) const {
+        if (static_cast<int>(p.size()) != order_) throw DomainError(std::string(what) + " permutation has wrong length");
+        std::vector<char> seen(order_, 0);
+        for (int v : p) {
+            if (v < 0 || v >= order_ || seen[v]) throw DomainError(std::string(what) + " argument is not a permutation");
+            seen[v] = 1;
+        }
+    }
+
     int order_;
     std::vector<T> entries_;
 };
@@ -140,7 +166,10 @@ class SquareMatrix {
     explicit SquareMatrix(Matrix<Int> m) : m_(std::move(m)) {}
     explicit SquareMatrix(Matrix<Real> m) : m_(std::move(m)) {}
     explicit SquareMatrix(Matrix<Cplx> m) : m_(std::move(m)) {}
-    RingTag ring() const { return static_cast<RingTag>(m_.index()); }
+    RingTag ring() const {
+        static constexpr RingTag kTags[] = {RingTag::Int, RingTag::Real, RingTag::Complex};
+        return kTags[m_.index()];
+    }
     int order() const {
         return std::visit([](const auto& m) { return m.order(); }, m_);
     }

@@ -3,7 +3,7 @@
  *
  * The reference ("permlab", arXiv 1802.02779) has no FFI layer; the path sits
  * behind free C++ functions in namespace permlab (reference
- * proj/include/permlab/permanent.hpp:77-100, proj/src/permanent.cpp:414-427).
+ * proj/include/permlab/permanent.hpp:77-100, proj/src/permanent.cpp:310-322).
  * This header is the thin C layer the B200 engine exports underneath the C++
  * host API in include/permlab/ (which keeps those signatures); plain pointers
  * and sizes only, no torch or CUDA types. Every entry point says which
@@ -51,11 +51,11 @@ typedef enum pl_dtype { PL_I64 = 0, PL_F64 = 1, PL_C128 = 2 } pl_dtype;
 
 /* Resource guards (reference proj/include/permlab/limits.hpp:23-33).
  * subset_order_limit: reference default 30 with a hard mask cap of 31
- *   (permanent.cpp:155-157); the device engine uses 64-bit masks and uint32
+ *   (permanent.cpp:51-53); the device engine uses 64-bit masks and uint32
  *   colex ranks, so its hard cap is PL_MAX_ORDER (C(34,17) < 2^32) and its
  *   default is PL_MAX_ORDER.
  * memo_budget_bytes: the reference caps its 2^n-slot memo table
- *   (permanent.cpp:247-251); the device engine caps its layer scratch
+ *   (permanent.cpp:143-149); the device engine caps its layer scratch
  *   (2 * max_k C(n,k) entries) instead. 0 = no cap beyond free device memory. */
 typedef struct pl_limits {
     int32_t subset_order_limit;
@@ -82,7 +82,7 @@ void pl_limits_default(pl_limits* out);
 int32_t pl_device_count(void);
 
 /* Single permanent. Replaces permlab::store_zechin_permanent
- * (reference permanent.hpp:90, permanent.cpp:418-420). `out` receives one
+ * (reference permanent.hpp:90, permanent.cpp:314-316). `out` receives one
  * entry of `dtype`. `stream` is a cudaStream_t (NULL = the calling thread's
  * default stream). Synchronous unless PL_FLAG_ASYNC. */
 pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, uint32_t flags,
@@ -129,7 +129,7 @@ pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, c
                       const int32_t* guard_dev, int32_t* status_dev, void* stream);
 
 /* Top level: out_dev[0] = sum_j a[n-1][j] * layer_{n-1}[n-1-j], j ascending
- * (reference permanent.cpp:288-302). n >= 3. Asynchronous. */
+ * (reference permanent.cpp:184-198). n >= 3. Asynchronous. */
 pl_status pl_sz_top(pl_dtype dtype, int32_t n, const void* a_dev, const void* last_layer_dev, void* out_dev,
                     uint32_t flags, const int32_t* guard_dev, int32_t* status_dev, void* stream);
 

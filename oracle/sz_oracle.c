@@ -7,16 +7,16 @@
  * It restates the reference's memoised last-row development
  * (reference proj/src/permanent.cpp) as a layered dynamic programme:
  *   - layer k holds per(S) for every column subset S, |S| = k, over the
- *     leading k rows (permanent.cpp:242-243, "per(S) over the leading |S|
+ *     leading k rows (permanent.cpp:138-139, "per(S) over the leading |S|
  *     rows and column set S, developed along row |S|");
  *   - order-2 base case a(0,j1)a(1,j2) + a(0,j2)a(1,j1), j1 < j2
- *     (permanent.cpp:262-266);
+ *     (permanent.cpp:158-162);
  *   - expansion per(S) = sum over j in S ascending of a(|S|-1, j) *
  *     per(S \ {j}), the first term initialising the accumulator and each later
- *     term added left to right (permanent.cpp:268-279);
+ *     term added left to right (permanent.cpp:164-175);
  *   - top level sum_j a(n-1, j) * per(full \ {j}) for j = 0..n-1, the terms
- *     summed left to right (permanent.cpp:288-302);
- *   - n = 1 returns a[0]; n = 2 is the base case (permanent.cpp:364-370).
+ *     summed left to right (permanent.cpp:184-198);
+ *   - n = 1 returns a[0]; n = 2 is the base case (permanent.cpp:260-266).
  * The memo table is replaced by colex-ranked layer arrays (each distinct
  * subset is still evaluated exactly once), which is what makes n = 32
  * reachable on the CPU; the arithmetic sequence per subset is unchanged, so
@@ -408,7 +408,7 @@ int orc_sz_layer_step_c128(int n, const double* a, int k, const double* prev, do
     return orc_sz_layer_step_c128_(n, (const cplx*)a, k, (const cplx*)prev, (cplx*)cur, r0, r1);
 }
 
-/* Top-level development from the full layer n-1 (permanent.cpp:288-302). */
+/* Top-level development from the full layer n-1 (permanent.cpp:184-198). */
 int orc_sz_top_f64(int n, const double* a, const double* last, double* out) {
     const double* row = a + (size_t)(n - 1) * n;
     double total = row[0] * last[n - 1];

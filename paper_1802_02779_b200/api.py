@@ -160,7 +160,7 @@ def store_zechin_permanent(a, limits: Optional[Limits] = None, fma: bool = False
 
 
 def store_zechin_attributed(a, limits: Optional[Limits] = None) -> AttributionReport:
-    """Per-term cost split of the reference's DFS order (``permanent.cpp:283-303``),
+    """Per-term cost split of the reference's DFS order (``permanent.cpp:179-199``),
     in closed form: term j first demands the subsets T of full\\{j} that
     contain {0..j-1}, 2 <= |T| <= n-1."""
     m = _as_matrix(a)

@@ -1,7 +1,7 @@
 // C ABI of the B200 Store-zechin engine (include/permlab_b200.h).
 //
 // Host-side orchestration only: argument checks mirroring the reference's
-// guards (reference proj/src/permanent.cpp:336-344, :247-251), device
+// guards (reference proj/src/permanent.cpp:232-240, :143-149), device
 // scratch from the stream-ordered allocator, kernel selection by order, and
 // error mapping. No CPU arithmetic path exists: without a device every
 // compute call fails with PL_ERR_NODEVICE.

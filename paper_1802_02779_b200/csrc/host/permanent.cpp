@@ -1,7 +1,7 @@
 // permlab C++ host API over the B200 C ABI (include/permlab/permanent.hpp).
 //
 // Host work here is argument handling, the Limits / DomainError contract
-// (reference proj/src/limits.cpp:43-76, proj/src/permanent.cpp:336-344) and
+// (reference proj/src/limits.cpp:43-76, proj/src/permanent.cpp:232-240) and
 // closed-form diagnostics; every permanent is computed on the device through
 // pl_sz_permanent / pl_sz_permanent_batch. There is no CPU fallback.
 #include "permlab/permanent.hpp"
@@ -41,6 +41,8 @@ pl_dtype dtype_of(RingTag r) {
             return PL_F64;
         case RingTag::Complex:
             return PL_C128;
+        case RingTag::Rational:
+            throw DomainError("the rational ring has no device arithmetic (use int, real or complex)");
     }
     throw DomainError("unknown ring tag");
 }
@@ -65,7 +67,7 @@ std::uint64_t parse_u64(std::string_view key, std::string_view value) {
 
 std::uint64_t binom(int s, int l) { return pl_binom(s, l); }
 
-// Cost of evaluating one memo entry of size t (reference permanent.cpp:262-279).
+// Cost of evaluating one memo entry of size t (reference permanent.cpp:158-175).
 OpCount entry_cost(int t) { return t == 2 ? OpCount{2, 1} : OpCount{static_cast<std::uint64_t>(t), static_cast<std::uint64_t>(t - 1)}; }
 
 }  // namespace
@@ -109,11 +111,24 @@ std::string_view ring_name(RingTag tag) {
             return "real";
         case RingTag::Complex:
             return "complex";
+        case RingTag::Rational:
+            return "rational";
     }
     throw DomainError("unknown ring tag");
 }
 
-RingTag ring_of(const RingElement& v) { return static_cast<RingTag>(v.index()); }
+RingTag ring_from_name(std::string_view name) {
+    if (name == "int") return RingTag::Int;
+    if (name == "rational") return RingTag::Rational;
+    if (name == "complex") return RingTag::Complex;
+    if (name == "real") return RingTag::Real;
+    throw DomainError("unknown ring name: " + std::string(name));
+}
+
+RingTag ring_of(const RingElement& v) {
+    static constexpr RingTag kTags[] = {RingTag::Int, RingTag::Real, RingTag::Complex};
+    return kTags[v.index()];
+}
 
 bool approx_equal(const Cplx& a, const Cplx& b) {
     const double diff = std::abs(a - b);
@@ -206,7 +221,7 @@ PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limi
     return r;
 }
 
-// Closed form of the reference's per-term attribution (permanent.cpp:283-303):
+// Closed form of the reference's per-term attribution (permanent.cpp:179-199):
 // term j first demands exactly the subsets T of full \ {j} with
 // {0..j-1} subset of T and 2 <= |T| <= n-1 (everything missing one of
 // 0..j-1 was memoised by an earlier term), plus its own product.

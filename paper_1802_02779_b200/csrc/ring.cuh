@@ -1,7 +1,7 @@
 // Ring arithmetic for the Store-zechin kernels.
 //
 // The reference instantiates its engine on Counted<T> over cpp_int or
-// std::complex<double> (reference proj/src/permanent.cpp:356-381,
+// std::complex<double> (reference proj/src/permanent.cpp:253-277,
 // proj/include/permlab/op_count.hpp:119-137). On the device:
 //
 //   RI64<false>  int64 arithmetic, used when the per-matrix guard proves that

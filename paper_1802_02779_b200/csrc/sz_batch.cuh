@@ -13,7 +13,7 @@
 // global memory. sz_batch_pipe_kernel (below, inputs >= 64 MiB): one CTA per SM,
 // a producer warp and a ring of batches.
 //
-// Reference: the per-matrix recurrence is proj/src/permanent.cpp:254-302
+// Reference: the per-matrix recurrence is proj/src/permanent.cpp:150-198
 // (see sz_kernels.cuh for the evaluation order).
 #pragma once
 

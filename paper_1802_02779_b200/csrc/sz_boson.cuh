@@ -14,7 +14,7 @@
 //   * one thread per pattern runs the whole order-n DP in registers (n <= 6,
 //     the reference's full-distribution cap, boson.cpp:254-256) with
 //     compile-time subset masks, in the reference's ascending-j order
-//     (permanent.cpp:254-302), so the permanent is bitwise the reference's;
+//     (permanent.cpp:150-198), so the permanent is bitwise the reference's;
 //   * the probability is (re*re + im*im) / divisor with every operation
 //     individually rounded, the divisor the product of 2..c over each run of
 //     c equal rows in ascending mode order (boson.cpp:233-239).

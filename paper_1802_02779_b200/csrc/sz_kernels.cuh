@@ -1,10 +1,10 @@
 // Store-zechin device kernels (sm_100a).
 //
 // The reference evaluates per(S) for column subsets S by a memoised recursion
-// (reference proj/src/permanent.cpp:244-322):
-//     per(S) = sum_{j in S, ascending} a(|S|-1, j) * per(S \ {j})       (:268-279)
-//     per({j1<j2}) = a(0,j1) a(1,j2) + a(0,j2) a(1,j1)                    (:262-266)
-//     per(A) = sum_{j=0..n-1} a(n-1, j) * per(full \ {j}), left to right  (:288-302)
+// (reference proj/src/permanent.cpp:140-218):
+//     per(S) = sum_{j in S, ascending} a(|S|-1, j) * per(S \ {j})       (:164-175)
+//     per({j1<j2}) = a(0,j1) a(1,j2) + a(0,j2) a(1,j1)                    (:158-162)
+//     per(A) = sum_{j=0..n-1} a(n-1, j) * per(full \ {j}), left to right  (:184-198)
 // The device engine evaluates the same recurrence bottom-up, one layer
 // (subset size k) at a time, every layer stored densely in colex order:
 //     rank(S) = sum_{i=1..k} C(s_i, i),  s_1 < ... < s_k,

@@ -1,6 +1,6 @@
 // Warp-specialised per-layer kernel (the large-order hot path).
 //
-// Recurrence (reference proj/src/permanent.cpp:268-279):
+// Recurrence (reference proj/src/permanent.cpp:164-175):
 //     per(S) = sum_{j in S, ascending} a(k-1, j) * per(S \ {j}),   |S| = k,
 // evaluated one layer at a time, every layer dense in colex order.
 //

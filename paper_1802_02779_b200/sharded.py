@@ -156,11 +156,17 @@ def gather_last_layer(buf: torch.Tensor, n: int, rank: int, world: int, group=No
 def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
                      layer_fn: Callable[[int, torch.Tensor, torch.Tensor, int, int], None],
                      top_fn: Callable[[torch.Tensor, torch.Tensor], object],
-                     group=None, on_layer: Callable[[int], None] | None = None, plan: str = "auto"):
+                     group=None, on_layer: Callable[[int], None] | None = None, plan: str = "auto",
+                 status: torch.Tensor | None = None):
     """Run the layer DP of matrix `a` (n x n, already on this rank's device)
     sharded over `world` ranks. `layer_fn(k, prev, cur, r0, r1)` fills
     cur[r0:r1] of layer k; `top_fn(a, last)` returns the permanent.
-    plan: "blocks" (top-column blocks, world = 2^t), "allgather", or "auto"."""
+    plan: "blocks" (top-column blocks, world = 2^t), "allgather", or "auto".
+    `status` (int32, on the device the collectives use) is the rank's overflow
+    status word written by its layer kernels: before the top level it is
+    combined over the group (MAX), so either every rank sees an int64
+    overflow and raises, or none does (a wrapped value exchanged by one rank
+    never reaches a result silently)."""
     n = a.shape[0]
     if n < 3:
         raise ValueError("sharded DP needs n >= 3")
@@ -186,6 +192,7 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
                 on_layer(k)
             prev, cur = cur, prev
         gather_last_layer(prev, n, rank, world, group)
+        _combine_status(status, world, group)
         return top_fn(a, prev)
     size = max_padded_layer(n, world) + 4  # slack: 16-byte aligned ring copies may read one entry past a layer
     bufs = [torch.zeros(size, dtype=a.dtype, device=a.device) for _ in range(2)]
@@ -199,7 +206,13 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
         if on_layer is not None:
             on_layer(k)
         prev, cur = cur, prev
+    _combine_status(status, world, group)
     return top_fn(a, prev)
+
+
+def _combine_status(status: torch.Tensor | None, world: int, group) -> None:
+    if status is not None and world > 1:
+        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
 
 
 # ---------------------------------------------------------------- device hooks
@@ -230,6 +243,7 @@ def device_hooks(a: torch.Tensor, fma: bool = False, stream=None):
             raise DomainError("int64 overflow: an intermediate sub-permanent does not fit the exact int64 ring")
         return out.item()
 
+    layer_fn.status = status  # the rank's overflow word (combined over ranks by sharded_layer_dp)
     return layer_fn, top_fn
 
 
@@ -239,4 +253,4 @@ def sharded_permanent(a: torch.Tensor, group=None, fma: bool = False):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     layer_fn, top_fn = device_hooks(a, fma=fma)
-    return sharded_layer_dp(a, rank, world, layer_fn, top_fn, group=group)
+    return sharded_layer_dp(a, rank, world, layer_fn, top_fn, group=group, status=layer_fn.status)

@@ -139,6 +139,31 @@ void host_closed_forms() {
         CHECK(algorithm_from_name(algorithm_name(a)) == a);
     }
     CHECK_THROWS_AS(algorithm_from_name("glynn"), DomainError);
+    // rings (reference ring.hpp:39-42, ring.cpp:34-45): the reference's tags, plus real
+    for (RingTag t : {RingTag::Int, RingTag::Rational, RingTag::Complex, RingTag::Real}) {
+        CHECK(ring_from_name(ring_name(t)) == t);
+    }
+    CHECK(ring_name(RingTag::Rational) == "rational");
+    CHECK_THROWS_AS(ring_from_name("quaternion"), DomainError);
+    CHECK(SquareMatrix(Matrix<Real>::identity(2)).ring() == RingTag::Real);
+    CHECK(SquareMatrix(Matrix<Cplx>::identity(2)).ring() == RingTag::Complex);
+    CHECK(ring_of(RingElement(Real{1})) == RingTag::Real);
+    {
+        std::int64_t in = 1, out = 0;  // no device arithmetic for the rational ring (checked before any device call)
+        CHECK_THROWS_AS(store_zechin_permanent_batch(RingTag::Rational, 1, 1, &in, &out), DomainError);
+    }
+    // matrix index validation (reference matrix.hpp:93-184, test_matrix.cpp)
+    {
+        const Matrix<Int> m = Matrix<Int>::identity(3);
+        CHECK_THROWS_AS(m.permute({0, 1}, {0, 1, 2}), DomainError);      // wrong length
+        CHECK_THROWS_AS(m.permute({0, 0, 1}, {0, 1, 2}), DomainError);   // not a permutation
+        CHECK_THROWS_AS(m.permute({0, 1, 2}, {0, 1, 3}), DomainError);   // out of range
+        CHECK(m.permute({2, 0, 1}, {2, 0, 1}) == m);
+        CHECK_THROWS_AS(m.remove_rows_cols({0, 0}, {0, 1}), DomainError);  // duplicate row
+        CHECK_THROWS_AS(m.remove_rows_cols({3}, {0}), DomainError);        // row out of range
+        CHECK_THROWS_AS(m.remove_rows_cols({0}, {-1}), DomainError);       // column out of range
+        CHECK(m.remove_rows_cols({1}, {1}) == Matrix<Int>::identity(2));
+    }
     // limits (reference tests/test_permanent.cpp:280-294): rejected before any device work
     Limits limits;
     limits.subset_order_limit = 4;

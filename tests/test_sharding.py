@@ -185,3 +185,46 @@ def test_gloo_sharded_dp_bitwise(world, cplx):
     a_np = configs.complex_uniform((n, n), seed=31) if cplx else configs.uniform((n, n), seed=31)
     want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
     assert set(results.values()) == {want}
+
+
+def _overflow_worker(rank, world, port, n, bad_rank, plan, q):
+    """Rank `bad_rank`'s layer step flags an int64 overflow in its own status
+    word; every rank must raise (the status is combined over the group
+    before the top level), none may return a value."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = torch.from_numpy(configs.uniform((n, n), seed=5))
+        layer_fn, _ = cpu_hooks(a)
+        status = torch.zeros(1, dtype=torch.int32)
+
+        def flagged_layer(k, prev, cur, r0, r1):
+            layer_fn(k, prev, cur, r0, r1)
+            if rank == bad_rank and k == n // 2:
+                status[0] |= 1  # what the device layer kernel does on an actual overflow
+
+        def top_fn(a_, last):
+            if int(status[0]) & 1:
+                return "overflow"
+            return "value"
+
+        q.put((rank, sharded_layer_dp(a, rank, world, flagged_layer, top_fn, plan=plan, status=status)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,plan", [(2, "blocks"), (3, "allgather"), (4, "blocks")])
+def test_gloo_overflow_status_combined_over_ranks(world, plan):
+    n = 10
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overflow_worker, args=(r, world, port, n, world - 1, plan, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert set(results.values()) == {"overflow"}
