@@ -151,12 +151,56 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workloads
 
-def workload(name: str):
-    from paper_1802_02779_b200 import configs
+def _configs_module():
+    """paper_1802_02779_b200/configs.py loaded by path: the seeded generators
+    only (libpermlab_gen.so), never the engine's libpermlab_b200.so -- the
+    reference arm must not map the product library."""
+    import importlib.util
 
+    spec = importlib.util.spec_from_file_location("permlab_bench_configs", ROOT / "paper_1802_02779_b200" / "configs.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def workload(name: str):
+    configs = _configs_module()
     spec = configs.CONFIGS[name]
     a = configs.generate(name)
     return spec, a
+
+
+def config_spec(name: str):
+    return _configs_module().CONFIGS[name]
+
+
+def config_dict(name: str, world: int, fma: bool) -> dict:
+    """The `config` object of both arms' JSON lines (identical for the same
+    workload, so the driver can pair them)."""
+    spec = config_spec(name)
+    batched = spec["n"] <= 16
+    if batched:
+        l2 = "inputs from HBM every step: rotating device copies of the batch (>= 320 MiB > L2), K steps in one CUDA graph"
+        par = f"dp{world} (batch by matrix, no collective)"
+    else:
+        l2 = "L2 flushed between timed steps (256 MiB write, then 256 MiB read), one event pair per step"
+        par = "1 GPU" if world == 1 else f"layer DP sharded over {world} GPUs"
+    return {"workload": f"{name}: {spec['desc']}", "n": spec["n"], "count": spec["count"],
+            "per_rank_count": spec["count"], "l2": l2,
+            "arith": "fma" if fma else "reference rounding order (no FMA)", "parallelism": par}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def cpu_reference_time(name: str, a: np.ndarray, budget_s: float, threads: int):
@@ -177,16 +221,80 @@ def cpu_reference_time(name: str, a: np.ndarray, budget_s: float, threads: int):
         O.ref_sz_batch(a[:1], nthreads=1, memo_budget_bytes=8 << 30)
         dt = time.perf_counter() - t
         return 1.0 / dt, f"1 matrix n={n}, reference engine (single-threaded by design)", "reference", 1
+    # contiguous chunks of the batch (one contiguous slice per thread inside
+    # ref_sz_batch), growing until one takes >= 0.25 s, repeated to budget_s
     done, t0 = 0, time.perf_counter()
-    chunk = a
+    size, pos = min(a.shape[0], 256 * threads), 0
     while True:
-        O.ref_sz_batch(chunk, nthreads=threads)
-        done += chunk.shape[0]
-        el = time.perf_counter() - t0
-        if el >= budget_s:
+        if pos + size > a.shape[0]:
+            pos = 0
+        t1 = time.perf_counter()
+        O.ref_sz_batch(a[pos:pos + size], nthreads=threads)
+        pos += size
+        done += size
+        now = time.perf_counter()
+        if now - t0 >= budget_s:
             break
+        if now - t1 < 0.25:
+            size = min(a.shape[0], size * 2)
+    el = time.perf_counter() - t0
     return done / el, f"{done} matrices n={n} ({el:.1f} s wall, {threads} threads, contiguous chunks)", \
         "reference", threads
+
+
+CPU_LARGE = ROOT / "profiles" / "cpu_large.json"
+
+
+def measure_cpu_large() -> dict:
+    """The single large matrices on the host: C4 through the reference engine
+    itself (oracle/_ref, single-threaded as it is written, ~1 min) and C5
+    through the oracle port (the reference cannot run n = 32; all threads,
+    ~19 GB of host memory). Written to profiles/cpu_large.json by
+    `bench.py --cpu-large-only` on the GPU box's host, read by the suite."""
+    out = {"cpu_model": cpu_model(), "nproc": os.cpu_count(), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    for name in ("c4", "c5"):
+        _, a = workload(name)
+        threads = 1 if name == "c4" else (os.cpu_count() or 1)
+        try:
+            import psutil
+
+            if name == "c5" and psutil.virtual_memory().available < (40 << 30):
+                out[name] = {"error": "less than 40 GB of host memory available for the n = 32 port"}
+                continue
+        except ImportError:
+            pass
+        v, sample, kind, cores = cpu_reference_time(name, a, 0.0, threads)
+        out[name] = {"value": v, "unit": "permanents/s", "seconds_per_permanent": 1.0 / v, "cores": cores,
+                     "kind": kind, "sample": sample}
+    return out
+
+
+def suite_cpu_baseline(name: str, a: np.ndarray, budget_s: float, live_large: bool):
+    """cpu_baseline of one suite entry: batched configs at all host threads
+    (the value) and at one thread; the single large matrices from
+    profiles/cpu_large.json (measured on a GPU box's host, provenance inside)
+    unless --cpu-large re-measures them here."""
+    threads = os.cpu_count() or 1
+    spec = config_spec(name)
+    if spec["n"] >= 20:
+        if live_large:
+            d = measure_cpu_large()
+            src = "measured in this run"
+        elif CPU_LARGE.exists():
+            d = json.loads(CPU_LARGE.read_text())
+            src = f"profiles/cpu_large.json ({d.get('when', '?')}, bench.py --cpu-large-only on a GPU box host)"
+        else:
+            return None
+        e = dict(d.get(name) or {})
+        if not e or "error" in e:
+            return e or None
+        e.update({"cpu_model": d.get("cpu_model"), "nproc": d.get("nproc"), "source": src})
+        return e
+    v, sample, kind, cores = cpu_reference_time(name, a, budget_s, threads)
+    v1, sample1, _, _ = cpu_reference_time(name, a, budget_s, 1)
+    return {"value": v, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample,
+            "single_thread": {"value": v1, "cores": 1, "sample": sample1}, "cpu_model": cpu_model(),
+            "nproc": os.cpu_count()}
 
 
 def run_reference_arm(args):
@@ -210,9 +318,10 @@ def run_reference_arm(args):
         "metric": f"permanents/s ({name.upper()}: {spec['desc']})",
         "value": value, "unit": "permanents/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * count / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": DT_SHORT[spec["dtype"]], "data": "synthetic (seeded generator, BASELINE.json recipe)",
-        "config": {"workload": f"{name}: {spec['desc']}", "n": n, "count": count},
-        "cpu_baseline": {"value": value, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample},
+        "dtype": DT_SHORT[spec["dtype"]], "data": "synthetic (seeded generators following BASELINE.json recipes; no public dataset)",
+        "config": config_dict(name, args.gpus, args.fma),
+        "cpu_baseline": {"value": value, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "permanents/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -349,7 +458,7 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
                 "d2h_bytes_per_step": count * s},
         "algorithmic_bytes_per_step": bytes_per_launch, "per_step_s": per_launch_s,
         "launches_per_step": launches_per_step, "flops_per_step": flops_per_perm(n, spec["dtype"]) * count,
-        "sharded": sharded, "timing": timing,
+        "sharded": sharded, "timing": timing, "fma": fma,
     }
 
 
@@ -467,14 +576,85 @@ def boson_cpu_reference(budget_s: float):
             "sample": f"{done} patterns ({done // p.shape[0]} x full_distribution, {el:.1f} s, 1 thread)"}
 
 
+DFMA_PEAK = (33.40, "measured DFMA rate x 2 flop (profiles/microbench_b200.json: 16.7 T DFMA/s)")
+
+
+def kernel_name(n: int) -> str:
+    if n <= 5:
+        return "sz_batch_tma_kernel"
+    if n <= 14:
+        return "sz_batch_smem_pack_kernel (8-byte) / sz_batch_smem_kernel (complex)"
+    return "sz_ws_kernel (all layers of one step)"
+
+
 def roofline_of(res, peak, peak_src, traffic):
-    achieved = res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9
+    """The dominant kernel's roofline on its binding resource: HBM for the
+    streaming batches (n <= 5) and the layer DP (compulsory layer traffic);
+    the FP64 pipe for the shared-memory batch kernels (n = 6..14), whose
+    input is a few KB per matrix against ~10^4-10^5 DFMA (C3: 45,045 exact
+    integer ops per permanent executed as DFMA on exact doubles)."""
+    n = res["spec"]["n"]
     tr = traffic.get(res["name"])
-    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": tr, "peak_source": peak_src,
-            "kernel": "sz_batch_tma_kernel" if res["spec"]["n"] <= 5 else (
-                "sz_batch_smem_kernel" if res["spec"]["n"] <= 14 else "sz_ws_kernel (all layers of one step)"),
-            "fp_rate_tflops": res["flops_per_step"] / res["per_step_s"] / 1e12}
+    fp = res["flops_per_step"] / res["per_step_s"] / 1e12
+    if 6 <= n <= 14:
+        return {"bound": "fp64", "achieved": fp, "peak": DFMA_PEAK[0], "unit": "TFLOP/s", "frac": fp / DFMA_PEAK[0],
+                "peak_source": DFMA_PEAK[1], "traffic": tr, "kernel": kernel_name(n),
+                "hbm_gbs": res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9,
+                "note": "bytes are ~1 KB per 45 k ops: neither HBM nor L2 binds; the FP64 pipe is the ceiling "
+                        "(shared-memory operand loads are the measured limiter, DESIGN.md section 4)"}
+    achieved = res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": tr, "peak_source": peak_src, "kernel": kernel_name(n), "fp_rate_tflops": fp}
+    if n >= 20:
+        fpk = FP64_PEAK if not res.get("fma") else DFMA_PEAK
+        out["fp64_frac"] = fp / fpk[0]
+        out["fp64_peak_source"] = fpk[1]
+    return out
+
+
+def cold_call(name: str, fma: bool) -> dict:
+    """First call of the public API in a fresh process (library load, module
+    load, tables and schedules, scratch allocation, H2D, compute, D2H), after
+    the CUDA context exists: what a one-matrix-per-process caller (the
+    reference CLI `perm`) pays. Run as `bench.py --cold-call NAME`."""
+    import torch
+
+    torch.cuda.init()
+    torch.zeros(1, device="cuda")
+    torch.cuda.synchronize()
+    _, a = workload(name)
+    t0 = time.perf_counter()
+    import paper_1802_02779_b200 as pl
+
+    t1 = time.perf_counter()
+    v = pl.store_zechin_permanent_batch(a, fma=fma)
+    t2 = time.perf_counter()
+    pl.store_zechin_permanent_batch(a, fma=fma)
+    t3 = time.perf_counter()
+    return {"config": name, "first_call_ms": 1e3 * (t2 - t0), "import_ms": 1e3 * (t1 - t0),
+            "second_call_ms": 1e3 * (t3 - t2), "value_ok": bool(np.all(np.isfinite(np.asarray(v).view(np.float64))))}
+
+
+def measure_cold(name: str, fma: bool):
+    import subprocess
+
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--cold-call", name] + (["--fma"] if fma else [])
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": repr(e)[:200]}
+
+
+def suite_entry(r, name, steps, peak, peak_src, traffic, world):
+    from paper_1802_02779_b200.sharded import block_plan_applies
+
+    return {"value": r["value"], "unit": "permanents/s", "ms_per_step": r["ms_per_step"], "steps": steps,
+            "time_to_permanent_ms": r["ms_per_step"] if r["spec"]["count"] == 1 else None,
+            "arith": "fma" if r["fma"] else "reference rounding order (no FMA)",
+            "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"], "timing": r["timing"],
+            "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
+                         else "equal slices, all-gather") if r["sharded"] else None)}
 
 
 def main():
@@ -486,12 +666,21 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-large", action="store_true", help="re-measure the C4/C5 CPU baselines in this run (~2 min)")
+    ap.add_argument("--cpu-large-only", action="store_true", help="print the C4/C5 CPU baselines as JSON and exit")
+    ap.add_argument("--cold-call", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--fma", action="store_true", help="allow FMA contraction (not the reference rounding order)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.cpu_large_only:
+        print(json.dumps(measure_cpu_large(), indent=1), flush=True)
+        return 0
+    if args.cold_call:
+        print(json.dumps(cold_call(args.cold_call, args.fma)), flush=True)
+        return 0
 
     import torch
     import torch.distributed as dist
@@ -507,46 +696,59 @@ def main():
         # a finite timeout: a stuck collective in the sharded suite entries errors out
         # (and is reported in the suite) instead of hanging the job
         dist.init_process_group("nccl", device_id=device, timeout=datetime.timedelta(seconds=300))
-    from paper_1802_02779_b200.sharded import block_plan_applies
 
     flush_buf = torch.zeros(2, 64 * 1024 * 1024, dtype=torch.float32, device=device)  # 2 x 256 MiB > 126 MB L2
     peak, peak_src = load_peaks()
     traffic = load_traffic()
+    cpu_on = rank == 0 and world == 1 and not args.no_cpu
 
     with ClockSampler(local) as clocks:
         head = measure_config(args.config, args.steps, args.warmup, rank, world, device, flush_buf, args.fma)
         suite = {}
         if not args.no_suite:
-            for name in ("c1", "c2", "c3", "c4", "c5"):
+            plan = [("c1", False), ("c2", False), ("c3", False), ("c4", False), ("c4_fma", True), ("c5", False),
+                    ("c5_fma", True)]
+            for key, fma in plan:
+                name = key.split("_")[0]
                 k = {"c1": 10, "c2": 10, "c3": 10, "c4": 5, "c5": 2}[name]
                 try:
-                    r = head if name == args.config else measure_config(name, k, 3, rank, world, device, flush_buf,
-                                                                        args.fma)
+                    same = name == args.config and fma == args.fma
+                    r = head if same else measure_config(name, k, 3, rank, world, device, flush_buf, fma)
                 except Exception as e:  # e.g. the sharded large-order path on a multi-GPU run
-                    print(f"bench: suite entry {name} failed: {e!r}", file=sys.stderr, flush=True)
-                    suite[name] = {"error": repr(e)[:300]}
+                    print(f"bench: suite entry {key} failed: {e!r}", file=sys.stderr, flush=True)
+                    suite[key] = {"error": repr(e)[:300]}
                     continue
-                suite[name] = {"value": r["value"], "unit": "permanents/s", "ms_per_step": r["ms_per_step"],
-                               "steps": args.steps if name == args.config else k,
-                               "time_to_permanent_ms": r["ms_per_step"] if r["spec"]["count"] == 1 else None,
-                               "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"],
-                               "timing": r["timing"],
-                               "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
-                                            else "equal slices, all-gather") if r["sharded"] else None)}
+                suite[key] = suite_entry(r, name, args.steps if same else k, peak, peak_src, traffic, world)
             for key, steps_b, spec_b in (("boson", 10, BOSON), ("boson_large", 3, BOSON_LARGE)):
                 try:
                     suite[key] = measure_boson(steps_b, 3, rank, world, device, flush_buf, args.fma, spec_b)
                 except Exception as e:
                     print(f"bench: suite entry {key} failed: {e!r}", file=sys.stderr, flush=True)
                     suite[key] = {"error": repr(e)[:300]}
-            if rank == 0 and world == 1 and not args.no_cpu and "error" not in suite["boson"]:
-                suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
+
+    if not args.no_suite and rank == 0 and world == 1:
+        # cold first calls (fresh processes), outside the clock-sampled region
+        for key in ("c4", "c5"):
+            if key in suite and "error" not in suite[key]:
+                suite[key]["cold_call"] = measure_cold(key, False)
+    if cpu_on and not args.no_suite:
+        for key in ("c1", "c2", "c3", "c4", "c5"):
+            if key in suite and "error" not in suite[key]:
+                _, a = workload(key)
+                try:
+                    suite[key]["cpu_baseline"] = suite_cpu_baseline(key, a, 3.0, args.cpu_large)
+                except Exception as e:  # noqa: BLE001
+                    suite[key]["cpu_baseline"] = {"error": repr(e)[:200]}
+        if "error" not in suite.get("boson", {"error": 1}):
+            suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        _, a = workload(args.config)
-        v, sample, kind, cores = cpu_reference_time(args.config, a, 10.0, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": "permanents/s", "cores": cores, "kind": kind, "sample": sample}
+    if cpu_on:
+        if not args.no_suite and args.config in suite and suite[args.config].get("cpu_baseline"):
+            cpu = dict(suite[args.config]["cpu_baseline"])
+        else:
+            _, a = workload(args.config)
+            cpu = suite_cpu_baseline(args.config, a, 10.0, args.cpu_large)
 
     if rank == 0:
         spec = head["spec"]
@@ -557,10 +759,7 @@ def main():
             "scaling": "weak" if not head["sharded"] else "strong", "vs_baseline": None,
             "dtype": DT_SHORT[spec["dtype"]],
             "data": "synthetic (seeded generators following BASELINE.json recipes; no public dataset)",
-            "config": {"workload": f"{args.config}: {spec['desc']}", "n": spec["n"], "count": spec["count"],
-                       "per_rank_count": spec["count"], "l2": head["timing"],
-                       "arith": "fma" if args.fma else "reference rounding order (no FMA)",
-                       "parallelism": f"dp{world} (batch by matrix, no collective)"},
+            "config": config_dict(args.config, world, args.fma),
             "roofline": roofline_of(head, peak, peak_src, traffic),
             "cpu_baseline": cpu,
             "e2e": head["e2e"],

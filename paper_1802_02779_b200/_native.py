@@ -115,34 +115,8 @@ def last_error() -> str:
     return lib.pl_last_error().decode()
 
 
-_gen = None
-
-
 def gen():
-    """Seeded config generators (``csrc/gen/configs.c``)."""
-    global _gen
-    if _gen is None:
-        if not GEN_PATH.exists():
-            raise ImportError(f"{GEN_PATH} is missing: run `make` at the repo root")
-        G = C.CDLL(str(GEN_PATH))
-        vp, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
-        G.pl_gen_haar.argtypes = [i32, u64, i32, vp]
-        G.pl_gen_haar.restype = C.c_int
-        G.pl_gen_c1.argtypes = [i64, u64, vp]
-        G.pl_gen_c1.restype = None
-        G.pl_gen_c2.argtypes = [i64, u64, vp]
-        G.pl_gen_c2.restype = C.c_int
-        G.pl_gen_c3.argtypes = [i64, u64, vp]
-        G.pl_gen_c3.restype = None
-        G.pl_gen_c4.argtypes = [i32, u64, vp]
-        G.pl_gen_c4.restype = None
-        G.pl_gen_c5.argtypes = [i32, i32, u64, vp]
-        G.pl_gen_c5.restype = C.c_int
-        G.pl_gen_int_matrices.argtypes = [i32, i64, u64, i64, i64, vp]
-        G.pl_gen_int_matrices.restype = None
-        G.pl_gen_uniform.argtypes = [i64, u64, C.c_double, C.c_double, vp]
-        G.pl_gen_uniform.restype = None
-        G.pl_gen_mt64_stream.argtypes = [u64, i64, vp]
-        G.pl_gen_mt64_stream.restype = None
-        _gen = G
-    return _gen
+    """Seeded config generators (``csrc/gen/configs.c``), loaded by configs.py."""
+    from .configs import N as _G
+
+    return _G.gen()

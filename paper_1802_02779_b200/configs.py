@@ -7,11 +7,43 @@ uniforms, Box-Muller, Gram-Schmidt Haar unitaries; reference
 """
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
+from pathlib import Path
 
 import numpy as np
 
-from . import _native as N
+# Self-contained on purpose (no package-relative imports): bench.py's reference
+# arm loads this file by path, so generating the workload never maps the
+# engine's libpermlab_b200.so into the reference arm's process.
+GEN_PATH = Path(__file__).resolve().parent / "libpermlab_gen.so"
+
+
+class _Gen:
+    _lib = None
+
+    def gen(self):
+        """Seeded config generators (``csrc/gen/configs.c``)."""
+        if self._lib is None:
+            if not GEN_PATH.exists():
+                raise ImportError(f"{GEN_PATH} is missing: run `make` at the repo root")
+            G = C.CDLL(str(GEN_PATH))
+            vp, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
+            for name, args, res in (("pl_gen_haar", [i32, u64, i32, vp], C.c_int),
+                                    ("pl_gen_c1", [i64, u64, vp], None), ("pl_gen_c2", [i64, u64, vp], C.c_int),
+                                    ("pl_gen_c3", [i64, u64, vp], None), ("pl_gen_c4", [i32, u64, vp], None),
+                                    ("pl_gen_c5", [i32, i32, u64, vp], C.c_int),
+                                    ("pl_gen_int_matrices", [i32, i64, u64, i64, i64, vp], None),
+                                    ("pl_gen_uniform", [i64, u64, C.c_double, C.c_double, vp], None),
+                                    ("pl_gen_mt64_stream", [u64, i64, vp], None)):
+                f = getattr(G, name)
+                f.argtypes = args
+                f.restype = res
+            self._lib = G
+        return self._lib
+
+
+N = _Gen()
 
 CONFIGS = {
     "c1": dict(n=5, count=100_000, dtype="int64", seed=1,
