@@ -28,8 +28,12 @@ $(BUILD)/boson.o: $(CSRC)/boson.cu $(CSRC)/sz_boson.cuh $(CSRC)/capi_internal.h 
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/boson.cu
 
-$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/boson.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+$(BUILD)/multi.o: $(CSRC)/multi.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh include/permlab_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/multi.cu
+
+$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/boson.o $(BUILD)/multi.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c
 	gcc -O2 -fPIC -ffp-contract=off -std=gnu11 -Wall -shared -o $@ $< -lm

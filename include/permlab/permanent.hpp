@@ -40,6 +40,10 @@ struct Limits {
     int subset_order_limit = 34;
     std::uint64_t enumeration_cap = 100000;
     std::uint64_t memo_budget_bytes = 0;
+    /// Devices to run on (addition; pl_limits.num_gpus): 0 = the current
+    /// device; g >= 1 = devices 0..g-1, the large-order layer DP sharded over
+    /// them with NCCL, batches split by matrix. PERMLAB_LIMITS key num_gpus.
+    int num_gpus = 0;
     static Limits from_env();
 };
 

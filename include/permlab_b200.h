@@ -44,7 +44,8 @@ typedef enum pl_status {
     PL_ERR_OVERFLOW = 3, /* an int64 intermediate would overflow (exact ring guard) */
     PL_ERR_NOMEM = 4,    /* device allocation failed                                 */
     PL_ERR_CUDA = 5,     /* CUDA runtime error                                       */
-    PL_ERR_NODEVICE = 6  /* no CUDA device: the engine has no CPU fallback          */
+    PL_ERR_NODEVICE = 6, /* no CUDA device: the engine has no CPU fallback          */
+    PL_ERR_NCCL = 7      /* NCCL unavailable or a collective failed (multi-GPU)     */
 } pl_status;
 
 typedef enum pl_dtype { PL_I64 = 0, PL_F64 = 1, PL_C128 = 2 } pl_dtype;
@@ -60,6 +61,14 @@ typedef enum pl_dtype { PL_I64 = 0, PL_F64 = 1, PL_C128 = 2 } pl_dtype;
 typedef struct pl_limits {
     int32_t subset_order_limit;
     uint64_t memo_budget_bytes;
+    /* Devices to run on (an addition: the reference is single-threaded).
+     * 0 (default): the calling thread's current device, no collectives.
+     * g >= 1: devices 0..g-1 of this process through the multi-GPU path --
+     * a large-order matrix (n >= 15) runs its layer DP sharded over the g
+     * devices with NCCL exchanges after every layer (single-process
+     * communicators, pl_sz_permanent_multi); a batch of smaller orders is
+     * split by matrix across them, with no collective. */
+    int32_t num_gpus;
 } pl_limits;
 
 #define PL_MAX_ORDER 34
@@ -141,6 +150,42 @@ pl_status pl_sz_guard_i64(int32_t n, const int64_t* a_dev, int32_t* guard_dev, v
 /* Device scratch bytes a single-matrix run of order n needs (two layer
  * buffers of max_k C(n,k) entries). */
 uint64_t pl_sz_scratch_bytes(pl_dtype dtype, int32_t n);
+
+/* Large-order calls (n >= 15) keep their layer scratch (cudaMalloc blocks,
+ * up to 2 x 9.6 GB at n = 32 complex) in a per-device cache for the next
+ * call, as a caching allocator does; this frees every idle block (blocks of
+ * calls still running on a stream are returned to the cache when their
+ * stream finishes them) and the cached per-order tile lists of the layer
+ * kernel (after synchronising the devices that hold them).
+ * PL_SCRATCH_CACHE=0 frees the scratch after every synchronous call. */
+void pl_release_scratch(void);
+
+/* ---- multi-GPU inside one process ----------------------------------------
+ * pl_limits.num_gpus = g >= 1 routes pl_sz_permanent / pl_sz_permanent_batch
+ * here (synchronous; host or device pointers, UVA copies): a large order
+ * (n >= 15) runs each matrix's layer DP sharded over devices 0..g-1 with
+ * single-process NCCL communicators (ncclCommInitAll, cached per device set;
+ * NCCL is loaded with dlopen) -- top-column blocks with ncclSend/ncclRecv
+ * when g = 2^t (n - t >= 3), else equal slices with an in-place
+ * ncclAllGather after every layer; smaller orders split the batch by matrix.
+ * Results are bitwise those of the single-device path (same kernel on rank
+ * ranges). The reference is single-threaded (permanent.cpp:310-316); this
+ * is the engine's addition, the single-process counterpart of sharded.py. */
+pl_status pl_sz_permanent_multi(pl_dtype dtype, int32_t n, int64_t count, const void* a, void* out, uint32_t flags,
+                                const pl_limits* limits, int32_t num_gpus, const int32_t* devices);
+
+/* The shard plans (shared with the torch.distributed driver, sharded.py). */
+#define PL_SHARD_ALLGATHER 0 /* equal padded slices + in-place all-gather      */
+#define PL_SHARD_BLOCKS 1    /* top-column blocks + point-to-point exchange    */
+/* Plan of order n over `world` devices (-1 on bad arguments). */
+int32_t pl_shard_plan(int32_t n, int32_t world);
+/* Colex-rank range [r0, r1) of layer k computed by `rank`. */
+pl_status pl_shard_range(int32_t n, int32_t world, int32_t rank, int32_t k, uint64_t* r0, uint64_t* r1);
+/* Point-to-point operations of `rank` after layer k under the block plan
+ * (0 under the all-gather plan; layer n-1 goes to rank 0): returns their
+ * count and, if ops != NULL, writes up to max_ops quadruples
+ * (recv ? 1 : 0, peer, r0, r1). -1 on bad arguments. */
+int32_t pl_shard_exchange(int32_t n, int32_t world, int32_t rank, int32_t k, uint64_t* ops, int32_t max_ops);
 
 /* ---- boson sampling (reference proj/include/permlab/boson.hpp:67-99) ------
  * An m-mode interferometer is its unitary U: m*m complex128 entries,

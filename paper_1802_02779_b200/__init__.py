@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     colex_rank,
     colex_unrank,
     device_count,
+    release_scratch,
     scratch_bytes,
     store_zechin_attributed,
     store_zechin_counts,

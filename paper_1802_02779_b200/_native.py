@@ -15,7 +15,8 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("PL_NATIVE_LIB", PKG_DIR / "libpermlab_b200.so"))  # override: tuning variants
 GEN_PATH = PKG_DIR / "libpermlab_gen.so"
 
-PL_OK, PL_ERR_ARG, PL_ERR_LIMIT, PL_ERR_OVERFLOW, PL_ERR_NOMEM, PL_ERR_CUDA, PL_ERR_NODEVICE = range(7)
+PL_OK, PL_ERR_ARG, PL_ERR_LIMIT, PL_ERR_OVERFLOW, PL_ERR_NOMEM, PL_ERR_CUDA, PL_ERR_NODEVICE, PL_ERR_NCCL = range(8)
+PL_SHARD_ALLGATHER, PL_SHARD_BLOCKS = 0, 1
 PL_I64, PL_F64, PL_C128 = 0, 1, 2
 PL_FLAG_DEVICE_PTRS = 0x1
 PL_FLAG_FMA = 0x2
@@ -32,6 +33,7 @@ STATUS_NAMES = {
     PL_ERR_NOMEM: "PL_ERR_NOMEM",
     PL_ERR_CUDA: "PL_ERR_CUDA",
     PL_ERR_NODEVICE: "PL_ERR_NODEVICE",
+    PL_ERR_NCCL: "PL_ERR_NCCL",
 }
 
 # Every symbol include/permlab_b200.h declares (checked by the CPU test suite).
@@ -51,6 +53,11 @@ EXPORTED_SYMBOLS = (
     "pl_sz_top",
     "pl_sz_guard_i64",
     "pl_sz_scratch_bytes",
+    "pl_release_scratch",
+    "pl_sz_permanent_multi",
+    "pl_shard_plan",
+    "pl_shard_range",
+    "pl_shard_exchange",
     "pl_boson_pattern_count",
     "pl_boson_unrank_pattern",
     "pl_boson_probabilities",
@@ -59,7 +66,7 @@ EXPORTED_SYMBOLS = (
 
 
 class pl_limits(C.Structure):
-    _fields_ = [("subset_order_limit", C.c_int32), ("memo_budget_bytes", C.c_uint64)]
+    _fields_ = [("subset_order_limit", C.c_int32), ("memo_budget_bytes", C.c_uint64), ("num_gpus", C.c_int32)]
 
 
 def _load():
@@ -97,6 +104,16 @@ def _load():
     L.pl_sz_guard_i64.restype = C.c_int
     L.pl_sz_scratch_bytes.argtypes = [C.c_int, i32]
     L.pl_sz_scratch_bytes.restype = u64
+    L.pl_release_scratch.argtypes = []
+    L.pl_release_scratch.restype = None
+    L.pl_sz_permanent_multi.argtypes = [C.c_int, i32, i64, vp, vp, u32, C.POINTER(pl_limits), i32, vp]
+    L.pl_sz_permanent_multi.restype = C.c_int
+    L.pl_shard_plan.argtypes = [i32, i32]
+    L.pl_shard_plan.restype = i32
+    L.pl_shard_range.argtypes = [i32, i32, i32, i32, C.POINTER(u64), C.POINTER(u64)]
+    L.pl_shard_range.restype = C.c_int
+    L.pl_shard_exchange.argtypes = [i32, i32, i32, i32, C.POINTER(u64), i32]
+    L.pl_shard_exchange.restype = i32
     L.pl_boson_pattern_count.argtypes = [i32, i32]
     L.pl_boson_pattern_count.restype = u64
     L.pl_boson_unrank_pattern.argtypes = [i32, i32, u64, vp]

@@ -43,6 +43,7 @@ class Limits:
     subset_order_limit: int = N.PL_MAX_ORDER
     enumeration_cap: int = 100000
     memo_budget_bytes: int = 0
+    num_gpus: int = 0  # 0: current device; g >= 1: devices 0..g-1 (sharded layer DP / split batch)
 
     @staticmethod
     def from_env() -> "Limits":
@@ -61,13 +62,14 @@ class Limits:
                 raise DomainError(f"PERMLAB_LIMITS: empty value for {key}")
             if not value.isdigit():
                 raise DomainError(f"PERMLAB_LIMITS: non-numeric value for {key}")
-            if key not in ("naive_order_limit", "subset_order_limit", "enumeration_cap", "memo_budget_bytes"):
+            if key not in ("naive_order_limit", "subset_order_limit", "enumeration_cap", "memo_budget_bytes",
+                           "num_gpus"):
                 raise DomainError(f"PERMLAB_LIMITS: unknown key '{key}'")
             setattr(lim, key, int(value))
         return lim
 
     def to_c(self) -> N.pl_limits:
-        return N.pl_limits(int(self.subset_order_limit), int(self.memo_budget_bytes))
+        return N.pl_limits(int(self.subset_order_limit), int(self.memo_budget_bytes), int(self.num_gpus))
 
 
 @dataclass(frozen=True)
@@ -277,6 +279,12 @@ def colex_unrank(k: int, rank: int) -> int:
 
 def scratch_bytes(dtype, n: int) -> int:
     return int(N.lib.pl_sz_scratch_bytes(_DTYPES[np.dtype(dtype)], n))
+
+
+def release_scratch() -> None:
+    """Free the idle layer scratch the large-order path keeps cached between
+    calls (``pl_release_scratch``)."""
+    N.lib.pl_release_scratch()
 
 
 def version() -> str:

@@ -64,6 +64,85 @@ uint64_t max_layer(int n) {
     return m;
 }
 
+// ---------------------------------------------------------------- layer scratch
+// Large-order scratch (two layers: up to 2 x 9.6 GB at n = 32 complex) comes
+// from plain cudaMalloc blocks kept in a per-device cache: a first 19 GB
+// cudaMallocAsync costs ~115 ms (and returning it to the OS as much again,
+// profiles/r2/alloc_probe.cu), cudaMalloc ~2 ms. A call takes a free block of
+// sufficient size (or allocates one), and hands it back when its stream
+// reaches the end of the call (host callback), so concurrent calls never
+// share scratch. pl_release_scratch() frees the idle blocks; with
+// PL_SCRATCH_CACHE=0 every synchronous call does so before returning.
+using plc::ScratchBlock;
+
+struct ScratchCache {
+    std::mutex mu;
+    std::vector<ScratchBlock> idle;
+};
+
+ScratchCache& scratch_cache() {
+    static ScratchCache* c = new ScratchCache;  // never destroyed: host callbacks may run at exit
+    return *c;
+}
+
+bool scratch_caching() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_SCRATCH_CACHE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+pl_status scratch_acquire(size_t bytes, ScratchBlock* out) {
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    {
+        ScratchCache& c = scratch_cache();
+        std::lock_guard<std::mutex> lock(c.mu);
+        int best = -1;
+        for (int i = 0; i < (int)c.idle.size(); ++i) {
+            const ScratchBlock& b = c.idle[i];
+            if (b.dev == dev && b.bytes >= bytes && (best < 0 || b.bytes < c.idle[best].bytes)) best = i;
+        }
+        if (best >= 0) {
+            *out = c.idle[best];
+            c.idle.erase(c.idle.begin() + best);
+            return PL_OK;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        // idle blocks of this device may be holding the memory: drop them and retry
+        cudaGetLastError();
+        pl_release_scratch();
+        e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(layer scratch)");
+    *out = ScratchBlock{p, bytes, dev};
+    return PL_OK;
+}
+
+void CUDART_CB scratch_return_cb(void* arg) {
+    ScratchBlock* b = static_cast<ScratchBlock*>(arg);
+    {
+        ScratchCache& c = scratch_cache();
+        std::lock_guard<std::mutex> lock(c.mu);
+        c.idle.push_back(*b);
+    }
+    delete b;
+}
+
+pl_status scratch_release_on_stream(const ScratchBlock& b, cudaStream_t st) {
+    ScratchBlock* arg = new ScratchBlock(b);
+    const cudaError_t e = cudaLaunchHostFunc(st, scratch_return_cb, arg);
+    if (e != cudaSuccess) {
+        delete arg;
+        return cuda_fail(e, "cudaLaunchHostFunc(scratch return)");
+    }
+    return PL_OK;
+}
+
 pl_status have_device() {
     static const int count = [] {
         int c = 0;
@@ -74,17 +153,18 @@ pl_status have_device() {
         return c;
     }();
     if (count == 0) return fail(PL_ERR_NODEVICE, "no CUDA device available (the engine has no CPU fallback)");
-    // Layer scratch comes from the stream-ordered allocator. Keep freed blocks
-    // cached in the device's default pool (as a caching allocator does): with
-    // the default release threshold of 0 every synchronisation would return
-    // them to the OS and the next call would re-map up to 2 x 9.6 GB.
+    // Per-call buffers of the host-pointer paths (inputs, outputs, status
+    // words) come from the stream-ordered pool: keep up to PL_POOL_KEEP_MB
+    // (default 1024) of freed pool memory mapped between calls, so a call
+    // does not re-map its staging buffers (layer scratch is separate, above).
     static std::once_flag pool_once[64];
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
         std::call_once(pool_once[dev], [dev] {
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t keep = UINT64_MAX;
+                const char* e = std::getenv("PL_POOL_KEEP_MB");
+                uint64_t keep = (e ? std::strtoull(e, nullptr, 10) : 1024ull) << 20;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
             }
             cudaGetLastError();
@@ -408,85 +488,92 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
     return fail(PL_ERR_ARG, "shared-memory kernel order out of range");
 }
 
-// Tile schedule of one layer range for the layer kernel: the valid tiles F of
-// [r0, r1) in increasing order, each dealt to the CTA with the least load so
-// far (load = chunks of `chunk` outputs, at least one per tile). Device
-// layout: offsets[grid + 1] then the concatenated per-CTA lists. Cached per
-// (device, n, k, D, r0, r1, grid).
-pl_status get_sched(int n, int k, int D, uint64_t r0, uint64_t r1, int grid, int chunk, const uint32_t** out) {
-    static std::mutex mu;
-    static std::map<std::vector<uint64_t>, uint32_t*> cache;
+// Tile tickets of one layer range (see sz_ws.cuh): the valid high sets F of
+// layer k (popcount in [max(0, k - D), min(k, H)]) from the range's first
+// one on, in increasing order. valid_below(X) counts the valid F < X.
+uint64_t valid_below(uint64_t X, int H, int fmin, int fmax) {
+    uint64_t c = 0;
+    int p = 0;
+    for (int b = H; b >= 0; --b) {
+        if (b == H) {
+            if (X >> H) {  // X = 2^H: every valid F counts
+                for (int j = fmin; j <= fmax; ++j) c += pl::binom_u64(H, j);
+                return c;
+            }
+            continue;
+        }
+        if ((X >> b) & 1) {
+            for (int j = std::max(0, fmin - p); j <= std::min(b, fmax - p); ++j) c += pl::binom_u64(b, j);
+            ++p;
+        }
+    }
+    return c;
+}
+
+struct Tickets {
+    uint32_t rank0 = 0, ntiles = 0;
+};
+
+Tickets layer_tickets(int n, int k, int D, uint64_t r0, uint64_t r1) {
+    const int H = n - D;
+    const int fmin = std::max(0, k - D), fmax = std::min(k, H);
+    const uint64_t F0 = pl_colex_unrank(k, r0) >> D;
+    const uint64_t F1 = pl_colex_unrank(k, r1 - 1) >> D;
+    Tickets t;
+    t.rank0 = (uint32_t)valid_below(F0, H, fmin, fmax);
+    t.ntiles = (uint32_t)(valid_below(F1 + 1, H, fmin, fmax) - t.rank0);
+    return t;
+}
+
+// Every layer's list of valid high sets (sz_tile_list_kernel), generated on
+// the device once per (device, n, D) -- at most a few tens of MB (n = 32:
+// ~7.6 M entries) -- and freed by pl_release_scratch.
+struct TileLists {
+    uint32_t* buf = nullptr;
+    std::vector<uint64_t> off;  // off[k]: first entry of layer k
+};
+
+std::mutex g_lists_mu;
+std::map<std::vector<int>, TileLists>& lists_cache() {
+    static auto* m = new std::map<std::vector<int>, TileLists>;
+    return *m;
+}
+
+pl_status get_tile_lists(int n, int D, const uint32_t** layer_base, int k) {
     int dev = 0;
     PL_CUDA(cudaGetDevice(&dev));
-    const std::vector<uint64_t> key = {(uint64_t)dev, (uint64_t)n, (uint64_t)k, (uint64_t)D, r0, r1, (uint64_t)grid, (uint64_t)chunk};
-    std::lock_guard<std::mutex> lock(mu);
+    std::lock_guard<std::mutex> lock(g_lists_mu);
+    auto& cache = lists_cache();
+    const std::vector<int> key = {dev, n, D};
     auto it = cache.find(key);
-    if (it != cache.end()) {
-        *out = it->second;
-        return PL_OK;
-    }
-    const uint32_t F0 = (uint32_t)(pl_colex_unrank(k, r0) >> D);
-    const uint32_t F1 = (uint32_t)(pl_colex_unrank(k, r1 - 1) >> D);
-    std::vector<std::vector<uint32_t>> lists(grid);
-    // least-loaded CTA, lowest index among equals: a bucket queue over loads (loads only
-    // grow, so the minimum moves forward), each bucket a bitset of CTAs -- O(1) per tile
-    const int words = (grid + 63) / 64;
-    std::vector<uint64_t> bits((size_t)words * 64, 0);  // bucket b at [b * words, (b + 1) * words)
-    auto bucket = [&](uint64_t b) -> uint64_t* {
-        if ((b + 1) * (uint64_t)words > bits.size()) bits.resize(std::max<size_t>(bits.size() * 2, (b + 1) * words), 0);
-        return bits.data() + b * (uint64_t)words;
-    };
-    for (int c = 0; c < grid; ++c) bucket(0)[c / 64] |= 1ull << (c % 64);
-    uint64_t min_load = 0;
-    static const auto C = [] {
-        std::vector<uint64_t> c(pl::kBinomDim * pl::kBinomDim);
-        for (int a = 0; a < pl::kBinomDim; ++a)
-            for (int b = 0; b < pl::kBinomDim; ++b) c[a * pl::kBinomDim + b] = pl::binom_u64(a, b);
-        return c;
-    }();
-    auto binom = [&](int a, int b) { return C[a * pl::kBinomDim + b]; };
-    const bool whole = r0 == 0 && r1 == binom(n, k);
-    for (uint32_t F = F0; F <= F1; ++F) {
-        const int f = __builtin_popcount(F), m = k - f;
-        if (m < 0 || m > D) continue;
-        const uint64_t len = binom(D, m);
-        uint64_t lo = 0, hi = len;
-        if (!whole) {
-            uint64_t base = 0;
-            int l = 1;
-            for (uint32_t ff = F; ff; ff &= ff - 1, ++l) base += binom(D + __builtin_ctz(ff), m + l);
-            lo = std::max(base, r0);
-            hi = std::min(base + len, r1);
+    if (it == cache.end()) {
+        const int H = n - D;
+        TileLists L;
+        L.off.assign(n + 1, 0);
+        uint64_t total = 0;
+        for (int kk = 3; kk <= n - 1; ++kk) {
+            L.off[kk] = total;
+            const int fmin = std::max(0, kk - D), fmax = std::min(kk, H);
+            total += valid_below(1ull << H, H, fmin, fmax);
         }
-        if (hi <= lo) continue;
-        const uint64_t chunks = (hi - lo + chunk - 1) / chunk;
-        for (;;) {
-            uint64_t* w = bucket(min_load);
-            int c = -1;
-            for (int i = 0; i < words; ++i) {
-                if (w[i]) {
-                    c = i * 64 + __builtin_ctzll(w[i]);
-                    break;
-                }
-            }
-            if (c < 0) {
-                ++min_load;
-                continue;
-            }
-            w[c / 64] &= ~(1ull << (c % 64));
-            lists[c].push_back(F);
-            bucket(min_load + chunks)[c / 64] |= 1ull << (c % 64);
-            break;
+        L.off[n] = total;
+        PL_CUDA(cudaMalloc(&L.buf, std::max<uint64_t>(total, 1) * sizeof(uint32_t)));
+        cudaStream_t st;
+        PL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (int kk = 3; kk <= n - 1; ++kk) {
+            const int fmin = std::max(0, kk - D), fmax = std::min(kk, H);
+            const uint32_t cnt = (uint32_t)(L.off[kk + 1] - L.off[kk]);
+            if (cnt == 0) continue;
+            const unsigned blocks = (unsigned)std::min<uint64_t>((cnt + 255) / 256, 4096);
+            pl::sz_tile_list_kernel<<<blocks, 256, 0, st>>>(H, fmin, fmax, cnt, L.buf + L.off[kk]);
         }
+        const cudaError_t e = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        PL_CUDA(e);
+        PL_CUDA(cudaGetLastError());
+        it = cache.emplace(key, std::move(L)).first;
     }
-    std::vector<uint32_t> flat(grid + 1, 0);
-    for (int b = 0; b < grid; ++b) flat[b + 1] = flat[b] + (uint32_t)lists[b].size();
-    for (int b = 0; b < grid; ++b) flat.insert(flat.end(), lists[b].begin(), lists[b].end());
-    uint32_t* d = nullptr;
-    PL_CUDA(cudaMalloc(&d, flat.size() * sizeof(uint32_t)));
-    PL_CUDA(cudaMemcpy(d, flat.data(), flat.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    cache[key] = d;
-    *out = d;
+    *layer_base = it->second.buf + it->second.off[k];
     return PL_OK;
 }
 
@@ -583,9 +670,11 @@ struct Unchecked<pl::RI64<true>> {
     using type = pl::RI64<false>;
 };
 
+// `tickets`: a device word that is zero when this launch starts (the layer
+// kernel's tile counter; unused for k = 2).
 template <class R>
 pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur, uint64_t r0, uint64_t r1,
-                       const int32_t* guard, int32_t* status, cudaStream_t st) {
+                       uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
     if (r1 <= r0) return PL_OK;
     if (k == 2) {
@@ -599,17 +688,13 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     Qtab q;
     pl_status s = get_qtab(D, &q);
     if (s != PL_OK) return s;
-    const uint32_t* sched = nullptr;
-    static const int team = [] {
-        const char* e = std::getenv("PL_WS_TEAM");  // tuning override: CTAs per tile
-        return e ? std::max(1, std::min(atoi(e), 8)) : 1;
-    }();
     static const int grid = [] {
         const char* e = std::getenv("PL_WS_GRID");  // tuning override of the layer-kernel grid
-        const int g = e ? std::max(1, std::min(atoi(e), num_sms())) : num_sms();
-        return std::max(team, g / team * team);
+        return e ? std::max(1, std::min(atoi(e), num_sms())) : num_sms();
     }();
-    s = get_sched(n, k, D, r0, r1, grid / team, pl::WsGeom<(int)sizeof(T)>::CHUNK, &sched);
+    const Tickets tk = layer_tickets(n, k, D, r0, r1);
+    const uint32_t* flist = nullptr;
+    s = get_tile_lists(n, D, &flist, k);
     if (s != PL_OK) return s;
     const size_t smem = pl::WsSmem<T>::bytes();
     auto kern = pl::sz_ws_kernel<R, typename Unchecked<R>::type>;
@@ -641,9 +726,9 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                               static_cast<T*>(cur), r0, r1, sched, static_cast<const uint4*>(q.ltab),
-                               static_cast<const uint32_t*>(q.offs), static_cast<const uint2*>(q.binom_pairs),
-                               guard, status, ws_hints(), team));
+                               static_cast<T*>(cur), r0, r1, tickets, flist + tk.rank0, tk.ntiles,
+                               static_cast<const uint4*>(q.ltab), static_cast<const uint32_t*>(q.offs),
+                               static_cast<const uint2*>(q.binom_pairs), guard, status, ws_hints()));
     if (trace) {
         PL_CUDA(cudaStreamSynchronize(st));
         std::vector<unsigned long long> hb((size_t)4 * pl::kWsTraceCap * 2);
@@ -670,15 +755,16 @@ pl_status launch_top(int n, const void* a, const void* last, void* out, const in
 }
 
 // Full single-matrix layer DP for one device-resident matrix (n >= 3).
+// tickets[k] (k < n) must be zero.
 template <class R>
-pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* buf1, const int32_t* guard,
-                     int32_t* status, cudaStream_t st) {
+pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* buf1, uint32_t* tickets,
+                     const int32_t* guard, int32_t* status, cudaStream_t st) {
     void* prev = buf0;
     void* cur = buf1;
-    pl_status s = launch_layer<R>(n, a_dev, 2, nullptr, prev, 0, pl::binom_u64(n, 2), guard, status, st);
+    pl_status s = launch_layer<R>(n, a_dev, 2, nullptr, prev, 0, pl::binom_u64(n, 2), nullptr, guard, status, st);
     if (s != PL_OK) return s;
     for (int k = 3; k <= n - 1; ++k) {
-        s = launch_layer<R>(n, a_dev, k, prev, cur, 0, pl::binom_u64(n, k), guard, status, st);
+        s = launch_layer<R>(n, a_dev, k, prev, cur, 0, pl::binom_u64(n, k), tickets + k, guard, status, st);
         if (s != PL_OK) return s;
         std::swap(prev, cur);
     }
@@ -686,8 +772,11 @@ pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* 
 }
 
 // Device-side batch compute: a_dev/out_dev device pointers, enqueue only.
+// `held`: a synchronous caller takes the large-order scratch block and
+// returns it to the cache after its stream synchronisation; otherwise a host
+// callback on the stream returns it.
 pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
-                        int32_t* status_dev, cudaStream_t st) {
+                        int32_t* status_dev, cudaStream_t st, ScratchBlock* held = nullptr) {
     if (count == 0) return PL_OK;
     if (n <= kRegsMaxOrder) {
         return with_ring(dt, fma, [&](auto r) { return launch_regs<decltype(r)>(n, a_dev, out_dev, count, status_dev, st); });
@@ -696,32 +785,40 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
         return with_ring(dt, fma,
                          [&](auto r) { return launch_smem<decltype(r)>(dt, n, a_dev, out_dev, count, status_dev, st); });
     }
-    // Large orders: one layer DP per matrix through global scratch.
+    // Large orders: one layer DP per matrix through global scratch (a cached
+    // cudaMalloc block; returned to the cache when the stream gets there).
     const size_t es = elem_size(dt);
     const uint64_t ml = max_layer(n);
-    void* bufs = nullptr;
-    int32_t* guards = nullptr;
+    // Head: tile tickets of every layer (64 words) and the int64 guard flag.
     // Layer buffers carry 64 bytes of slack: 8-byte rings stage 16-byte aligned
     // spans that may read one element past a layer's last entry.
     // Each buffer starts 256-byte aligned (TMA bulk copies need 16).
+    constexpr size_t kHead = 512;
     const size_t stride = (ml * es + 64 + 255) & ~size_t(255);
-    PL_CUDA(cudaMallocAsync(&bufs, 2 * stride, st));
-    PL_CUDA(cudaMallocAsync((void**)&guards, sizeof(int32_t), st));
-    PL_CUDA(cudaMemsetAsync(guards, 0, sizeof(int32_t), st));
-    pl_status s = PL_OK;
+    ScratchBlock blk;
+    pl_status s = scratch_acquire(kHead + 2 * stride, &blk);
+    if (s != PL_OK) return s;
+    uint32_t* tickets = static_cast<uint32_t*>(blk.ptr);
+    int32_t* guards = reinterpret_cast<int32_t*>(static_cast<char*>(blk.ptr) + 256);
+    char* bufs = static_cast<char*>(blk.ptr) + kHead;
     for (int64_t b = 0; b < count && s == PL_OK; ++b) {
         const char* ab = static_cast<const char*>(a_dev) + (size_t)b * n * n * es;
         char* ob = static_cast<char*>(out_dev) + (size_t)b * es;
+        s = cuda_fail_if(cudaMemsetAsync(blk.ptr, 0, kHead, st), "cudaMemsetAsync(tickets)");
+        if (s != PL_OK) break;
         if (dt == PL_I64) {
             pl::sz_guard_i64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(ab), n, guards);
         }
         s = with_ring(dt, fma, [&](auto r) {
-            return run_layers<decltype(r)>(n, ab, ob, bufs, static_cast<char*>(bufs) + stride, guards, status_dev, st);
+            return run_layers<decltype(r)>(n, ab, ob, bufs, bufs + stride, tickets, guards, status_dev, st);
         });
     }
-    cudaFreeAsync(bufs, st);
-    cudaFreeAsync(guards, st);
-    return s;
+    if (held) {
+        *held = blk;
+        return s;
+    }
+    const pl_status s2 = scratch_release_on_stream(blk, st);
+    return s != PL_OK ? s : s2;
 }
 
 // Host-pointer batches of batched orders: the batch moves in chunks so that the
@@ -832,6 +929,7 @@ pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out,
     }
     pl_status s = PL_OK;
     bool out_copied = false;
+    ScratchBlock held;
     static const bool host_pipe = [] {
         const char* e = std::getenv("PL_HOST_PIPE");  // 0: one upload, one kernel, one download (A/B)
         return !(e && e[0] == '0');
@@ -841,7 +939,7 @@ pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out,
         out_copied = true;
     } else {
         if (!dev_ptrs) PL_CUDA(cudaMemcpyAsync(a_dev, a, in_bytes, cudaMemcpyHostToDevice, st));
-        s = enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
+        s = enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st, &held);
     }
     int32_t status_host = 0;
     if (s == PL_OK) {
@@ -859,6 +957,14 @@ pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out,
     cudaFreeAsync(status_dev, st);
     const cudaError_t e3 = cudaStreamSynchronize(st);
     if (s == PL_OK && e3 != cudaSuccess) s = cuda_fail(e3, "cudaStreamSynchronize");
+    if (held.ptr) {
+        if (e3 == cudaSuccess) {
+            scratch_return_cb(new ScratchBlock(held));
+        } else {
+            cudaFree(held.ptr);  // the stream failed: do not recycle a block that may still be in use
+        }
+    }
+    if (!scratch_caching()) pl_release_scratch();
     if (s == PL_OK && (status_host & PL_STATUS_BIT_OVERFLOW)) {
         s = fail(PL_ERR_OVERFLOW,
                  "int64 overflow: an intermediate sub-permanent does not fit the exact int64 ring");
@@ -890,6 +996,24 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     return ::enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);
 }
 pl_status check_order_limits(int n, const pl_limits* lim) { return check_order(n, lim); }
+pl_status check_budget_limits(pl_dtype dt, int n, const pl_limits* lim) { return check_budget(dt, n, lim); }
+pl_status layer(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t r0,
+                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st) {
+    return with_ring(dt, fma, [&](auto r) {
+        return launch_layer<decltype(r)>(n, a, k, prev, cur, r0, r1, tickets, guard, status, st);
+    });
+}
+pl_status top(pl_dtype dt, bool fma, int n, const void* a, const void* last, void* out, const int32_t* guard,
+              int32_t* status, cudaStream_t st) {
+    return with_ring(dt, fma, [&](auto r) { return launch_top<decltype(r)>(n, a, last, out, guard, status, st); });
+}
+pl_status guard_i64(int n, const void* a, int32_t* guard, cudaStream_t st) {
+    pl::sz_guard_i64_kernel<<<1, 1, 0, st>>>(static_cast<const long long*>(a), n, guard);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+pl_status scratch_get(size_t bytes, ScratchBlock* out) { return ::scratch_acquire(bytes, out); }
+pl_status scratch_put(const ScratchBlock& b, cudaStream_t st) { return ::scratch_release_on_stream(b, st); }
 
 }  // namespace plc
 
@@ -903,6 +1027,7 @@ void pl_limits_default(pl_limits* out) {
     if (!out) return;
     out->subset_order_limit = PL_MAX_ORDER;
     out->memo_budget_bytes = 0;
+    out->num_gpus = 0;
 }
 
 int32_t pl_device_count(void) {
@@ -976,6 +1101,9 @@ pl_status pl_sz_permanent_batch(pl_dtype dtype, int32_t n, int64_t count, const 
                                 const pl_limits* limits, void* stream, int32_t* status_dev) {
     pl_status s = common_checks(dtype, n, count, a, out, limits);
     if (s != PL_OK) return s;
+    if (limits && limits->num_gpus >= 1) {
+        return plc::run_multi(dtype, n, count, a, out, flags, limits, nullptr, static_cast<cudaStream_t>(stream));
+    }
     return run_batch(dtype, n, count, a, out, flags, status_dev, static_cast<cudaStream_t>(stream));
 }
 
@@ -984,6 +1112,9 @@ pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, u
     if (flags & PL_FLAG_ASYNC) return fail(PL_ERR_ARG, "pl_sz_permanent is synchronous; use the batch entry point");
     pl_status s = common_checks(dtype, n, 1, a, out, limits);
     if (s != PL_OK) return s;
+    if (limits && limits->num_gpus >= 1) {
+        return plc::run_multi(dtype, n, 1, a, out, flags, limits, nullptr, static_cast<cudaStream_t>(stream));
+    }
     return run_batch(dtype, n, 1, a, out, flags, nullptr, static_cast<cudaStream_t>(stream));
 }
 
@@ -998,10 +1129,45 @@ pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, c
     if (dtype == PL_I64 && !guard_dev) return fail(PL_ERR_ARG, "int64 layers need the guard flag");
     pl_status s = have_device();
     if (s != PL_OK) return s;
-    return with_ring(dtype, flags & PL_FLAG_FMA, [&](auto r) {
-        return launch_layer<decltype(r)>(n, a_dev, k, prev_dev, cur_dev, r0, r1, guard_dev, status_dev,
-                                         static_cast<cudaStream_t>(stream));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* tickets = nullptr;
+    if (k > 2) {  // a zeroed tile counter for this launch, stream-ordered
+        PL_CUDA(cudaMallocAsync((void**)&tickets, sizeof(uint32_t), st));
+        PL_CUDA(cudaMemsetAsync(tickets, 0, sizeof(uint32_t), st));
+    }
+    s = with_ring(dtype, flags & PL_FLAG_FMA, [&](auto r) {
+        return launch_layer<decltype(r)>(n, a_dev, k, prev_dev, cur_dev, r0, r1, tickets, guard_dev, status_dev,
+                                         st);
     });
+    if (tickets) cudaFreeAsync(tickets, st);
+    return s;
+}
+
+void pl_release_scratch(void) {
+    std::vector<ScratchBlock> drop;
+    {
+        ScratchCache& c = scratch_cache();
+        std::lock_guard<std::mutex> lock(c.mu);
+        drop.swap(c.idle);
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const ScratchBlock& b : drop) {
+        cudaSetDevice(b.dev);
+        cudaFree(b.ptr);
+    }
+    {
+        // the cached tile lists: wait for every device's work that may still read them
+        std::lock_guard<std::mutex> lock(g_lists_mu);
+        for (auto& kv : lists_cache()) {
+            cudaSetDevice(kv.first[0]);
+            cudaDeviceSynchronize();
+            cudaFree(kv.second.buf);
+        }
+        lists_cache().clear();
+    }
+    cudaSetDevice(cur);
+    cudaGetLastError();
 }
 
 pl_status pl_sz_top(pl_dtype dtype, int32_t n, const void* a_dev, const void* last_dev, void* out_dev,

@@ -22,6 +22,27 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
                         int32_t* status_dev, cudaStream_t st);
 // Order check of the permanent entry points (subset_order_limit, device cap).
 pl_status check_order_limits(int n, const pl_limits* lim);
+// memo_budget_bytes check (layer scratch of one device).
+pl_status check_budget_limits(pl_dtype dt, int n, const pl_limits* lim);
+// One layer range / the top level / the int64 guard on the current device (see pl_sz_layer;
+// `tickets` a zeroed device word for k > 2).
+pl_status layer(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t r0,
+                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st);
+pl_status top(pl_dtype dt, bool fma, int n, const void* a, const void* last, void* out, const int32_t* guard,
+              int32_t* status, cudaStream_t st);
+pl_status guard_i64(int n, const void* a, int32_t* guard, cudaStream_t st);
+// Cached layer scratch of the current device (cudaMalloc blocks), handed back
+// to the cache when `st` reaches the point of the call.
+struct ScratchBlock {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    int dev = 0;
+};
+pl_status scratch_get(size_t bytes, ScratchBlock* out);
+pl_status scratch_put(const ScratchBlock& b, cudaStream_t st);
+// The multi-GPU path (multi.cu): limits->num_gpus >= 1, devices NULL = 0..g-1.
+pl_status run_multi(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,
+                    const pl_limits* lim, const int32_t* devices, cudaStream_t caller);
 
 }  // namespace plc
 

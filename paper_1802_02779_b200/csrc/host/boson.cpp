@@ -70,6 +70,7 @@ pl_limits to_c(const Limits& l) {
     pl_limits_default(&c);
     c.subset_order_limit = l.subset_order_limit;
     c.memo_budget_bytes = l.memo_budget_bytes;
+    c.num_gpus = l.num_gpus;
     return c;
 }
 

@@ -52,6 +52,7 @@ pl_limits to_c(const Limits& l) {
     pl_limits_default(&c);
     c.subset_order_limit = l.subset_order_limit;
     c.memo_budget_bytes = l.memo_budget_bytes;
+    c.num_gpus = l.num_gpus;
     return c;
 }
 
@@ -96,6 +97,8 @@ Limits Limits::from_env() {
             limits.enumeration_cap = v;
         } else if (key == "memo_budget_bytes") {
             limits.memo_budget_bytes = v;
+        } else if (key == "num_gpus") {
+            limits.num_gpus = static_cast<int>(v);
         } else {
             throw DomainError("PERMLAB_LIMITS: unknown key '" + std::string(key) + "'");
         }
@@ -211,6 +214,8 @@ PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limi
             r.value = v;
             break;
         }
+        case RingTag::Rational:
+            throw DomainError("the rational ring has no device arithmetic (use int, real or complex)");
         case RingTag::Complex: {
             Cplx v;
             check(pl_sz_permanent(PL_C128, a.order(), a.data(), &v, 0, &lim, nullptr));
@@ -298,6 +303,8 @@ std::vector<PermanentResult> store_zechin_permanent_batch(const std::vector<Squa
         case RingTag::Complex:
             run(Cplx{});
             break;
+        case RingTag::Rational:
+            throw DomainError("the rational ring has no device arithmetic (use int, real or complex)");
     }
     return out;
 }

@@ -19,11 +19,15 @@
 // ascending" is the reference's ascending-j order; the non-FMA rings keep its
 // rounding sequence bit for bit.
 //
-// Schedule. One CTA per SM, persistent. The host deals the layer's tiles, in
-// increasing F (increasing colex order), to the least-loaded CTA, so the GPU
-// sweeps each layer as one tight front and stream tiles of nearby high columns
-// are re-read from L2 (far ones are loaded evict-first). Launched with
-// programmatic dependent launch: the prologue overlaps the previous layer.
+// Schedule. One CTA per SM, persistent. Tiles are claimed on the device, in
+// increasing F (increasing colex order), from one ticket counter per launch:
+// ticket t is the t-th valid high set F (popcount in [k - D, k]) from the
+// range's first one on, read from the layer's tile list (generated once per
+// (device, n) by sz_tile_list_kernel and cached). So the GPU sweeps each
+// layer as one tight front, every SM takes the next tile when it has room
+// (no per-CTA schedule to build on the host), and stream tiles of nearby
+// high columns are re-read from L2 (far ones are loaded evict-first). Launched with programmatic dependent launch:
+// the prologue overlaps the previous layer.
 //
 // Roles (warp-specialised, mbarrier hand-offs, no CTA-wide sync after setup).
 //   publisher (last warp)  walks the CTA's tile list; per tile builds the
@@ -428,19 +432,34 @@ struct WsTrace {
 };
 #endif
 
-// ---------------------------------------------------------------- tile list
+// ---------------------------------------------------------------- tile lists
 
-// The CTA's tile list. The host deals the layer's tiles, in increasing F, to
-// the least-loaded team (load = chunks); a team of tP CTAs shares one list and
-// splits every tile's chunks (CTA tp takes chunks tp, tp + tP, ...).
-struct WsCursor {
-    const uint32_t* list;
-    uint32_t pos, end;
-};
-
-__device__ __forceinline__ WsCursor ws_cursor(const uint32_t* __restrict__ sched, int nteams, int team) {
-    const uint32_t* off = sched;
-    return {sched + nteams + 1, __ldg(off + team), __ldg(off + team + 1)};
+// Valid high sets of layer k: F in [0, 2^H) with fmin <= popc(F) <= fmax
+// (fmin = max(0, k - D), fmax = min(k, H)), in increasing integer order (=
+// increasing colex rank of their tiles). Thread g writes the g-th one: bit b
+// is 0 iff g < the number of valid completions of the prefix with bit b = 0,
+// sum_{j in [fmin - p, fmax - p]} C(b, j) (p = ones so far).
+__global__ void sz_tile_list_kernel(int H, int fmin, int fmax, uint32_t count, uint32_t* __restrict__ out) {
+    const uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t g = g0; g < count; g += gridDim.x * blockDim.x) {
+        uint32_t r = g, F = 0;
+        int p = 0;
+        for (int b = H - 1; b >= 0; --b) {
+            uint64_t c0 = 0;
+            const int jlo = fmin - p > 0 ? fmin - p : 0, jhi = fmax - p < b ? fmax - p : b;
+            uint64_t c = binom_u64(b, jlo);
+            for (int j = jlo; j <= jhi; ++j) {  // C(b, j) by the multiplicative step
+                c0 += c;
+                c = c * (uint64_t)(b - j) / (uint64_t)(j + 1);
+            }
+            if (r >= c0) {
+                r -= (uint32_t)c0;
+                F |= 1u << b;
+                ++p;
+            }
+        }
+        out[g] = F;
+    }
 }
 
 // ---------------------------------------------------------------- consumer math
@@ -623,10 +642,10 @@ __device__ __forceinline__ void ws_consume_dispatch(const WsSmem<T>& sm, const W
 template <class R, class RU>
 __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 1)
     __maxnreg__(WsGeom<(int)sizeof(typename R::T)>::kMaxReg) sz_ws_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
-                 typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ sched,
-                 const uint4* __restrict__ qtab, const uint32_t* __restrict__ qtab_off,
-                 const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
-                 int32_t* __restrict__ status, uint32_t hints, int tP) {
+                 typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, uint32_t* __restrict__ tickets,
+                 const uint32_t* __restrict__ flist, uint32_t ntiles, const uint4* __restrict__ qtab,
+                 const uint32_t* __restrict__ qtab_off, const uint2* __restrict__ binom_pairs,
+                 const int32_t* __restrict__ guard, int32_t* __restrict__ status, uint32_t hints) {
     using T = typename R::T;
     constexpr int NSG = WsSmem<T>::NSG;
     constexpr int NHDR = WsSmem<T>::NHDR;
@@ -676,15 +695,18 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
     __syncthreads();
 
-    const int nteams = (int)gridDim.x / tP;
-    const int tp = (int)blockIdx.x / nteams;
     if (warp == CW + WsSmem<T>::NST) {
         // ------------------------------------------------------------ publisher
-        // Walks the CTA's tile list; per tile with work for this CTA it builds
-        // the header (two warp scans, no loops) and stages the low source into
-        // the next tile slot; a terminal header ends the sequence.
-        WsCursor lst = ws_cursor(sched, nteams, (int)blockIdx.x % nteams);
+        // Claims tiles (see the schedule note above); per tile it builds the
+        // header (two warp scans, no loops) and stages the low source into the
+        // next tile slot; a terminal header ends the sequence. It publishes a
+        // new tile only while the chunks already queued here are at most
+        // `qcap` (hints bits 20-27; 0 = as far ahead as the slots allow): a CTA
+        // must not hoard tiles its consumers cannot reach before the layer's
+        // end while other SMs idle.
         const int H = n - D;
+        const uint32_t qcap = (hints >> 20) & 0xffu;
+        uint32_t queued = 0;         // chunks of published tiles not yet released
         uint32_t pub = 0, rel = 0;   // tiles published / tiles whose release this warp has seen
         uint32_t head = 0, tail = 0; // source ring: end of the newest, start of the oldest in-flight source
         // wait until tile `rel` is released by every consumer and streamer warp
@@ -694,6 +716,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 mbar_wait_slot(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u);
             else
                 mbar_wait_backoff(&sm.src_empty[rel % NHDR], (rel / NHDR) & 1u, kPubSleepNs);
+            queued -= sm.hdr[rel % NHDR].nchunks;
             ++rel;
             tail = rel < pub ? sm.hdr[rel % NHDR].src_off : head;
         };
@@ -720,11 +743,28 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
         };
         WsTrace tr;
         tr.init(3);
-        uint32_t F_next = lst.pos < lst.end ? __ldg(lst.list + lst.pos) : 0u;
-        for (; lst.pos < lst.end;) {
-            const uint32_t F = F_next;
-            ++lst.pos;
-            if (lst.pos < lst.end) F_next = __ldg(lst.list + lst.pos);
+        // lane 0 keeps two claims in flight: while tile i is published, the F
+        // of tile i + 1 is being loaded (its ticket arrived one tile ago) and
+        // the ticket of tile i + 2 is being taken; no round trip is waited for
+        // inside a tile. Tickets rise per CTA, so past ntiles nothing is lost.
+        uint32_t q_t1 = 0, q_F1 = 0, q_t2 = 0;
+        if (lane == 0) {
+            q_t1 = atomicAdd(tickets, 1u);
+            q_F1 = q_t1 < ntiles ? __ldg(flist + q_t1) : 0u;
+            q_t2 = atomicAdd(tickets, 1u);
+        }
+        for (;;) {
+            if (qcap) {
+                while (pub != rel && queued > qcap) release_one();
+            }
+            const uint32_t t_cur = __shfl_sync(0xffffffffu, q_t1, 0);
+            if (t_cur >= ntiles) break;
+            const uint32_t F = __shfl_sync(0xffffffffu, q_F1, 0);
+            if (lane == 0) {
+                q_t1 = q_t2;
+                q_F1 = q_t1 < ntiles ? __ldg(flist + q_t1) : 0u;
+                q_t2 = q_t1 < ntiles ? atomicAdd(tickets, 1u) : q_t1;
+            }
             const int f = __popc(F), m = k - f;
             // lane h stands for high column D + h; set lanes are F's elements in
             // increasing order, idx = position among them
@@ -749,8 +789,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             const uint32_t len = sm.B2[m * kBinomDim + D].x;
             const uint32_t q0 = r0 > cur_base ? (uint32_t)(r0 - cur_base) : 0u;
             const uint32_t q1 = (r1 - cur_base) < len ? (uint32_t)(r1 - cur_base) : len;
-            const uint32_t total = q1 > q0 ? (q1 - q0 + CHUNK - 1) / CHUNK : 0u;
-            const uint32_t nchunks = total > (uint32_t)tp ? (total - tp + tP - 1) / tP : 0u;
+            const uint32_t nchunks = q1 > q0 ? (q1 - q0 + CHUNK - 1) / CHUNK : 0u;
             if (nchunks == 0) continue;
 
             // the low source X(F, k-1): C(D, m-1) entries (+ alignment pad and round-up)
@@ -762,6 +801,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             head = soff + salloc;
             tr.ev(9, pub);
             ++pub;
+            queued += nchunks;
             WsHdr<T>& h = sm.hdr[ss];
             if (set) {
                 h.coef[idx] = row_sh[D + lane];
@@ -785,8 +825,8 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
                 h.f = f;
                 h.q1 = q1;
                 h.nchunks = nchunks;
-                h.cb = q0 + tp * CHUNK;
-                h.cs = tP * CHUNK;
+                h.cb = q0;
+                h.cs = CHUNK;
                 h.cur_base = cur_base;
                 h.qoff = qoff_sh[m];
                 h.pad_src = sizeof(T) == 16 ? 0u : (uint32_t)(src_base & 1u);
@@ -795,7 +835,7 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             }
             {
                 // chunk starts cb + i * cs share cb's parity (cs is even)
-                const uint32_t cbv = q0 + tp * CHUNK;
+                const uint32_t cbv = q0;
                 const uint32_t pm = __reduce_or_sync(0xffffffffu, set && ((sbase + cbv) & 1u) ? 1u << idx : 0u);
                 if (lane == 0) h.padmask = sizeof(T) == 16 ? 0u : pm;
             }

@@ -20,6 +20,7 @@
 
 #include "permlab/boson.hpp"
 #include "permlab/permanent.hpp"
+#include "permlab_b200.h"
 
 using namespace permlab;
 
@@ -282,6 +283,38 @@ void device_run_and_batch() {
     CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(20, 1)))) == 2432902008176640000LL);
 }
 
+// Limits.num_gpus >= 1: the single-process multi-GPU path (NCCL communicators
+// over devices 0..g-1; this box has one GPU, so g = 1 -- the all-gather plan
+// through ncclAllGather on a one-rank communicator). Bitwise equal to the
+// oracle and to the default single-device path.
+void device_multi() {
+    int devices = pl_device_count();
+    Limits multi;
+    multi.num_gpus = 1;
+    std::mt19937_64 g(73);
+    for (int n : {15, 18, 21}) {
+        const auto mc = random_cplx_matrix(n, g);
+        const Cplx vm = std::get<Cplx>(store_zechin_permanent(SquareMatrix(mc), multi).value);
+        CHECK(vm == oracle_cplx(mc));
+        CHECK(vm == std::get<Cplx>(store_zechin_permanent(SquareMatrix(mc)).value));
+        const auto mi = random_int_matrix(n, g, -2, 2);
+        CHECK(value_of(store_zechin_permanent(SquareMatrix(mi), multi)) == oracle_int(mi));
+    }
+    // int64 overflow is a DomainError through the sharded path too
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(22, 1000)), multi), DomainError);
+    // a batch of small orders is split by matrix across the devices
+    std::vector<SquareMatrix> batch;
+    for (int b = 0; b < 64; ++b) batch.emplace_back(random_int_matrix(9, g));
+    const auto split = store_zechin_permanent_batch(batch, multi);
+    for (std::size_t b = 0; b < batch.size(); ++b) {
+        CHECK(value_of(split[b]) == oracle_int(batch[b].as<Int>()));
+    }
+    // more devices than the box has: a DomainError before any work
+    Limits too_many;
+    too_many.num_gpus = devices + 1;
+    CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(16, 1)), too_many), DomainError);
+}
+
 // ---------------------------------------------------------------- boson sampling
 // mirrors reference tests/test_boson.cpp case by case
 
@@ -431,6 +464,7 @@ int main(int argc, char** argv) {
         device_oracle_agreement();
         device_identities();
         device_run_and_batch();
+        device_multi();
         device_boson();
     }
     std::printf("%d checks, %d failures\n", g_checks, g_failures);

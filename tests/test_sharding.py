@@ -228,3 +228,80 @@ def test_gloo_overflow_status_combined_over_ranks(world, plan):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert set(results.values()) == {"overflow"}
+
+
+# ---------------------------------------------------------------- the C ABI's single-process plans
+
+def _c_plan(n, world, rank, k):
+    import ctypes as C
+    from paper_1802_02779_b200 import _native as N
+
+    r0, r1 = C.c_uint64(), C.c_uint64()
+    assert N.lib.pl_shard_range(n, world, rank, k, C.byref(r0), C.byref(r1)) == 0
+    cnt = N.lib.pl_shard_exchange(n, world, rank, k, None, 0)
+    buf = (C.c_uint64 * (4 * max(cnt, 1)))()
+    assert N.lib.pl_shard_exchange(n, world, rank, k, buf, cnt) == cnt
+    ops = [("recv" if buf[4 * i] else "send", int(buf[4 * i + 1]), int(buf[4 * i + 2]), int(buf[4 * i + 3]))
+           for i in range(cnt)]
+    return (int(r0.value), int(r1.value)), ops
+
+
+def _py_exchange(n, k, rank, world):
+    """The schedule sharded.exchange_blocks / gather_last_layer run, as a list."""
+    from paper_1802_02779_b200.sharded import top_columns
+
+    t = top_columns(world)
+    ops = []
+    if k < n - 1:
+        for i in range(t):
+            partner = rank ^ (1 << i)
+            if rank >> i & 1:
+                r0, r1 = top_block(n, k, world, partner)
+                if r1 > r0:
+                    ops.append(("recv", partner, r0, r1))
+            else:
+                r0, r1 = top_block(n, k, world, rank)
+                if r1 > r0:
+                    ops.append(("send", partner, r0, r1))
+    else:  # layer n-1 to rank 0 (the C path's top level runs on device 0)
+        for h in range(1, world):
+            r0, r1 = top_block(n, k, world, h)
+            if r1 > r0:
+                if rank == 0:
+                    ops.append(("recv", h, r0, r1))
+                if rank == h:
+                    ops.append(("send", 0, r0, r1))
+    return ops
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8, 16])
+def test_c_abi_shard_plan_matches_sharded_py(world):
+    """pl_shard_* (the single-process NCCL path of pl_sz_permanent_multi) use
+    the same ranges and point-to-point schedule as sharded.py; every output
+    is owned by exactly one rank and every received block is sent by its
+    owner."""
+    from paper_1802_02779_b200 import _native as N
+
+    for n in (5, 9, 12, 20, 26, 32):
+        blocks = block_plan_applies(n, world)
+        assert N.lib.pl_shard_plan(n, world) == (N.PL_SHARD_BLOCKS if blocks else N.PL_SHARD_ALLGATHER)
+        for k in range(2, n):
+            owned = []
+            sends, recvs = set(), set()
+            for rank in range(world):
+                rng, ops = _c_plan(n, world, rank, k)
+                want = top_block(n, k, world, rank) if blocks else layer_slices(n, k, world)[1][rank]
+                assert rng == tuple(want)
+                if rng[1] > rng[0]:
+                    owned.append(rng)
+                if blocks:
+                    assert ops == _py_exchange(n, k, rank, world)
+                    for kind, peer, r0, r1 in ops:
+                        (sends if kind == "send" else recvs).add((rank, peer, r0, r1) if kind == "send" else
+                                                                 (peer, rank, r0, r1))
+                else:
+                    assert ops == []
+            owned.sort()
+            assert owned[0][0] == 0 and owned[-1][1] == comb(n, k)
+            assert all(owned[i][1] == owned[i + 1][0] for i in range(len(owned) - 1))
+            assert sends == recvs
