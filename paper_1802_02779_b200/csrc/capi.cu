@@ -21,6 +21,7 @@
 #include "../../include/permlab_b200.h"
 #include "sz_kernels.cuh"
 #include "sz_ws.cuh"
+#include "sz_lean.cuh"
 #include "sz_batch.cuh"
 #include "capi_internal.h"
 
@@ -75,13 +76,24 @@ uint64_t max_layer(int n) {
 // PL_SCRATCH_CACHE=0 every synchronous call does so before returning.
 using plc::ScratchBlock;
 
+// An idle block remembers the stream of its last use and an event recorded
+// there at the end of that use: a call on the same stream reuses it at once
+// (stream order), a call on another stream first waits for the event. No host
+// callback sits in the stream (a cudaLaunchHostFunc node stalls the stream
+// until a driver thread has run it: ~0.3 ms per C4 call, round 2).
+struct IdleBlock {
+    ScratchBlock b;
+    cudaEvent_t ev = nullptr;  // null: no use pending
+    cudaStream_t st = nullptr;
+};
+
 struct ScratchCache {
     std::mutex mu;
-    std::vector<ScratchBlock> idle;
+    std::vector<IdleBlock> idle;
 };
 
 ScratchCache& scratch_cache() {
-    static ScratchCache* c = new ScratchCache;  // never destroyed: host callbacks may run at exit
+    static ScratchCache* c = new ScratchCache;  // never destroyed: calls may still run at exit
     return *c;
 }
 
@@ -93,22 +105,47 @@ bool scratch_caching() {
     return on;
 }
 
-pl_status scratch_acquire(size_t bytes, ScratchBlock* out) {
+// Block for a call on stream `st` (may be null: the caller then synchronises
+// with the block's last use itself, see scratch_acquire_sync).
+pl_status scratch_acquire_on(size_t bytes, cudaStream_t st, ScratchBlock* out) {
     int dev = 0;
     PL_CUDA(cudaGetDevice(&dev));
+    IdleBlock got;
+    bool have = false;
     {
         ScratchCache& c = scratch_cache();
         std::lock_guard<std::mutex> lock(c.mu);
         int best = -1;
         for (int i = 0; i < (int)c.idle.size(); ++i) {
-            const ScratchBlock& b = c.idle[i];
-            if (b.dev == dev && b.bytes >= bytes && (best < 0 || b.bytes < c.idle[best].bytes)) best = i;
+            const ScratchBlock& b = c.idle[i].b;
+            if (b.dev == dev && b.bytes >= bytes && (best < 0 || b.bytes < c.idle[best].b.bytes)) best = i;
         }
         if (best >= 0) {
-            *out = c.idle[best];
+            got = c.idle[best];
             c.idle.erase(c.idle.begin() + best);
-            return PL_OK;
+            have = true;
         }
+    }
+    if (have) {
+        if (got.ev) {
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
+            cudaError_t e = cudaSuccess;
+            if (got.st != st && cap == cudaStreamCaptureStatusNone) {
+                e = cudaStreamWaitEvent(st, got.ev, 0);
+            } else if (got.st != st) {
+                // a capture cannot depend on uncaptured work: wait for it on the host
+                // (relaxed mode for this thread: a global-mode capture forbids the sync)
+                cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+                cudaThreadExchangeStreamCaptureMode(&mode);
+                e = cudaEventSynchronize(got.ev);
+                cudaThreadExchangeStreamCaptureMode(&mode);
+            }
+            cudaEventDestroy(got.ev);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent(scratch)");
+        }
+        *out = got.b;
+        return PL_OK;
     }
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
@@ -123,23 +160,32 @@ pl_status scratch_acquire(size_t bytes, ScratchBlock* out) {
     return PL_OK;
 }
 
-void CUDART_CB scratch_return_cb(void* arg) {
-    ScratchBlock* b = static_cast<ScratchBlock*>(arg);
-    {
-        ScratchCache& c = scratch_cache();
-        std::lock_guard<std::mutex> lock(c.mu);
-        c.idle.push_back(*b);
-    }
-    delete b;
+
+// A block whose use has completed (the caller synchronised).
+void scratch_return_idle(const ScratchBlock& b) {
+    ScratchCache& c = scratch_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.idle.push_back(IdleBlock{b, nullptr, nullptr});
 }
 
 pl_status scratch_release_on_stream(const ScratchBlock& b, cudaStream_t st) {
-    ScratchBlock* arg = new ScratchBlock(b);
-    const cudaError_t e = cudaLaunchHostFunc(st, scratch_return_cb, arg);
-    if (e != cudaSuccess) {
-        delete arg;
-        return cuda_fail(e, "cudaLaunchHostFunc(scratch return)");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
+    if (cap != cudaStreamCaptureStatusNone) {
+        // captured into a CUDA graph: every replay uses this block, so the graph
+        // owns it for the life of the process
+        return PL_OK;
     }
+    cudaEvent_t ev = nullptr;
+    PL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    const cudaError_t e = cudaEventRecord(ev, st);
+    if (e != cudaSuccess) {
+        cudaEventDestroy(ev);
+        return cuda_fail(e, "cudaEventRecord(scratch)");
+    }
+    ScratchCache& c = scratch_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.idle.push_back(IdleBlock{b, ev, st});
     return PL_OK;
 }
 
@@ -661,6 +707,94 @@ pl_status get_qtab(int D, Qtab* out) {
     return PL_OK;
 }
 
+// Compact low-term table of the lean kernel (sz_lean.cuh, ln_ltab): the m
+// entries of the m-subset V of [0, D) in one uint4 (m <= 8) or two (m > 8);
+// offs[m] in uint4 units. D <= 12: at most 70 KB (D = 10: 20 KB), L1-resident.
+struct LtabCompact {
+    uint4* ltab = nullptr;
+    uint32_t* offs = nullptr;
+};
+
+pl_status get_ltab_compact(int D, LtabCompact* out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, LtabCompact> cache;
+    int dev = 0;
+    PL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, D});
+    if (it != cache.end()) {
+        *out = it->second;
+        return PL_OK;
+    }
+    if (D > pl::kLnMaxD) return fail(PL_ERR_LIMIT, "lean layer window %d exceeds %d", D, pl::kLnMaxD);
+    std::vector<uint32_t> offs(D + 2, 0);
+    for (int m = 0; m <= D; ++m) offs[m + 1] = offs[m] + (m <= 8 ? 1u : 2u) * (uint32_t)pl::binom_u64(D, m);
+    std::vector<uint16_t> tab((size_t)offs[D + 1] * 8, 0);
+    for (uint32_t mask = 0; mask < (1u << D); ++mask) {
+        const int m = __builtin_popcount(mask);
+        uint32_t r = 0;
+        int i = 1;
+        for (uint32_t mm = mask; mm; mm &= mm - 1, ++i) r += (uint32_t)pl::binom_u64(__builtin_ctz(mm), i);
+        uint16_t* e = &tab[((size_t)offs[m] + (size_t)r * (m <= 8 ? 1 : 2)) * 8];
+        int t = 0;
+        for (uint32_t mm = mask; mm; mm &= mm - 1, ++t) {
+            const int v = __builtin_ctz(mm);
+            const uint32_t rest = mask & ~(1u << v);
+            uint32_t rr = 0;
+            int l = 1;
+            for (uint32_t q = rest; q; q &= q - 1, ++l) rr += (uint32_t)pl::binom_u64(__builtin_ctz(q), l);
+            e[t] = (uint16_t)(rr | (uint32_t)v << pl::kWsLtabRankBits);
+        }
+    }
+    LtabCompact q;
+    PL_CUDA(cudaMalloc(&q.ltab, std::max<size_t>(tab.size(), 8) * sizeof(uint16_t)));
+    PL_CUDA(cudaMalloc(&q.offs, offs.size() * sizeof(uint32_t)));
+    PL_CUDA(cudaMemcpy(q.ltab, tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    PL_CUDA(cudaMemcpy(q.offs, offs.data(), offs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    cache[{dev, D}] = q;
+    *out = q;
+    return PL_OK;
+}
+
+// Layer kernel choice: the lean kernel (sz_lean.cuh) for layers of at most
+// PL_LEAN_MAX_MB (default 24) -- the outer layers, where the warp-specialised
+// kernel's per-tile pipeline latency dominates (C4 k <= 8, k >= 17: 9-36 us
+// against 11-46 us per layer, profiles/r2b) -- and the warp-specialised
+// kernel (sz_ws.cuh) for the large middle layers, where its staged streams
+// keep more loads in flight. PL_LAYER_KERNEL=lean|ws forces one.
+bool use_lean_layer(size_t elem, int n, int k) {
+    static const int force = [] {
+        const char* e = std::getenv("PL_LAYER_KERNEL");
+        if (e && std::string(e) == "lean") return 1;
+        if (e && std::string(e) == "ws") return 0;
+        return -1;
+    }();
+    if (force >= 0) return force == 1;
+    static const uint64_t max_bytes = [] {
+        const char* e = std::getenv("PL_LEAN_MAX_MB");
+        return (e ? std::strtoull(e, nullptr, 10) : 24ull) << 20;
+    }();
+    return pl::binom_u64(n, k) * elem <= max_bytes;
+}
+
+int lean_window(int n) { return std::max(1, std::min(pl::kLnMaxD, n - 3)); }  // >= 8 high sets per layer
+
+template <class K>
+int blocks_per_sm(K kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<const void*, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(reinterpret_cast<const void*>(kern));
+    if (it != cache.end()) return it->second;
+    int b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem) != cudaSuccess || b < 1) {
+        cudaGetLastError();
+        b = 1;
+    }
+    cache[reinterpret_cast<const void*>(kern)] = b;
+    return b;
+}
+
 template <class R>
 struct Unchecked {
     using type = R;
@@ -682,6 +816,46 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         pl::sz_base_layer_kernel<R><<<blocks, 256, 0, st>>>(static_cast<const T*>(a), n, static_cast<T*>(cur), r0, r1,
                                                             status);
         PL_CUDA(cudaGetLastError());
+        return PL_OK;
+    }
+    if (use_lean_layer(sizeof(T), n, k)) {
+        const int D = lean_window(n);
+        LtabCompact lt;
+        pl_status s = get_ltab_compact(D, &lt);
+        if (s != PL_OK) return s;
+        Qtab qb;
+        s = get_qtab(D, &qb);  // binomial pairs
+        if (s != PL_OK) return s;
+        const Tickets tk = layer_tickets(n, k, D, r0, r1);
+        const uint32_t* flist = nullptr;
+        s = get_tile_lists(n, D, &flist, k);
+        if (s != PL_OK) return s;
+        const size_t smem = sizeof(pl::LnSmem<T>);
+        auto kern = pl::sz_lean_kernel<R, typename Unchecked<R>::type>;
+        constexpr int threads = pl::LnGeom<(int)sizeof(T)>::kThreads;
+        PL_CUDA(set_smem_once(kern, smem));
+        const int per_sm = blocks_per_sm(kern, threads, smem);
+        constexpr int wpb = pl::LnGeom<(int)sizeof(T)>::WPB;
+        const unsigned grid = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((tk.ntiles + wpb - 1) / wpb, (uint64_t)num_sms() * per_sm));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        static const bool pdl_l = [] {
+            const char* e = std::getenv("PL_WS_PDL");
+            return !(e && e[0] == '0');
+        }();
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_l ? 1 : 0;
+        PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
+                                   static_cast<T*>(cur), r0, r1, flist + tk.rank0, tk.ntiles,
+                                   static_cast<const uint4*>(lt.ltab), static_cast<const uint32_t*>(lt.offs),
+                                   static_cast<const uint2*>(qb.binom_pairs), guard, status));
         return PL_OK;
     }
     const int D = tile_window(sizeof(T), n);
@@ -796,7 +970,7 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     constexpr size_t kHead = 512;
     const size_t stride = (ml * es + 64 + 255) & ~size_t(255);
     ScratchBlock blk;
-    pl_status s = scratch_acquire(kHead + 2 * stride, &blk);
+    pl_status s = scratch_acquire_on(kHead + 2 * stride, st, &blk);
     if (s != PL_OK) return s;
     uint32_t* tickets = static_cast<uint32_t*>(blk.ptr);
     int32_t* guards = reinterpret_cast<int32_t*>(static_cast<char*>(blk.ptr) + 256);
@@ -959,7 +1133,7 @@ pl_status run_batch(pl_dtype dt, int n, int64_t count, const void* a, void* out,
     if (s == PL_OK && e3 != cudaSuccess) s = cuda_fail(e3, "cudaStreamSynchronize");
     if (held.ptr) {
         if (e3 == cudaSuccess) {
-            scratch_return_cb(new ScratchBlock(held));
+            scratch_return_idle(held);
         } else {
             cudaFree(held.ptr);  // the stream failed: do not recycle a block that may still be in use
         }
@@ -1012,7 +1186,7 @@ pl_status guard_i64(int n, const void* a, int32_t* guard, cudaStream_t st) {
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
-pl_status scratch_get(size_t bytes, ScratchBlock* out) { return ::scratch_acquire(bytes, out); }
+pl_status scratch_get(size_t bytes, cudaStream_t st, ScratchBlock* out) { return ::scratch_acquire_on(bytes, st, out); }
 pl_status scratch_put(const ScratchBlock& b, cudaStream_t st) { return ::scratch_release_on_stream(b, st); }
 
 }  // namespace plc
@@ -1144,7 +1318,7 @@ pl_status pl_sz_layer(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, c
 }
 
 void pl_release_scratch(void) {
-    std::vector<ScratchBlock> drop;
+    std::vector<IdleBlock> drop;
     {
         ScratchCache& c = scratch_cache();
         std::lock_guard<std::mutex> lock(c.mu);
@@ -1152,9 +1326,13 @@ void pl_release_scratch(void) {
     }
     int cur = 0;
     cudaGetDevice(&cur);
-    for (const ScratchBlock& b : drop) {
-        cudaSetDevice(b.dev);
-        cudaFree(b.ptr);
+    for (const IdleBlock& ib : drop) {
+        cudaSetDevice(ib.b.dev);
+        if (ib.ev) {
+            cudaEventSynchronize(ib.ev);  // its last use has finished
+            cudaEventDestroy(ib.ev);
+        }
+        cudaFree(ib.b.ptr);
     }
     {
         // the cached tile lists: wait for every device's work that may still read them

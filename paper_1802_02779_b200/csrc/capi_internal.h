@@ -31,14 +31,14 @@ pl_status layer(pl_dtype dt, bool fma, int n, const void* a, int k, const void* 
 pl_status top(pl_dtype dt, bool fma, int n, const void* a, const void* last, void* out, const int32_t* guard,
               int32_t* status, cudaStream_t st);
 pl_status guard_i64(int n, const void* a, int32_t* guard, cudaStream_t st);
-// Cached layer scratch of the current device (cudaMalloc blocks), handed back
-// to the cache when `st` reaches the point of the call.
+// Cached layer scratch of the current device (cudaMalloc blocks) for work on
+// stream `st`; scratch_put hands it back, ordered after the work on `st`.
 struct ScratchBlock {
     void* ptr = nullptr;
     size_t bytes = 0;
     int dev = 0;
 };
-pl_status scratch_get(size_t bytes, ScratchBlock* out);
+pl_status scratch_get(size_t bytes, cudaStream_t st, ScratchBlock* out);
 pl_status scratch_put(const ScratchBlock& b, cudaStream_t st);
 // The multi-GPU path (multi.cu): limits->num_gpus >= 1, devices NULL = 0..g-1.
 pl_status run_multi(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,

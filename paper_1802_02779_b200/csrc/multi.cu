@@ -248,7 +248,7 @@ pl_status sharded_dp(DeviceGroup& G, pl_dtype dt, int n, const void* a, void* ou
     auto dev_ptr = [&](int g, size_t off) { return static_cast<char*>(blk[g].ptr) + off; };
     for (int g = 0; g < world && s == PL_OK; ++g) {
         PLC_CUDA(cudaSetDevice(G.devs[g]));
-        s = plc::scratch_get(mat_off + ((mat_bytes + 255) & ~size_t(255)), &blk[g]);
+        s = plc::scratch_get(mat_off + ((mat_bytes + 255) & ~size_t(255)), G.streams[g], &blk[g]);
         if (s != PL_OK) break;
         PLC_CUDA(cudaMemsetAsync(blk[g].ptr, 0, kHead, G.streams[g]));
         PLC_CUDA(cudaMemcpyAsync(dev_ptr(g, mat_off), a, mat_bytes, cudaMemcpyDefault, G.streams[g]));
