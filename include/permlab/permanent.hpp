@@ -198,7 +198,7 @@ Algorithm algorithm_from_name(std::string_view name);
 
 struct PermanentResult {
     RingElement value;
-    OpCount counts;  // the Store-zechin counts n*2^(n-1)-n, n*2^(n-1)-2^n+1
+    OpCount counts;  // store-zechin: n*2^(n-1)-n, n*2^(n-1)-2^n+1; ryser: see ryser_counts
     Algorithm algorithm;
 };
 
@@ -224,6 +224,12 @@ struct BatchOptions {
 };
 
 PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limits = {});
+/// Ryser's formula on the device (reference permanent.hpp:84): float rings
+/// bitwise the reference's visit-order fold, Int exact (guarded like
+/// store_zechin_permanent); counts = count_formula(Ryser, n).
+PermanentResult ryser_permanent(const SquareMatrix& a, const Limits& limits = {});
+/// Closed-form Ryser operation counts (reference cost_model.cpp:168-174).
+OpCount ryser_counts(int n);
 StoreZechinRun store_zechin_run(const SquareMatrix& a, const Limits& limits = {});
 AttributionReport store_zechin_attributed(const SquareMatrix& a, const Limits& limits = {});
 

@@ -115,6 +115,26 @@ pl_status pl_sz_counts(int32_t n, uint64_t* multiplications, uint64_t* additions
  * cache_misses = distinct_subsets = 2^n - n - 2 for n >= 3, 1 for n = 2, 0 for n = 1. */
 pl_status pl_sz_diagnostics(int32_t n, uint64_t* cache_misses, uint64_t* distinct_subsets);
 
+/* ---- Ryser engine (reference permanent.hpp:84, permanent.cpp:85-136) -----
+ * permlab::ryser_permanent: inclusion-exclusion over the nonempty column
+ * subsets, visited in the reference's depth-first (lexicographic preorder)
+ * order. Float rings (PL_F64, PL_C128) reproduce the reference's rounding
+ * sequence bit for bit: every row sum is the ascending left fold of its
+ * columns, every product the left fold of the row sums, and the total the
+ * left fold of the signed products in visit order (a sequential device
+ * fold). PL_I64 is exact (wrapping 128-bit arithmetic, exact whenever
+ * prod_i max(1, sum_j |a_ij|) < 2^126 and the permanent fits int64, else
+ * PL_ERR_OVERFLOW). Synchronous;
+ * host pointers, or device pointers with PL_FLAG_DEVICE_PTRS. PL_FLAG_FMA is
+ * ignored (the engine has no multiply-add). Orders are limited as for
+ * store-zechin (subset_order_limit, PL_MAX_ORDER). */
+pl_status pl_ryser_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, uint32_t flags,
+                             const pl_limits* limits, void* stream);
+/* Operation counts of Ryser (reference count_formula, cost_model.cpp:168-174,
+ * equal to its instrumented counts): (2^n - 1)(n - 1) multiplications and
+ * (2^n - n)(n + 1) - 2 additions (n >= 2; n = 1 -> (0, 0)). */
+pl_status pl_ryser_counts(int32_t n, uint64_t* multiplications, uint64_t* additions);
+
 /* ---- layer primitives (sharded multi-GPU driver, tests) -------------------
  * Layer k (2 <= k <= n-1) holds per(S) for every k-subset S of the columns
  * over the leading k rows, stored at its colex rank

@@ -51,6 +51,9 @@ def lib():
         L.orc_sz_batch_f64.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int]
         L.orc_sz_batch_c128.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int]
         L.orc_sz_layer_f64.argtypes = [C.c_int, _dp, C.c_int, _dp]
+        L.orc_ryser_f64.argtypes = [C.c_int, _dp, _dp]
+        L.orc_ryser_c128.argtypes = [C.c_int, _dp, _dp]
+        L.orc_ryser_i64.argtypes = [C.c_int, _i64p, _i64p, _i64p]
         L.orc_binom.argtypes = [C.c_int, C.c_int]
         L.orc_binom.restype = C.c_uint64
         L.orc_colex_rank.argtypes = [C.c_uint64]
@@ -169,6 +172,34 @@ def sz_batch(a: np.ndarray, nthreads: int | None = None) -> np.ndarray:
     if rc != 0:
         raise OracleError(f"oracle batch status {rc}")
     return out
+
+
+def ryser(a: np.ndarray):
+    """Restated reference Ryser (visit-order fold, sz_oracle.c): int / float / complex."""
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    if a.dtype == np.int64:
+        lo, hi = C.c_int64(), C.c_int64()
+        if lib().orc_ryser_i64(n, _ptr(a, _i64p), C.byref(lo), C.byref(hi)):
+            raise OracleError("128-bit overflow")
+        return _lohi_to_int(lo.value, hi.value)
+    if a.dtype == np.float64:
+        out = np.zeros(1)
+        lib().orc_ryser_f64(n, _ptr(a, _dp), _ptr(out, _dp))
+        return float(out[0])
+    out = np.zeros(2)
+    lib().orc_ryser_c128(n, _ptr(a.view(np.float64), _dp), _ptr(out, _dp))
+    return complex(out[0], out[1])
+
+
+def ref_ryser_c128(a: np.ndarray) -> complex:
+    """The reference engine's ryser_permanent on a complex (or real) matrix."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+    out = np.zeros(2)
+    rc = ref().ref_ryser_c128(a.shape[0], _ptr(a.view(np.float64), _dp), _ptr(out, _dp))
+    if rc:
+        raise _ref_err(rc)
+    return complex(out[0], out[1])
 
 
 def sz_layer_f64(a: np.ndarray, k: int) -> np.ndarray:

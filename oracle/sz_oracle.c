@@ -426,3 +426,105 @@ int orc_sz_top_c128(int n, const double* a, const double* last, double* out) {
     out[1] = total.im;
     return 0;
 }
+
+/* ---------------------------------------------------------------- Ryser
+ * Restatement of the reference's RyserEval (proj/src/permanent.cpp:85-136):
+ * depth-first over the nonempty column subsets, a subset extended only by
+ * columns above its maximum; the row sums carried down (child = parent +
+ * a[:, j], :125-128), the product a left fold over rows (:112-116), the total
+ * a left fold in visit order, minus for odd subset sizes (:117-122), negated
+ * at the end for odd n (:103-105). Integers in checked 128-bit arithmetic. */
+typedef struct {
+    int n;
+    const double* a;  /* complex (re, im) pairs, or reals with stride 1 */
+    int cplx;
+    double* sums;     /* (n + 1) levels x n entries (x2 for complex) */
+    double tot_re, tot_im;
+    int have;
+} ryser_state;
+
+static void ryser_visit(ryser_state* st, int max_col, int size) {
+    const int n = st->n, w = st->cplx ? 2 : 1;
+    const double* s = st->sums + (size_t)size * n * w;
+    double pr = s[0], pi = st->cplx ? s[1] : 0.0;
+    for (int i = 1; i < n; ++i) {
+        if (st->cplx) {
+            const double br = s[2 * i], bi = s[2 * i + 1];
+            const double r = pr * br - pi * bi, im = pr * bi + pi * br;
+            pr = r;
+            pi = im;
+        } else {
+            pr = pr * s[i];
+        }
+    }
+    const int odd = size & 1;
+    if (!st->have) {
+        st->tot_re = odd ? -pr : pr;
+        st->tot_im = odd ? -pi : pi;
+        st->have = 1;
+    } else if (odd) {
+        st->tot_re = st->tot_re - pr;
+        st->tot_im = st->tot_im - pi;
+    } else {
+        st->tot_re = st->tot_re + pr;
+        st->tot_im = st->tot_im + pi;
+    }
+    for (int j = max_col + 1; j < n; ++j) {
+        double* nx = st->sums + (size_t)(size + 1) * n * w;
+        for (int i = 0; i < n; ++i) {
+            if (st->cplx) {
+                nx[2 * i] = s[2 * i] + st->a[2 * ((size_t)i * n + j)];
+                nx[2 * i + 1] = s[2 * i + 1] + st->a[2 * ((size_t)i * n + j) + 1];
+            } else {
+                nx[i] = s[i] + st->a[(size_t)i * n + j];
+            }
+        }
+        ryser_visit(st, j, size + 1);
+    }
+}
+
+static int ryser_float(int n, const double* a, int cplx, double* out) {
+    const int w = cplx ? 2 : 1;
+    ryser_state st = {n, a, cplx, calloc((size_t)(n + 1) * n * w, sizeof(double)), 0.0, 0.0, 0};
+    if (!st.sums) return 2;
+    for (int j = 0; j < n; ++j) {
+        double* lv = st.sums + (size_t)1 * n * w;
+        for (int i = 0; i < n; ++i) {
+            if (cplx) {
+                lv[2 * i] = a[2 * ((size_t)i * n + j)];
+                lv[2 * i + 1] = a[2 * ((size_t)i * n + j) + 1];
+            } else {
+                lv[i] = a[(size_t)i * n + j];
+            }
+        }
+        ryser_visit(&st, j, 1);
+    }
+    free(st.sums);
+    out[0] = (n & 1) ? -st.tot_re : st.tot_re;
+    if (cplx) out[1] = (n & 1) ? -st.tot_im : st.tot_im;
+    return 0;
+}
+
+int orc_ryser_f64(int n, const double* a, double* out) { return ryser_float(n, a, 0, out); }
+int orc_ryser_c128(int n, const double* a, double* out) { return ryser_float(n, a, 1, out); }
+
+/* Integers: the same sum in checked 128-bit arithmetic (the subset order is
+ * irrelevant for exact integers). */
+int orc_ryser_i64(int n, const int64_t* a, int64_t* out_lo, int64_t* out_hi) {
+    i128 total = 0;
+    for (uint64_t S = 1; S < (1ull << n); ++S) {
+        i128 prod = 1;
+        for (int i = 0; i < n; ++i) {
+            i128 s = 0;
+            for (int j = 0; j < n; ++j)
+                if ((S >> j) & 1) s += a[(size_t)i * n + j];
+            if (__builtin_mul_overflow(prod, s, &prod)) return 1;
+        }
+        if (__builtin_popcountll(S) & 1) prod = -prod;
+        if (__builtin_add_overflow(total, prod, &total)) return 1;
+    }
+    if (n & 1) total = -total;
+    *out_lo = (int64_t)(uint64_t)total;
+    *out_hi = (int64_t)(total >> 64);
+    return 0;
+}

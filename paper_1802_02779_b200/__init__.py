@@ -14,6 +14,8 @@ from .api import (  # noqa: F401
     colex_unrank,
     device_count,
     release_scratch,
+    ryser_counts,
+    ryser_permanent,
     scratch_bytes,
     store_zechin_attributed,
     store_zechin_counts,

@@ -62,6 +62,8 @@ EXPORTED_SYMBOLS = (
     "pl_boson_unrank_pattern",
     "pl_boson_probabilities",
     "pl_boson_distribution",
+    "pl_ryser_permanent",
+    "pl_ryser_counts",
 )
 
 
@@ -122,6 +124,10 @@ def _load():
     L.pl_boson_probabilities.restype = C.c_int
     L.pl_boson_distribution.argtypes = [i32, vp, i32, vp, u64, i64, vp, u32, vp]
     L.pl_boson_distribution.restype = C.c_int
+    L.pl_ryser_permanent.argtypes = [C.c_int, i32, vp, vp, u32, C.POINTER(pl_limits), vp]
+    L.pl_ryser_permanent.restype = C.c_int
+    L.pl_ryser_counts.argtypes = [i32, C.POINTER(u64), C.POINTER(u64)]
+    L.pl_ryser_counts.restype = C.c_int
     return L
 
 

@@ -161,6 +161,25 @@ def store_zechin_permanent(a, limits: Optional[Limits] = None, fma: bool = False
     return PermanentResult(_py_value(out), store_zechin_counts(n))
 
 
+def ryser_counts(n: int) -> OpCount:
+    """Ryser operation counts (reference ``cost_model.cpp:168-174``)."""
+    m, a = C.c_uint64(), C.c_uint64()
+    _check(N.lib.pl_ryser_counts(int(n), C.byref(m), C.byref(a)))
+    return OpCount(m.value, a.value)
+
+
+def ryser_permanent(a, limits: Optional[Limits] = None) -> PermanentResult:
+    """Permanent by Ryser's formula on the device (reference ``permanent.hpp:84``,
+    ``permanent.cpp:85-136``): float rings bitwise the reference's visit-order
+    fold, int64 exact (guarded)."""
+    m = _as_matrix(a)
+    n = m.shape[0]
+    lim = (limits or Limits()).to_c()
+    out = np.zeros(1, dtype=m.dtype)
+    _check(N.lib.pl_ryser_permanent(_DTYPES[m.dtype], n, m.ctypes.data, out.ctypes.data, 0, C.byref(lim), None))
+    return PermanentResult(_py_value(out), ryser_counts(n), "ryser")
+
+
 def store_zechin_attributed(a, limits: Optional[Limits] = None) -> AttributionReport:
     """Per-term cost split of the reference's DFS order (``permanent.cpp:179-199``),
     in closed form: term j first demands the subsets T of full\\{j} that

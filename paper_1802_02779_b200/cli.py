@@ -2,7 +2,7 @@
 Store-zechin and boson-sampling subcommands with the same arguments, output
 formats and exit codes (reference ``proj/tools/permlab_cli.cpp``).
 
-    python -m paper_1802_02779_b200.cli perm --matrix FILE --algorithm store-zechin [--ring int|complex] [--format text|json]
+    python -m paper_1802_02779_b200.cli perm --matrix FILE --algorithm store-zechin|ryser [--ring int|complex] [--format text|json]
     python -m paper_1802_02779_b200.cli bs-dist --unitary FILE --input 1,2,3 [--format text|csv|json]
     python -m paper_1802_02779_b200.cli bs-sample --unitary FILE --input 1,2 --count N --seed S [--format text|json]
     python -m paper_1802_02779_b200.cli randu --modes M --seed S --out FILE
@@ -384,17 +384,18 @@ def run_perm(opt) -> str:
     m = load_matrix(opt.matrix, opt.ring)
     if opt.algorithm not in ("naive", "ryser", "store-zechin"):
         raise DomainError("unknown algorithm: " + opt.algorithm)
-    if opt.algorithm != "store-zechin":
-        raise DomainError(f"the {opt.algorithm} engine is not offered by the device engine (store-zechin only)")
-    r = api.store_zechin_permanent(m, opt.limits)
+    if opt.algorithm == "naive":
+        raise DomainError("the naive engine is not offered by the device engine (store-zechin and ryser only)")
+    run = api.ryser_permanent if opt.algorithm == "ryser" else api.store_zechin_permanent
+    r = run(m, opt.limits)
     n = m.shape[0]
     if opt.format == "json":
         v = r.value
         vj = int(v) if isinstance(v, (int, np.integer)) else [complex(v).real, complex(v).imag]
-        return json_dump({"algorithm": "store-zechin", "order": n, "value": vj,
+        return json_dump({"algorithm": opt.algorithm, "order": n, "value": vj,
                           "counts": {"multiplications": r.counts.multiplications,
                                      "additions": r.counts.additions}}, 2) + "\n"
-    return ("algorithm: store-zechin\n" + "value: " + value_text(r.value) + "\n" +
+    return ("algorithm: " + opt.algorithm + "\n" + "value: " + value_text(r.value) + "\n" +
             "multiplications: %d\n" % r.counts.multiplications + "additions: %d\n" % r.counts.additions)
 
 

@@ -226,6 +226,42 @@ PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limi
     return r;
 }
 
+OpCount ryser_counts(int n) {
+    OpCount c;
+    check(pl_ryser_counts(n, &c.multiplications, &c.additions));
+    return c;
+}
+
+PermanentResult ryser_permanent(const SquareMatrix& a, const Limits& limits) {
+    const pl_limits lim = to_c(limits);
+    PermanentResult r;
+    r.algorithm = Algorithm::Ryser;
+    r.counts = ryser_counts(a.order());
+    switch (a.ring()) {
+        case RingTag::Int: {
+            Int v = 0;
+            check(pl_ryser_permanent(PL_I64, a.order(), a.data(), &v, 0, &lim, nullptr));
+            r.value = v;
+            break;
+        }
+        case RingTag::Real: {
+            Real v = 0;
+            check(pl_ryser_permanent(PL_F64, a.order(), a.data(), &v, 0, &lim, nullptr));
+            r.value = v;
+            break;
+        }
+        case RingTag::Rational:
+            throw DomainError("the rational ring has no device arithmetic (use int, real or complex)");
+        case RingTag::Complex: {
+            Cplx v;
+            check(pl_ryser_permanent(PL_C128, a.order(), a.data(), &v, 0, &lim, nullptr));
+            r.value = v;
+            break;
+        }
+    }
+    return r;
+}
+
 // Closed form of the reference's per-term attribution (permanent.cpp:179-199):
 // term j first demands exactly the subsets T of full \ {j} with
 // {0..j-1} subset of T and 2 <= |T| <= n-1 (everything missing one of

@@ -198,6 +198,17 @@ void device_goldens() {
     CHECK((r5.counts == OpCount{75, 49}));
     const auto one = store_zechin_permanent(SquareMatrix(int_matrix(1, {42})));
     CHECK(value_of(one) == 42);
+    // the Ryser engine on the same goldens (reference permanent.hpp:84), with
+    // the reference's counts (tests/acceptance.cpp:72)
+    const auto ry4 = ryser_permanent(SquareMatrix(kDev4));
+    CHECK(value_of(ry4) == 9722);
+    CHECK((ry4.counts == OpCount{45, 58}));
+    CHECK(ry4.algorithm == Algorithm::Ryser);
+    const auto ry5 = ryser_permanent(a5);
+    CHECK(value_of(ry5) == 988);
+    CHECK((ry5.counts == OpCount{124, 160}));
+    CHECK(value_of(ryser_permanent(SquareMatrix(int_matrix(1, {42})))) == 42);
+    CHECK_THROWS_AS(ryser_permanent(SquareMatrix(Matrix<Int>::filled(21, 1))), DomainError);
     CHECK((one.counts == OpCount{0, 0}));
     const auto two = store_zechin_permanent(SquareMatrix(int_matrix(2, {2, 3, 5, 7})));
     CHECK(value_of(two) == 29);

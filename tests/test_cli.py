@@ -132,4 +132,4 @@ def test_usage_errors_exit_1_and_domain_errors_exit_2(tmp_path):
     assert r.returncode == 2 and r.stderr.startswith("error: cannot read file:") and r.stdout == ""
     r = subprocess.run([sys.executable, "-m", "paper_1802_02779_b200.cli", "perm", "--matrix",
                         str(FIX / "dev4.json"), "--algorithm", "naive"], capture_output=True, text=True, cwd=ROOT)
-    assert r.returncode == 2 and "store-zechin only" in r.stderr
+    assert r.returncode == 2 and "store-zechin and ryser only" in r.stderr

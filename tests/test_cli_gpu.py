@@ -64,3 +64,16 @@ def test_boson_workflow_matches_reference(tmp_path):
     assert run("bs-sample", "--unitary", str(f), "--input", "1,3,4", "--count", "50", "--seed", "9", "--format",
                "json") == gold("sample_u6_134_50_9.json")
     assert run("bs-sample", "--unitary", str(f), "--input", "1,2", "--count", "0", "--seed", "1") == ""
+
+
+def test_perm_ryser(tmp_path):
+    # reference tests/test_cli.cpp:114-121: `perm --algorithm ryser --format json` on I3
+    id3 = tmp_path / "id3.csv"
+    id3.write_text("1,0,0\n0,1,0\n0,0,1\n")
+    import json
+
+    js = json.loads(run("perm", "--matrix", str(id3), "--algorithm", "ryser", "--format", "json"))
+    assert js["value"] == 1 and js["algorithm"] == "ryser"
+    assert js["counts"] == {"multiplications": 14, "additions": 18}
+    out = run("perm", "--matrix", str(FIX / "dev4.json"), "--algorithm", "ryser")
+    assert out == "algorithm: ryser\nvalue: 9722\nmultiplications: 45\nadditions: 58\n"

@@ -49,6 +49,17 @@ def test_counts_and_diagnostics():
         assert (c.multiplications, c.additions) == (n * 2 ** (n - 1) - n, n * 2 ** (n - 1) - 2 ** n + 1)
 
 
+def test_ryser_counts_match_reference_tables():
+    # reference tests/test_cost_model.cpp:28 and tests/acceptance.cpp:72
+    # (count_formula == the instrumented engine's counts, acceptance.cpp:236)
+    assert pl.ryser_counts(3) == pl.OpCount(14, 18)
+    assert pl.ryser_counts(4) == pl.OpCount(45, 58)
+    assert pl.ryser_counts(5) == pl.OpCount(124, 160)
+    assert pl.ryser_counts(1) == pl.OpCount(0, 0)
+    for n in range(2, 30):
+        assert pl.ryser_counts(n) == pl.OpCount((2**n - 1) * (n - 1), (2**n - n) * (n + 1) - 2)
+
+
 def test_binomials_and_colex():
     for s in range(0, 40):
         for k in range(0, s + 1):
@@ -118,6 +129,10 @@ def test_domain_errors_before_device_work():
         pl.store_zechin_permanent(np.ones((2, 2), dtype=object))
     with pytest.raises(pl.DomainError):
         pl.store_zechin_permanent_batch(np.ones((3, 4, 4), dtype=np.float32))
+    with pytest.raises(pl.DomainError, match="subset_order_limit"):
+        pl.ryser_permanent(a5, pl.Limits(subset_order_limit=4))
+    with pytest.raises(pl.DomainError):
+        pl.ryser_permanent(np.ones((35, 35), dtype=np.int64))
 
 
 def test_no_cpu_fallback_without_device():
@@ -127,6 +142,8 @@ def test_no_cpu_fallback_without_device():
         pl.store_zechin_permanent(np.eye(3))
     with pytest.raises(pl.DeviceError, match="NODEVICE"):
         pl.store_zechin_permanent_batch(np.ones((4, 5, 5), dtype=np.int64))
+    with pytest.raises(pl.DeviceError, match="NODEVICE"):
+        pl.ryser_permanent(np.eye(3))
 
 
 def test_cpp_host_suite():

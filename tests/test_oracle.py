@@ -111,3 +111,27 @@ def test_oracle_against_committed_fixtures(goldens):
     a = configs.c4()
     assert configs.sha256(a) == g["input_sha256"]
     assert hexf(O.sz_f64(a)) == g["value_hex"] == g["reference_value_hex"]
+
+
+# ---------------------------------------------------------------- Ryser
+
+def test_ryser_restatement_goldens():
+    # reference tests/test_permanent.cpp: the Ryser engine agrees with the
+    # others on the golden matrices
+    assert O.ryser(np.array([[1, 2], [3, 4]], dtype=np.int64)) == 10
+    assert O.ryser(np.arange(1, 10, dtype=np.int64).reshape(3, 3)) == 450
+    assert O.ryser(DEV4.astype(np.int64)) == 9722
+    assert O.ryser(A5.astype(np.int64)) == 988
+    assert O.ryser(np.array([[42]], dtype=np.int64)) == 42
+
+
+@need_ref
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 14])
+def test_ryser_restatement_bitwise_equals_reference(n):
+    rng = np.random.default_rng(100 + n)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    assert O.ryser(a) == O.ref_ryser_c128(a)
+    r = rng.uniform(-1, 1, (n, n))
+    assert hexf(O.ryser(r)) == hexf(O.ref_ryser_c128(r.astype(np.complex128)).real)
+    i = rng.integers(-9, 10, (n, n)).astype(np.int64)
+    assert O.ryser(i) == O.ref_ryser_int(i) == O.sz_int(i)
