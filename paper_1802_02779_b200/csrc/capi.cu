@@ -17,6 +17,7 @@
 
 #include <map>
 #include <vector>
+#include <type_traits>
 
 #include "../../include/permlab_b200.h"
 #include "sz_kernels.cuh"
@@ -465,6 +466,35 @@ pl_status launch_pack_n(const void* a, void* out, int64_t count, int32_t* status
     return PL_OK;
 }
 
+// int64, 10 <= n <= 14: the FP32-exact four-matrix pack kernel (PL_BATCH_F32=0: the
+// double pack kernel).
+bool use_f32_pack() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_BATCH_F32");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int N, int P>
+pl_status launch_f32_pack_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st,
+                            const Ptab& pt) {
+    const int maxc = (int)max_layer(N);
+    const size_t smem = (size_t)(N * N + 2 * maxc) * 4 * P + 64;  // 4P-byte packs (the single layout fits inside)
+    auto kern = pl::sz_batch_f32_pack_kernel<N, P>;
+    PL_CUDA(set_smem_once(kern, smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kF32Threads, smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t packs = (count + P - 1) / P;
+    const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, pl::kF32Threads, smem, st>>>(static_cast<const long long*>(a),
+                                                         static_cast<long long*>(out), count, maxc, pt.tab,
+                                                               pt.off, pt.t32(8), pt.t32(4 * P), status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
 // Warp-per-matrix kernel for 8-byte rings, 6 <= n <= 9 (PL_BATCH_SMEM=cta forces the CTA
 // kernel). Measured (profiles/c3_ab.py): n = 8 x 50k int64 104 -> 74 us; equal at n = 10;
 // slower at n = 12 (C3: 205 -> 293 us), where a matrix's layers take ~16 KB and a warp per
@@ -509,6 +539,29 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
         return launch_warp_n<R, NN>(a, out, count, status, st, pt);
                 PL_WARP_N(6) PL_WARP_N(7) PL_WARP_N(8) PL_WARP_N(9)
 #undef PL_WARP_N
+            }
+        }
+        if constexpr (std::is_same_v<R, pl::RI64<true>>) {
+            if (n >= 10 && n <= 14 && count >= 4 && use_f32_pack()) {
+                static const int p8 = [] {
+                    const char* e = std::getenv("PL_BATCH_F32_P");  // 8: eight-matrix packs (n <= 13)
+                    return e && atoi(e) == 8;
+                }();
+                if (p8 && n <= 13) {
+                    switch (n) {
+                        case 10: return launch_f32_pack_n<10, 8>(a, out, count, status, st, pt);
+                        case 11: return launch_f32_pack_n<11, 8>(a, out, count, status, st, pt);
+                        case 12: return launch_f32_pack_n<12, 8>(a, out, count, status, st, pt);
+                        case 13: return launch_f32_pack_n<13, 8>(a, out, count, status, st, pt);
+                    }
+                }
+                switch (n) {
+                    case 10: return launch_f32_pack_n<10, 4>(a, out, count, status, st, pt);
+                    case 11: return launch_f32_pack_n<11, 4>(a, out, count, status, st, pt);
+                    case 12: return launch_f32_pack_n<12, 4>(a, out, count, status, st, pt);
+                    case 13: return launch_f32_pack_n<13, 4>(a, out, count, status, st, pt);
+                    case 14: return launch_f32_pack_n<14, 4>(a, out, count, status, st, pt);
+                }
             }
         }
         const int P = n >= 10 && n <= 14 ? pack_width(n) : 1;

@@ -471,6 +471,54 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
     }
 }
 
+// Exact integer arithmetic on the FP32 pipe: every operand, product and
+// partial sum of a matrix whose bound (below) is under 2^24 is an integer
+// that a float holds exactly, so each rounded operation is exact.
+struct RF32X {
+    using T = float;
+    static constexpr bool kChecked = false;
+    __device__ __forceinline__ static T mul(T a, T b, bool&) { return __fmul_rn(a, b); }
+    __device__ __forceinline__ static T add(T a, T b, bool&) { return __fadd_rn(a, b); }
+    __device__ __forceinline__ static T mac(T acc, T a, T b, bool&) { return __fmaf_rn(a, b, acc); }
+    __device__ __forceinline__ static T zero() { return 0.0f; }
+};
+
+// int64 exact-path choice including the FP32 path: 3 when every sub-permanent
+// and partial sum is provably below 2^24 -- by the row-sum bound
+// prod_i max(1, sum_j |a_ij|), or for 0/1 matrices by Bregman's bound
+// prod_i (r_i!)^(1/r_i) (r_i the row sums; sub-matrices of a 0/1 matrix are
+// 0/1 with smaller row sums and (r!)^(1/r) grows with r, and with
+// nonnegative entries every partial sum is at most its sub-permanent) --
+// else the warp_i64_mode choice.
+template <int N>
+__device__ __forceinline__ int warp_i64_mode_f32(const long long* m) {
+    const int lane = threadIdx.x & 31;
+    bool zero_one = true;
+    double rd = 0.0, lg = 0.0;
+    if (lane < N) {
+        const long long* row = m + lane * N;
+        long long r01 = 0;
+        for (int j = 0; j < N; ++j) {
+            const long long v = row[j];
+            zero_one &= v == 0 || v == 1;
+            r01 += v;
+            rd += v < 0 ? -(double)v : (double)v;
+        }
+        if (zero_one && r01 > 0) lg = lgamma((double)r01 + 1.0) / (double)r01;  // log (r!)^(1/r)
+    }
+    zero_one = __all_sync(0xffffffffu, zero_one);
+    double pd = 1.0, lsum = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double d = __shfl_sync(0xffffffffu, rd, i);
+        pd *= d < 1.0 ? 1.0 : d;
+        lsum += __shfl_sync(0xffffffffu, lg, i);
+    }
+    const double kLim = 16777216.0 * (1.0 - 1e-9);  // 2^24, margin for the bound's own rounding
+    if (pd < kLim || (zero_one && exp(lsum) < kLim)) return 3;
+    return warp_i64_mode<N>(m);
+}
+
 // P matrices evaluated in lockstep (8-byte rings): every value is a pack
 // {matrix 0, ..., matrix P-1} of P * 8 bytes, so each term is one table load,
 // two P * 8-byte shared loads and P products -- the predecessor table and the
@@ -478,7 +526,7 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
 // order, so each member is bitwise what the single-matrix DP computes.
 template <class RR, int P>
 struct PackRing {
-    struct __align__(8 * P) T {
+    struct __align__(sizeof(typename RR::T) * P) T {
         typename RR::T v[P];
     };
     static constexpr bool kChecked = RR::kChecked;
@@ -629,6 +677,104 @@ __global__ void __launch_bounds__(pack_threads<N>()) sz_batch_smem_pack_kernel(
                     if ((flag & 1) || ov) {
                         atomicOr(status, 1);
                         total = R::zero();
+                    }
+                    out[b0 + h] = total;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// int64 batches, 10 <= n <= 14: four matrices per CTA in lockstep on the FP32
+// pipe when all four are FP32-exact (warp_i64_mode_f32 == 3): a pack is 16
+// bytes (the same byte offsets as a pair of doubles), so a term is one table
+// load, two 16-byte shared loads and four FFMAs, and twice the matrices of the
+// double pack share an SM. Other packs run their members one at a time on the
+// double / int64 exact paths (as sz_batch_smem_pack_kernel's fallback).
+#ifndef PL_F32_THREADS
+#define PL_F32_THREADS 256
+#endif
+constexpr int kF32Threads = PL_F32_THREADS;  // threads per four-matrix pack CTA
+
+template <int N, int P>
+__global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
+    const long long* __restrict__ a, long long* __restrict__ out, int64_t count, int maxc,
+    const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
+    const uint32_t* __restrict__ ptab32_16, int32_t* __restrict__ status) {
+    constexpr int n = N, E = N * N;
+    using PR = PackRing<RF32X, P>;
+    using PT = typename PR::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int mode[P], flag;
+    const int tid = threadIdx.x;
+    const int64_t npacks = (count + P - 1) / P;
+    for (int64_t pb = blockIdx.x; pb < npacks; pb += gridDim.x) {
+        const int64_t b0 = P * pb;
+        const int have = count - b0 < P ? (int)(count - b0) : P;
+        const long long* g = a + b0 * E;
+        for (int w = tid >> 5; w < have; w += (int)(blockDim.x >> 5)) {  // one warp per member's guard
+            const int md = warp_i64_mode_f32<N>(g + (size_t)w * E);
+            if ((tid & 31) == 0) mode[w] = md;
+        }
+        __syncthreads();
+        bool joint = have == P;
+#pragma unroll
+        for (int i = 0; i < P; ++i) joint &= i >= have || mode[i] == 3;
+        if (joint) {
+            PT* mat = reinterpret_cast<PT*>(smem_raw);
+            PT* buf0 = mat + E;
+            PT* buf1 = buf0 + maxc;
+            for (int e = tid; e < E; e += blockDim.x) {
+                PT x;
+#pragma unroll
+                for (int i = 0; i < P; ++i) x.v[i] = (float)g[(size_t)i * E + e];
+                mat[e] = x;
+            }
+            __syncthreads();
+            bool ov = false;
+            const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);  // 4P-byte offsets
+            if (tid == 0) {
+                const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
+#pragma unroll
+                for (int i = 0; i < P; ++i) out[b0 + i] = (long long)t.v[i];
+            }
+        } else {
+            for (int h = 0; h < have; ++h) {
+                const long long* gh = g + (size_t)h * E;
+                long long* mat = reinterpret_cast<long long*>(smem_raw);
+                long long* buf0 = mat + ((E + 1) & ~1);
+                long long* buf1 = buf0 + ((maxc + 1) & ~1);
+                for (int e = tid; e < E; e += blockDim.x) mat[e] = gh[e];
+                if (tid == 0) flag = 0;
+                __syncthreads();
+                bool ov = false;
+                long long total = 0;
+                const int md = mode[h];
+                if (md == 0 || md == 3) {
+                    double* dm = reinterpret_cast<double*>(mat);
+                    for (int e = tid; e < E; e += blockDim.x) dm[e] = (double)mat[e];
+                    __syncthreads();
+                    const double* last = smem_dp<RF64<true>, double, N>(dm, reinterpret_cast<double*>(buf0),
+                                                                         reinterpret_cast<double*>(buf1), n, ptab,
+                                                                         poff, ptab32_8, ov);
+                    if (tid == 0) total = (long long)smem_top<RF64<true>, double, N>(dm, last, n, ov);
+                } else if (md == 1) {
+                    const long long* last = smem_dp<RI64<false>, long long, N>(mat, buf0, buf1, n, ptab, poff,
+                                                                               ptab32_8, ov);
+                    if (tid == 0) total = smem_top<RI64<false>, long long, N>(mat, last, n, ov);
+                } else {
+                    const long long* last = smem_dp<RI64<true>, long long, N>(mat, buf0, buf1, n, ptab, poff,
+                                                                              ptab32_8, ov);
+                    if (ov) atomicOr(&flag, 1);
+                    __syncthreads();
+                    if (tid == 0 && !(flag & 1)) total = smem_top<RI64<true>, long long, N>(mat, last, n, ov);
+                }
+                if (tid == 0) {
+                    if ((flag & 1) || ov) {
+                        atomicOr(status, 1);
+                        total = 0;
                     }
                     out[b0 + h] = total;
                 }

@@ -428,3 +428,19 @@ def test_pair_kernel_mixed_modes_and_odd_counts(n):
     assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
     f = configs.uniform((17, n, n), seed=7000 + n)
     assert np.array_equal(pl.store_zechin_permanent_batch(f).view(np.uint64), O.sz_batch(f).view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [10, 11, 12, 13, 14])
+def test_f32_pack_kernel_paths(n):
+    # int64 10 <= n <= 14: packs of four run on the FP32 pipe when every member's
+    # bound (row sums, or Bregman's for 0/1 matrices) is below 2^24; mix in
+    # all-ones (Bregman 12! > 2^24 at n >= 11: the double path), 0/1 matrices with
+    # one entry 2 (not 0/1, row-sum bound over 2^24) and a count that leaves a
+    # partial pack
+    count = 4 * 9 + 3
+    a = configs.int_matrices(n, count, seed=8100 + n, lo=0, hi=1)
+    a[5] = 1
+    a[9, 3, 4] = 2
+    a[22] = np.eye(n, dtype=np.int64) * 3
+    want = O.sz_batch(a)
+    assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
