@@ -288,6 +288,29 @@ bool use_pipe_kernel(size_t in_bytes) {
     return force >= 0 ? force == 1 : in_bytes >= (size_t(64) << 20);
 }
 
+// Launch with programmatic stream serialisation (the batch kernels wait for
+// the previous grid with griddepcontrol.wait before touching memory, so a
+// back-to-back stream of batches overlaps launch and ramp with the previous
+// tail). PL_BATCH_PDL=0 launches plainly.
+template <class K, class... Args>
+cudaError_t launch_pdl(K kern, unsigned grid, unsigned threads, size_t smem, cudaStream_t st, Args... args) {
+    static const bool pdl = [] {
+        const char* e = std::getenv("PL_BATCH_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <class R, int N>
 pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st) {
     using T = typename R::T;
@@ -297,9 +320,8 @@ pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status
         PL_CUDA(set_smem_once(kern, Pg::kSmem));
         const int64_t nfull = count / 32;
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(nfull, num_sms()));
-        kern<<<(unsigned)blocks, Pg::kThreads, Pg::kSmem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count,
-                                                              status);
-        PL_CUDA(cudaGetLastError());
+        PL_CUDA(launch_pdl(kern, (unsigned)blocks, Pg::kThreads, Pg::kSmem, st, static_cast<const T*>(a),
+                           static_cast<T*>(out), count, status));
         return PL_OK;
     }
     using Gm = pl::BatchGeom<T, N>;
@@ -316,9 +338,8 @@ pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status
     }();
     const int64_t batches = (count + Gm::kBatch - 1) / Gm::kBatch;
     const int64_t blocks = std::min<int64_t>((batches + Gm::kWarps - 1) / Gm::kWarps, (int64_t)num_sms() * per_sm);
-    kern<<<(unsigned)blocks, Gm::kThreads, Gm::kSmem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count,
-                                                            status);
-    PL_CUDA(cudaGetLastError());
+    PL_CUDA(launch_pdl(kern, (unsigned)blocks, Gm::kThreads, Gm::kSmem, st, static_cast<const T*>(a),
+                       static_cast<T*>(out), count, status));
     return PL_OK;
 }
 
@@ -859,9 +880,12 @@ struct Unchecked<pl::RI64<true>> {
 
 // `tickets`: a device word that is zero when this launch starts (the layer
 // kernel's tile counter; unused for k = 2).
+// `nmat` > 1 (lean kernel only): the same layer of nmat matrices (contiguous
+// from `a`, their buffers lstride elements apart; guard[b] per matrix).
 template <class R>
 pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur, uint64_t r0, uint64_t r1,
-                       uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st) {
+                       uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st, uint32_t nmat = 1,
+                       uint64_t lstride = 0) {
     using T = typename R::T;
     if (r1 <= r0) return PL_OK;
     if (k == 2) {
@@ -871,7 +895,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         PL_CUDA(cudaGetLastError());
         return PL_OK;
     }
-    if (use_lean_layer(sizeof(T), n, k)) {
+    if (nmat > 1 || use_lean_layer(sizeof(T), n, k)) {
         const int D = lean_window(n);
         LtabCompact lt;
         pl_status s = get_ltab_compact(D, &lt);
@@ -890,7 +914,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         const int per_sm = blocks_per_sm(kern, threads, smem);
         constexpr int wpb = pl::LnGeom<(int)sizeof(T)>::WPB;
         const unsigned grid = (unsigned)std::max<uint64_t>(
-            1, std::min<uint64_t>((tk.ntiles + wpb - 1) / wpb, (uint64_t)num_sms() * per_sm));
+            1, std::min<uint64_t>(((uint64_t)tk.ntiles * nmat + wpb - 1) / wpb, (uint64_t)num_sms() * per_sm));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(threads);
@@ -906,7 +930,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         cfg.attrs = attr;
         cfg.numAttrs = pdl_l ? 1 : 0;
         PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
-                                   static_cast<T*>(cur), r0, r1, flist + tk.rank0, tk.ntiles,
+                                   static_cast<T*>(cur), r0, r1, flist + tk.rank0, tk.ntiles, nmat, lstride,
                                    static_cast<const uint4*>(lt.ltab), static_cast<const uint32_t*>(lt.offs),
                                    static_cast<const uint2*>(qb.binom_pairs), guard, status));
         return PL_OK;
@@ -998,6 +1022,74 @@ pl_status run_layers(int n, const void* a_dev, void* out_dev, void* buf0, void* 
     return launch_top<R>(n, a_dev, prev, out_dev, guard, status, st);
 }
 
+// Batches of large orders whose layers all fit the lean kernel (n <= ~22):
+// every layer of a group of matrices in one launch (tiles of all the group's
+// matrices), instead of one DP (n - 2 launches) per matrix. The group is
+// sized so its two layer buffers per matrix fit batch_scratch_bytes() (2 GB).
+// PL_BATCH_LAYERS=0: one matrix at a time.
+bool batch_layers_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_BATCH_LAYERS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// scratch per group of a large-order batch (PL_BATCH_SCRATCH_MB: tests force small groups)
+size_t batch_scratch_bytes() {
+    static const size_t b = [] {
+        const char* e = std::getenv("PL_BATCH_SCRATCH_MB");
+        return (e ? std::strtoull(e, nullptr, 10) : 2048ull) << 20;
+    }();
+    return b;
+}
+
+template <class R>
+pl_status run_layers_batch(int n, int64_t count, const void* a_dev, void* out_dev, int32_t* status_dev,
+                           cudaStream_t st, ScratchBlock* held) {
+    using T = typename R::T;
+    const uint64_t ml = max_layer(n);
+    const uint64_t stride = (ml + 8 + 31) & ~uint64_t(31);  // elements per matrix buffer (256-byte aligned, slack)
+    const int64_t group = std::max<int64_t>(1, std::min<int64_t>(count, (int64_t)(batch_scratch_bytes() / (2 * stride * sizeof(T)))));
+    constexpr size_t kHead = 256;
+    const size_t gbytes = ((size_t)group * sizeof(int32_t) + 255) & ~size_t(255);
+    ScratchBlock blk;
+    pl_status s = scratch_acquire_on(kHead + gbytes + 2 * (size_t)group * stride * sizeof(T), st, &blk);
+    if (s != PL_OK) return s;
+    int32_t* guards = reinterpret_cast<int32_t*>(static_cast<char*>(blk.ptr) + kHead);
+    T* buf0 = reinterpret_cast<T*>(static_cast<char*>(blk.ptr) + kHead + gbytes);
+    T* buf1 = buf0 + (size_t)group * stride;
+    for (int64_t g0 = 0; g0 < count && s == PL_OK; g0 += group) {
+        const uint32_t nm = (uint32_t)std::min<int64_t>(group, count - g0);
+        const T* ag = static_cast<const T*>(a_dev) + (size_t)g0 * n * n;
+        T* og = static_cast<T*>(out_dev) + g0;
+        const int32_t* gd = nullptr;
+        if constexpr (R::kChecked) {
+            pl::sz_guard_i64_batch_kernel<<<(nm + 127) / 128, 128, 0, st>>>(reinterpret_cast<const long long*>(ag), n,
+                                                                             nm, guards);
+            gd = guards;
+        }
+        const uint64_t c2 = pl::binom_u64(n, 2) * nm;
+        pl::sz_base_layer_batch_kernel<R><<<(unsigned)std::min<uint64_t>((c2 + 255) / 256, 4096), 256, 0, st>>>(
+            ag, n, buf0, stride, nm, status_dev);
+        PL_CUDA(cudaGetLastError());
+        T* prev = buf0;
+        T* cur = buf1;
+        for (int k = 3; k <= n - 1 && s == PL_OK; ++k) {
+            s = launch_layer<R>(n, ag, k, prev, cur, 0, pl::binom_u64(n, k), nullptr, gd, status_dev, st, nm, stride);
+            std::swap(prev, cur);
+        }
+        pl::sz_top_batch_kernel<R><<<(nm + 127) / 128, 128, 0, st>>>(ag, n, prev, stride, og, nm, status_dev);
+        PL_CUDA(cudaGetLastError());
+    }
+    if (held) {
+        *held = blk;
+        return s;
+    }
+    const pl_status s2 = scratch_release_on_stream(blk, st);
+    return s != PL_OK ? s : s2;
+}
+
 // Device-side batch compute: a_dev/out_dev device pointers, enqueue only.
 // `held`: a synchronous caller takes the large-order scratch block and
 // returns it to the cache after its stream synchronisation; otherwise a host
@@ -1016,6 +1108,11 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
     // cudaMalloc block; returned to the cache when the stream gets there).
     const size_t es = elem_size(dt);
     const uint64_t ml = max_layer(n);
+    if (count >= 2 && use_lean_layer(es, n, n / 2) && batch_layers_enabled()) {
+        return with_ring(dt, fma, [&](auto r) {
+            return run_layers_batch<decltype(r)>(n, count, a_dev, out_dev, status_dev, st, held);
+        });
+    }
     // Head: tile tickets of every layer (64 words) and the int64 guard flag.
     // Layer buffers carry 64 bytes of slack: 8-byte rings stage 16-byte aligned
     // spans that may read one element past a layer's last entry.

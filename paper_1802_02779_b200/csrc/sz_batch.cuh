@@ -85,12 +85,16 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
     const int64_t nfull = (reinterpret_cast<uintptr_t>(a) & 15u) ? 0 : count / Gm::kBatch;
     const int64_t stride = (int64_t)gridDim.x * Gm::kWarps;
     int64_t b = (int64_t)blockIdx.x * Gm::kWarps + warp;
+    // programmatic dependent launch: the next grid on the stream may be
+    // scheduled now; this grid reads nothing before the previous one is done
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (lane == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     auto issue = [&](int64_t batch, int slot) {
         if (lane == 0) {
             mbar_arrive_expect_tx(&bar[slot], Gm::kBatchBytes);
@@ -165,6 +169,7 @@ template <class R, int N>
 __global__ void __launch_bounds__(PipeGeom<typename R::T, N>::kThreads, 1)
     sz_batch_pipe_kernel(const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
                          int32_t* __restrict__ status) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     using T = typename R::T;
     using Gm = PipeGeom<T, N>;
     constexpr int S = Gm::S, W = Gm::W, E = Gm::kEnt;
@@ -183,6 +188,7 @@ __global__ void __launch_bounds__(PipeGeom<typename R::T, N>::kThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // see sz_batch_tma_kernel
     __syncthreads();
     bool ov_any = false;
     if (warp == W) {

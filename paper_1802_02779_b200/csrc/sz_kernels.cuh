@@ -889,6 +889,49 @@ __global__ void sz_top_kernel(const typename R::T* __restrict__ a, int n, const 
     out[0] = total;
 }
 
+// Batched forms for a batch of large orders (matrices n x n contiguous, layer
+// buffers `stride` elements apart): layer 2, the top level and the int64 guard
+// of every matrix in one launch each.
+template <class R>
+__global__ void sz_base_layer_batch_kernel(const typename R::T* __restrict__ a, int n, typename R::T* __restrict__ cur,
+                                           uint64_t stride, uint32_t nmat, int32_t* __restrict__ status) {
+    bool ov = false;
+    const uint64_t np = binom_u64(n, 2), total = np * nmat;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = t / np, r = t - b * np;
+        int j2 = 1;
+        while (binom_u64(j2 + 1, 2) <= r) ++j2;
+        const int j1 = (int)(r - binom_u64(j2, 2));
+        cur[b * stride + r] = base_pair<R>(a + b * (uint64_t)n * n, n, j1, j2, ov);
+    }
+    if (ov) atomicOr(status, 1);
+}
+
+template <class R>
+__global__ void sz_top_batch_kernel(const typename R::T* __restrict__ a, int n, const typename R::T* __restrict__ last,
+                                    uint64_t stride, typename R::T* __restrict__ out, uint32_t nmat,
+                                    int32_t* __restrict__ status) {
+    using T = typename R::T;
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nmat) return;
+    bool ov = false;
+    const T* row = a + ((uint64_t)b * n + (uint64_t)(n - 1)) * n;
+    const T* lb = last + (uint64_t)b * stride;
+    T total = R::mul(row[0], lb[n - 1], ov);
+    for (int j = 1; j < n; ++j) total = R::mac(total, row[j], lb[n - 1 - j], ov);
+    if (ov) {
+        atomicOr(status, 1);
+        total = R::zero();
+    }
+    out[b] = total;
+}
+
+static __global__ void sz_guard_i64_batch_kernel(const long long* __restrict__ a, int n, uint32_t nmat,
+                                                 int32_t* __restrict__ guard) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nmat) guard[b] = i64_guard_ok(a + (uint64_t)b * n * n, n) ? 0 : 1;
+}
+
 static __global__ void sz_guard_i64_kernel(const long long* __restrict__ a, int n, int32_t* __restrict__ guard) {
     if (threadIdx.x == 0 && blockIdx.x == 0) guard[0] = i64_guard_ok(a, n) ? 0 : 1;
 }

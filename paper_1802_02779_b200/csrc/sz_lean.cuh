@@ -93,7 +93,8 @@ struct LnHdr {
     T* out;                     // cur + rank of the tile's first output
     const uint4* lt;            // compact ltab rows of the m-subsets
     uint32_t pad_src;           // 8-byte rings: element offset of the source in its slot
-    uint32_t spare;
+    int32_t checked;            // int64: this matrix needs checked arithmetic (its guard flag)
+    T rowlow[kLnMaxD];          // a(k-1, v), v < D, of the tile's matrix
     T coef[kWsMaxHigh];         // a(k-1, F_l)
     const T* sptr[kWsMaxHigh];  // prev + base rank of stream tile (F \ {F_l}, k-1)
 };
@@ -110,7 +111,6 @@ struct alignas(16) LnWarp {
 template <class T>
 struct LnSmem {
     uint2 B2[kBinomDim * kBinomDim];  // (C(s, i), C(s, i - 1)) at [i * 35 + s]
-    T row[kMaxOrder + 2];             // a(k-1, j)
     LnWarp<T> w[LnGeom<(int)sizeof(T)>::WPB];
 };
 
@@ -273,14 +273,18 @@ __device__ __forceinline__ void ln_tile(const T* __restrict__ row, const LnHdr<T
 // Header of tile t (or the end marker) into the warp's slot s; the tile's low
 // source staged by one bulk copy completing on the slot's barrier. Returns
 // false when the tile has no outputs in [r0, r1) (nothing armed).
+// Batched form: tile t of the launch is tile t % ntiles of matrix t / ntiles
+// (matrices n x n contiguous from `a`, their layer buffers `lstride`
+// elements apart); a single matrix is nmat = 1.
 template <class T>
-__device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, uint32_t t, uint32_t ntiles,
-                                           const uint32_t* __restrict__ flist, int k, int D, int H,
-                                           const T* __restrict__ prev, T* __restrict__ cur, uint64_t r0,
-                                           uint64_t r1, const uint4* __restrict__ ltab,
-                                           const uint32_t* __restrict__ ltab_off, int lane) {
+__device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, uint64_t t, uint32_t ntiles,
+                                           uint64_t total, const uint32_t* __restrict__ flist, const T* __restrict__ a,
+                                           int n, int k, int D, int H, const T* __restrict__ prev_all,
+                                           T* __restrict__ cur_all, uint64_t lstride, uint64_t r0, uint64_t r1,
+                                           const uint4* __restrict__ ltab, const uint32_t* __restrict__ ltab_off,
+                                           const int32_t* __restrict__ guard, int lane) {
     LnHdr<T>& h = w.hdr[s];
-    if (t >= ntiles) {
+    if (t >= total) {
         if (lane == 0) {
             h.m = -1;
             mbar_arrive(&w.full[s]);
@@ -288,7 +292,11 @@ __device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, u
         __syncwarp();
         return true;
     }
-    const uint32_t F = __ldg(flist + t);
+    const uint64_t b = t / ntiles;
+    const T* prev = prev_all + b * lstride;
+    T* cur = cur_all + b * lstride;
+    const T* arow = a + (b * (uint64_t)n + (uint64_t)(k - 1)) * (uint64_t)n;
+    const uint32_t F = __ldg(flist + (t - b * ntiles));
     const int f = __popc(F), m = k - f;
     const bool set = lane < H && ((F >> lane) & 1u);
     const int idx = __popc(F & ((1u << lane) - 1u));
@@ -308,10 +316,12 @@ __device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, u
     const uint32_t q1 = (r1 - cur_base) < len ? (uint32_t)(r1 - cur_base) : len;
     if (q1 <= q0) return false;
     if (set) {
-        h.coef[idx] = sm.row[D + lane];
+        h.coef[idx] = arow[D + lane];
         h.sptr[idx] = prev + ((ix - x) + (src_base - iy));
     }
+    if (lane < D) h.rowlow[lane] = arow[lane];
     if (lane == 0) {
+        h.checked = guard != nullptr ? guard[b] : 0;
         h.m = m;
         h.f = f;
         h.q0 = q0;
@@ -336,9 +346,9 @@ __global__ void __launch_bounds__(LnGeom<(int)sizeof(typename R::T)>::kThreads,
                                   LnGeom<(int)sizeof(typename R::T)>::kMinBlocks)
     sz_lean_kernel(const typename R::T* __restrict__ a, int n, int k, int D, const typename R::T* __restrict__ prev,
                    typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ flist,
-                   uint32_t ntiles, const uint4* __restrict__ ltab, const uint32_t* __restrict__ ltab_off,
-                   const uint2* __restrict__ binom_pairs, const int32_t* __restrict__ guard,
-                   int32_t* __restrict__ status) {
+                   uint32_t ntiles, uint32_t nmat, uint64_t lstride, const uint4* __restrict__ ltab,
+                   const uint32_t* __restrict__ ltab_off, const uint2* __restrict__ binom_pairs,
+                   const int32_t* __restrict__ guard, int32_t* __restrict__ status) {
     using T = typename R::T;
     constexpr int WPB = LnGeom<(int)sizeof(T)>::WPB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -356,37 +366,38 @@ __global__ void __launch_bounds__(LnGeom<(int)sizeof(typename R::T)>::kThreads,
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous layer is complete and visible
     // generic-proxy stores of the previous layer, read below by bulk copies (async proxy)
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    const T* arow = a + (size_t)(k - 1) * n;
-    for (int v = threadIdx.x; v < n; v += blockDim.x) sm.row[v] = arow[v];
     __syncthreads();
 
-    bool use_checked = false;
-    if constexpr (R::kChecked) use_checked = guard != nullptr && guard[0] != 0;
     bool ov = false;
     const int H = n - D;
+    const uint64_t total = (uint64_t)ntiles * nmat;
     // warp gw takes tiles gw, gw + W, gw + 2W, ... (increasing F: one sweep front)
-    const uint32_t W = gridDim.x * WPB;
-    uint32_t t = blockIdx.x * WPB + warp;
-    while (!ln_prepare(sm, w, 0, t, ntiles, flist, k, D, H, prev, cur, r0, r1, ltab, ltab_off, lane)) t += W;
+    const uint64_t W = (uint64_t)gridDim.x * WPB;
+    uint64_t t = (uint64_t)blockIdx.x * WPB + warp;
+    auto prep = [&](int slot) {
+        return ln_prepare(sm, w, slot, t, ntiles, total, flist, a, n, k, D, H, prev, cur, lstride, r0, r1, ltab,
+                          ltab_off, guard, lane);
+    };
+    while (!prep(0)) t += W;
     for (uint32_t it = 0;; ++it) {
         const int s = (int)(it & 1u);
-        if (t < ntiles) {
+        if (t < total) {
             // next tile into the other slot (last read by this warp's previous tile)
             do {
                 t += W;
-            } while (!ln_prepare(sm, w, s ^ 1, t, ntiles, flist, k, D, H, prev, cur, r0, r1, ltab, ltab_off, lane));
+            } while (!prep(s ^ 1));
         }
         mbar_wait(&w.full[s], (it >> 1) & 1u);
         const LnHdr<T>& h = w.hdr[s];
         if (h.m < 0) break;
         const T* src = w.src[s] + h.pad_src;
         if constexpr (R::kChecked) {
-            if (use_checked)
-                ln_tile<R>(sm.row, h, src, lane, ov);
+            if (h.checked)
+                ln_tile<R>(h.rowlow, h, src, lane, ov);
             else
-                ln_tile<RU>(sm.row, h, src, lane, ov);
+                ln_tile<RU>(h.rowlow, h, src, lane, ov);
         } else {
-            ln_tile<R>(sm.row, h, src, lane, ov);
+            ln_tile<R>(h.rowlow, h, src, lane, ov);
         }
         __syncwarp();
     }

@@ -444,3 +444,43 @@ def test_f32_pack_kernel_paths(n):
     a[22] = np.eye(n, dtype=np.int64) * 3
     want = O.sz_batch(a)
     assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
+
+
+@pytest.mark.parametrize("n", [15, 17, 20, 22])
+def test_large_order_batches_one_launch_per_layer(n):
+    # batches of 15 <= n <= ~22 run every layer of a group of matrices in one lean
+    # launch (tiles of all the group's matrices); compare with the oracle per
+    # ring, with an int64 member that needs the checked path and a tail group
+    rng = np.random.default_rng(9100 + n)
+    count = 5
+    c = rng.standard_normal((count, n, n)) + 1j * rng.standard_normal((count, n, n))
+    assert np.array_equal(pl.store_zechin_permanent_batch(c).view(np.uint64), O.sz_batch(c).view(np.uint64))
+    f = rng.uniform(-1, 1, (count, n, n))
+    assert np.array_equal(pl.store_zechin_permanent_batch(f).view(np.uint64), O.sz_batch(f).view(np.uint64))
+    i = rng.integers(0, 2, (count, n, n)).astype(np.int64)
+    i[2] = rng.integers(-3, 4, (n, n))  # guard bound above 2^63: checked int64
+    want = O.sz_batch(i)
+    assert np.array_equal(pl.store_zechin_permanent_batch(i), want)
+
+
+def test_large_order_batch_groups():
+    # several groups (PL_BATCH_SCRATCH_MB=1 forces tiny groups) and the per-matrix path agree
+    n = 16
+    a = np.random.default_rng(9200).standard_normal((7, n, n)) + 0j
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); import paper_1802_02779_b200 as pl; "
+        "a = np.load(sys.argv[1]); np.save(sys.argv[2], pl.store_zechin_permanent_batch(a))" % str(ROOT))
+    import os
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        np.save(os.path.join(d, "a.npy"), a)
+        outs = []
+        for env in ({"PL_BATCH_SCRATCH_MB": "1"}, {"PL_BATCH_LAYERS": "0"}):
+            p = os.path.join(d, "o%d.npy" % len(outs))
+            subprocess.run(["python", "-c", code, os.path.join(d, "a.npy"), p], check=True,
+                           env={**os.environ, **env}, timeout=300)
+            outs.append(np.load(p))
+    want = O.sz_batch(a)
+    for o in outs:
+        assert np.array_equal(o.view(np.uint64), want.view(np.uint64))
