@@ -297,6 +297,27 @@ def suite_cpu_baseline(name: str, a: np.ndarray, budget_s: float, live_large: bo
             "nproc": os.cpu_count()}
 
 
+def suite_cpu_baseline_batch(a: np.ndarray, budget_s: float):
+    """The reference engine on a bounded sample of the batch_n16 matrices
+    (contiguous chunks over all host threads)."""
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return {"error": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    done, t0, pos = 0, time.perf_counter(), 0
+    while time.perf_counter() - t0 < budget_s:
+        size = min(threads * 4, a.shape[0] - pos) or threads * 4
+        if pos + size > a.shape[0]:
+            pos = 0
+        O.ref_sz_batch(a[pos:pos + size], nthreads=threads)
+        pos += size
+        done += size
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "permanents/s", "cores": threads, "kind": "reference",
+            "sample": f"{done} matrices n={a.shape[1]} ({el:.1f} s wall, {threads} threads)", "cpu_model": cpu_model()}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -579,12 +600,17 @@ def boson_cpu_reference(budget_s: float):
 DFMA_PEAK = (33.40, "measured DFMA rate x 2 flop (profiles/microbench_b200.json: 16.7 T DFMA/s)")
 
 
-def kernel_name(n: int) -> str:
+FP32_PEAK = (74.4, "nominal FFMA rate x 2 flop (148 SMs x 128 FFMA/clk x 1.965 GHz)")
+
+
+def kernel_name(n: int, dtype: str = "") -> str:
     if n <= 5:
         return "sz_batch_tma_kernel"
+    if 10 <= n <= 14 and dtype == "int64":
+        return "sz_batch_f32_pack_kernel (four matrices per CTA, exact integers on the FP32 pipe)"
     if n <= 14:
         return "sz_batch_smem_pack_kernel (8-byte) / sz_batch_smem_kernel (complex)"
-    return "sz_ws_kernel (all layers of one step)"
+    return "sz_ws_kernel (middle layers) + sz_lean_kernel (layers <= 24 MB), all layers of one step"
 
 
 def roofline_of(res, peak, peak_src, traffic):
@@ -594,17 +620,26 @@ def roofline_of(res, peak, peak_src, traffic):
     input is a few KB per matrix against ~10^4-10^5 DFMA (C3: 45,045 exact
     integer ops per permanent executed as DFMA on exact doubles)."""
     n = res["spec"]["n"]
+    dtype = res["spec"]["dtype"]
     tr = traffic.get(res["name"])
     fp = res["flops_per_step"] / res["per_step_s"] / 1e12
+    if 10 <= n <= 14 and dtype == "int64":
+        return {"bound": "fp32", "achieved": fp, "peak": FP32_PEAK[0], "unit": "TFLOP/s", "frac": fp / FP32_PEAK[0],
+                "peak_source": FP32_PEAK[1], "traffic": tr, "kernel": kernel_name(n, dtype),
+                "hbm_gbs": res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9,
+                "fp64_equivalent_frac": fp / DFMA_PEAK[0],
+                "note": "exact integers on the FP32 pipe (every value provably < 2^24); the measured limiter is "
+                        "the L1TEX/shared-memory pipe (operand and predecessor-table loads, ~89 % busy in "
+                        "profiles/r2b), not the FFMA rate"}
     if 6 <= n <= 14:
         return {"bound": "fp64", "achieved": fp, "peak": DFMA_PEAK[0], "unit": "TFLOP/s", "frac": fp / DFMA_PEAK[0],
-                "peak_source": DFMA_PEAK[1], "traffic": tr, "kernel": kernel_name(n),
+                "peak_source": DFMA_PEAK[1], "traffic": tr, "kernel": kernel_name(n, dtype),
                 "hbm_gbs": res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9,
                 "note": "bytes are ~1 KB per 45 k ops: neither HBM nor L2 binds; the FP64 pipe is the ceiling "
                         "(shared-memory operand loads are the measured limiter, DESIGN.md section 4)"}
     achieved = res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9
     out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-           "traffic": tr, "peak_source": peak_src, "kernel": kernel_name(n), "fp_rate_tflops": fp}
+           "traffic": tr, "peak_source": peak_src, "kernel": kernel_name(n, dtype), "fp_rate_tflops": fp}
     if n >= 20:
         fpk = FP64_PEAK if not res.get("fma") else DFMA_PEAK
         out["fp64_frac"] = fp / fpk[0]
@@ -655,6 +690,86 @@ def suite_entry(r, name, steps, peak, peak_src, traffic, world):
             "roofline": roofline_of(r, peak, peak_src, traffic), "e2e": r["e2e"], "timing": r["timing"],
             "sharded": (("top-column blocks, point-to-point" if block_plan_applies(r["spec"]["n"], world)
                          else "equal slices, all-gather") if r["sharded"] else None)}
+
+
+BATCH16 = {"n": 16, "count": 2000, "seed": 16,
+           "desc": "2,000 x 16x16 complex128 (standard complex Gaussian, seed 16): a batch of large orders, "
+                   "every layer of the batch in one lean launch"}
+RYSER = {"n": 22, "seed": 22, "cpu_n": 18,
+         "desc": "Ryser engine (pl_ryser_permanent), single 22x22 float64 matrix, uniform [-1, 1] (seed 22); "
+                 "bitwise the reference's visit-order fold"}
+
+
+def measure_batch16(steps, warmup, device):
+    """Batched large orders (callers looping store_zechin_permanent at 15 <= n <= 20):
+    value device-resident, events around K back-to-back calls; CPU baseline the reference engine."""
+    import torch
+
+    import paper_1802_02779_b200 as pl
+
+    n, cnt = BATCH16["n"], BATCH16["count"]
+    rng = np.random.default_rng(BATCH16["seed"])
+    a_np = rng.standard_normal((cnt, n, n)) + 1j * rng.standard_normal((cnt, n, n))
+    a = torch.from_numpy(a_np).to(device)
+    out = torch.empty(cnt, dtype=torch.complex128, device=device)
+    st = torch.zeros(1, dtype=torch.int32, device=device)
+    for _ in range(warmup):
+        pl.store_zechin_permanent_batch(a, out=out, status=st)
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pl.store_zechin_permanent_batch(a, out=out, status=st)
+    e1.record()
+    torch.cuda.synchronize(device)
+    t = e0.elapsed_time(e1) / 1000.0 / steps
+    flops = flops_per_perm(n, "complex128") * cnt
+    res = {"value": cnt / t, "unit": "permanents/s", "ms_per_step": 1e3 * t, "steps": steps,
+           "workload": BATCH16["desc"],
+           "roofline": {"bound": "fp64", "achieved": flops / t / 1e12, "peak": FP64_PEAK[0], "unit": "TFLOP/s",
+                        "frac": flops / t / 1e12 / FP64_PEAK[0], "peak_source": FP64_PEAK[1],
+                        "kernel": "sz_lean_kernel (batched: tiles of all matrices per launch)"},
+           "per_matrix_path_ms": None}
+    t0 = time.perf_counter()
+    host = pl.store_zechin_permanent_batch(a_np)
+    res["e2e"] = {"value": cnt / (time.perf_counter() - t0), "unit": "permanents/s",
+                  "h2d_bytes_per_step": int(a_np.nbytes), "d2h_bytes_per_step": int(host.nbytes)}
+    return res, a_np
+
+
+def measure_ryser(steps, warmup):
+    import torch
+
+    import paper_1802_02779_b200 as pl
+
+    a = np.random.default_rng(RYSER["seed"]).uniform(-1, 1, (RYSER["n"], RYSER["n"]))
+    for _ in range(warmup):
+        pl.ryser_permanent(a)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        pl.ryser_permanent(a)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": 1.0 / t, "unit": "permanents/s", "time_to_permanent_ms": 1e3 * t, "steps": steps,
+            "workload": RYSER["desc"],
+            "note": "host call incl. H2D/D2H; the visit-order fold of 2^22 - 1 terms is one sequential chain "
+                    "(bitwise the reference), so the device time is latency-bound by design"}
+
+
+def ryser_cpu_reference():
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return {"error": "oracle/_ref not built"}
+    n = RYSER["cpu_n"]
+    a = np.random.default_rng(RYSER["seed"]).uniform(-1, 1, (n, n)).astype(np.complex128)
+    t0 = time.perf_counter()
+    O.ref_ryser_c128(a)
+    t = time.perf_counter() - t0
+    scale = (RYSER["n"] * 2 ** RYSER["n"]) / (n * 2 ** n)
+    return {"value": 1.0 / (t * scale), "unit": "permanents/s", "cores": 1, "kind": "reference",
+            "sample": f"reference ryser_permanent at n={n} ({t:.2f} s, 1 thread), scaled by n*2^n to n={RYSER['n']}"}
 
 
 def main():
@@ -719,6 +834,16 @@ def main():
                     suite[key] = {"error": repr(e)[:300]}
                     continue
                 suite[key] = suite_entry(r, name, args.steps if same else k, peak, peak_src, traffic, world)
+            if world == 1:
+                try:
+                    suite["batch_n16"], a16 = measure_batch16(5, 2, device)
+                except Exception as e:  # noqa: BLE001
+                    print(f"bench: suite entry batch_n16 failed: {e!r}", file=sys.stderr, flush=True)
+                    suite["batch_n16"], a16 = {"error": repr(e)[:300]}, None
+                try:
+                    suite["ryser"] = measure_ryser(5, 2)
+                except Exception as e:  # noqa: BLE001
+                    suite["ryser"] = {"error": repr(e)[:300]}
             for key, steps_b, spec_b in (("boson", 10, BOSON), ("boson_large", 3, BOSON_LARGE)):
                 try:
                     suite[key] = measure_boson(steps_b, 3, rank, world, device, flush_buf, args.fma, spec_b)
@@ -741,6 +866,13 @@ def main():
                     suite[key]["cpu_baseline"] = {"error": repr(e)[:200]}
         if "error" not in suite.get("boson", {"error": 1}):
             suite["boson"]["cpu_baseline"] = boson_cpu_reference(5.0)
+        if "error" not in suite.get("batch_n16", {"error": 1}) and a16 is not None:
+            try:
+                suite["batch_n16"]["cpu_baseline"] = suite_cpu_baseline_batch(a16, 5.0)
+            except Exception as e:  # noqa: BLE001
+                suite["batch_n16"]["cpu_baseline"] = {"error": repr(e)[:200]}
+        if "error" not in suite.get("ryser", {"error": 1}):
+            suite["ryser"]["cpu_baseline"] = ryser_cpu_reference()
 
     cpu = None
     if cpu_on:
