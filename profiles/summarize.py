@@ -13,11 +13,14 @@ from __future__ import annotations
 import collections
 import csv
 import json
+import os
 import subprocess
 import sys
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
+if os.environ.get("SUMMARY_DIR"):  # on the GPU box: write next to the captures (gpurun_out/)
+    HERE = Path(os.environ["SUMMARY_DIR"]).resolve()
 
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -54,21 +57,23 @@ def summarize_launches(tag: str, path: Path):
     out = [f"# ncu launch list — {tag}", "", f"source: `{path.name}` (cold-cache, serialised; compare shares, not absolutes)", "",
            "| # | kernel | time (us) | DRAM read (MB) | DRAM write (MB) |", "|---|---|---|---|---|"]
     for (i, name), m in per.items():
-        if not name.startswith("void pl::") and "sz_" not in name:
+        if "sz_" not in name and "ryser" not in name:
             continue
         out.append(f"| {i} | `{name.split('(')[0][:70]}` | {m.get('gpu__time_duration.sum', 0) / 1e3:.1f} | "
                    f"{m.get('dram__bytes_read.sum', 0) / 1e6:.1f} | {m.get('dram__bytes_write.sum', 0) / 1e6:.1f} |")
     (HERE / f"{tag}_launches.md").write_text("\n".join(out) + "\n")
     # DRAM bytes per step per config: batched configs launch one kernel per step; a layer-DP
     # step (C4 f64 n=26, C5 c128 n=32) is every sz_ kernel of that ring, counted per top kernel.
-    groups = {"c1": ("sz_batch_tma_kernel<pl::RI64", None), "c2": ("sz_batch_tma_kernel<pl::RC128", None),
-              "c3": ("sz_batch_smem_kernel<pl::RI64", None), "c4": ("RF64", "sz_top_kernel<pl::RF64"),
-              "c5": ("RC128<", "sz_top_kernel<pl::RC128")}
+    # (ncu prints kernel names with or without the pl:: namespace depending on version)
+    per = collections.OrderedDict(((i, name.replace("pl::", "")), m) for (i, name), m in per.items())
+    groups = {"c1": ("sz_batch_tma_kernel<RI64", None), "c2": ("sz_batch_tma_kernel<RC128", None),
+              "c3": ("sz_batch_f32_pack_kernel", None), "c4": ("RF64", "sz_top_kernel<RF64"),
+              "c5": ("RC128<", "sz_top_kernel<RC128")}
     traffic, times = {}, {}
     for cfg, (needle, marker) in groups.items():
         byts, t, steps = 0.0, 0.0, 0
-        sel = [m for (_, name), m in per.items() if "pl::" in name and needle in name
-               and not (cfg in ("c4", "c5") and "sz_batch" in name)]
+        sel = [m for (_, name), m in per.items() if "sz_" in name and needle in name
+               and not (cfg in ("c4", "c5") and ("sz_batch" in name or "tile_list" in name))]
         if marker is None and sel:
             # batched configs: one launch per device-resident step; the e2e calls move the
             # batch in chunks (smaller launches), which are left out
@@ -80,7 +85,7 @@ def summarize_launches(tag: str, path: Path):
         if marker is None:
             steps = len(sel)
         else:
-            steps = sum(1 for (_, name), m in per.items() if "pl::" in name and marker in name)
+            steps = sum(1 for (_, name), m in per.items() if marker in name)
         if steps:
             traffic[cfg] = byts / steps
             times[cfg] = t / steps / 1e3
