@@ -32,11 +32,15 @@ $(BUILD)/multi.o: $(CSRC)/multi.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh incl
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/multi.cu
 
+$(BUILD)/batch.o: $(CSRC)/batch.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/batch.cu
+
 $(BUILD)/ryser.o: $(CSRC)/ryser.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh include/permlab_b200.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/ryser.cu
 
-$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o
+$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/batch.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c

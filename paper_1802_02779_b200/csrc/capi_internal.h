@@ -20,6 +20,10 @@ int sm_count();
 // Enqueue the batched permanent kernels on device pointers (see capi.cu).
 pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
                         int32_t* status_dev, cudaStream_t st);
+// Small orders (n <= 14): the register / shared-memory batch kernels (batch.cu).
+bool small_order_batch(pl_dtype dt, int n);
+pl_status launch_small_batch(pl_dtype dt, bool fma, int n, int64_t count, const void* a_dev, void* out_dev,
+                             int32_t* status_dev, cudaStream_t st);
 // Order check of the permanent entry points (subset_order_limit, device cap).
 pl_status check_order_limits(int n, const pl_limits* lim);
 // memo_budget_bytes check (layer scratch of one device).

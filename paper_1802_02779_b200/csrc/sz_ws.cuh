@@ -406,7 +406,7 @@ __device__ __forceinline__ uint32_t loaded_dep(const T* v, int n, uint32_t rt_ze
 // Event trace of CTA 0 for pipeline analysis (PL_WS_TRACE, see capi.cu):
 // region r holds (clock64, event | arg << 8) pairs; r = 0/1 first warp of
 // consumer group 0/1, 2 streamer of group 0, 3 publisher.
-__device__ unsigned long long* g_ws_trace = nullptr;
+static __device__ unsigned long long* g_ws_trace = nullptr;
 constexpr int kWsTraceCap = 65536;
 
 #ifndef PL_WS_TRACE_ENABLE
@@ -439,7 +439,7 @@ struct WsTrace {
 // increasing colex rank of their tiles). Thread g writes the g-th one: bit b
 // is 0 iff g < the number of valid completions of the prefix with bit b = 0,
 // sum_{j in [fmin - p, fmax - p]} C(b, j) (p = ones so far).
-__global__ void sz_tile_list_kernel(int H, int fmin, int fmax, uint32_t count, uint32_t* __restrict__ out) {
+static __global__ void sz_tile_list_kernel(int H, int fmin, int fmax, uint32_t count, uint32_t* __restrict__ out) {
     const uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x;
     for (uint32_t g = g0; g < count; g += gridDim.x * blockDim.x) {
         uint32_t r = g, F = 0;
