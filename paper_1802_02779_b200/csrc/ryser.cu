@@ -141,7 +141,26 @@ __global__ void __launch_bounds__(256) ryser_fold_kernel(const T* __restrict__ t
                 total = v[0];
                 i = 1;
             }
-#pragma unroll 8
+            // the chain is one dependent add per term: keep the next 16 terms'
+            // shared-memory loads in flight while the current 16 are added
+            constexpr int U = 16;
+            T cur[U];
+            if (i + U <= len) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) cur[u] = v[i + u];
+                for (; i + 2 * U <= len; i += U) {
+                    T nxt[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) nxt[u] = v[i + U + u];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) total = fold_add(total, cur[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) total = fold_add(total, cur[u]);
+                i += U;
+            }
             for (; i < len; ++i) total = fold_add(total, v[i]);
         }
         __syncthreads();
