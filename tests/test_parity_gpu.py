@@ -191,6 +191,12 @@ def test_int64_overflow_guard():
         pl.store_zechin_permanent_batch(np.full((3, 5, 5), 10 ** 4, dtype=np.int64))
     with pytest.raises(pl.DomainError, match="overflow"):
         pl.store_zechin_permanent_batch(np.full((3, 9, 9), 10 ** 3, dtype=np.int64))
+    # batches of large orders (one lean launch per layer for the whole batch): the
+    # overflowing member is reported, the others' checked / exact paths stay exact
+    with pytest.raises(pl.DomainError, match="overflow"):
+        pl.store_zechin_permanent_batch(np.stack([np.eye(21, dtype=np.int64), np.ones((21, 21), dtype=np.int64)]))
+    b = np.stack([np.ones((20, 20), dtype=np.int64), np.eye(20, dtype=np.int64) * 2])
+    assert pl.store_zechin_permanent_batch(b).tolist() == [math.factorial(20), 2 ** 20]
     # INT64_MIN entry can never be exact-negated: guard -> checked path
     a = np.zeros((3, 3), dtype=np.int64)
     a[0, 0] = np.iinfo(np.int64).min
