@@ -207,6 +207,21 @@ pl_status pl_shard_range(int32_t n, int32_t world, int32_t rank, int32_t k, uint
  * (recv ? 1 : 0, peer, r0, r1). -1 on bad arguments. */
 int32_t pl_shard_exchange(int32_t n, int32_t world, int32_t rank, int32_t k, uint64_t* ops, int32_t max_ops);
 
+/* Overlapped block plan (sharded.py, and pl_sz_permanent_multi by default;
+ * PL_SHARD_OVERLAP=0 turns it off): `rank`'s block of layer k without the
+ * terms of the top log2(world) columns, from its own block of layer k-1 only
+ * -- so it can run while the exchange of layer k-1 is in flight -- then, once
+ * the blocks P \ {c} of layer k-1 have been received, those top-column
+ * terms. The top columns are the highest, so their terms come last in the
+ * reference's ascending order (permanent.cpp:164-174): the two steps are the
+ * same rounding sequence as pl_sz_layer. 3 <= k <= n-1; world = 2^t. */
+pl_status pl_shard_block_partial(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,
+                                 void* cur_dev, int32_t world, int32_t rank, uint32_t flags, const int32_t* guard_dev,
+                                 int32_t* status_dev, void* stream);
+pl_status pl_shard_block_top_terms(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,
+                                   void* cur_dev, int32_t world, int32_t rank, uint32_t flags, int32_t* status_dev,
+                                   void* stream);
+
 /* ---- boson sampling (reference proj/include/permlab/boson.hpp:67-99) ------
  * An m-mode interferometer is its unitary U: m*m complex128 entries,
  * row-major, interleaved (re, im) (reference Interferometer, boson.hpp:40-56;

@@ -528,3 +528,65 @@ int orc_ryser_i64(int n, const int64_t* a, int64_t* out_lo, int64_t* out_hi) {
     *out_hi = (int64_t)(total >> 64);
     return 0;
 }
+
+/* ------------------------------------------------ overlapped block plan (CPU)
+ * The CPU stand-ins of pl_shard_block_partial / pl_shard_block_top_terms for
+ * the multi-rank (gloo) tests of sharded.py. Partial: the layer step with only
+ * the terms of columns j < jmax (the top columns' terms come last in the
+ * reference's ascending order, permanent.cpp:164-174); an output without any
+ * such term is left 0. Top terms: cur[base + i] (+)= sum_s a(k-1, cols[s]) *
+ * prev[sbase[s] + i], s ascending; init: the first term initialises. */
+#define DEFINE_PARTIAL(NAME, T, MUL, ADD, ZERO)                                             \
+    int NAME(int n, const T* a, int k, const T* prev, T* cur, uint64_t r0, uint64_t r1,     \
+             int jmax) {                                                                    \
+        binom_init();                                                                       \
+        if (n < 3 || k < 3 || k > n - 1 || r1 > g_binom[n][k] || r0 > r1) return 1;         \
+        if (r0 == r1) return 0;                                                             \
+        const T* row = a + (size_t)(k - 1) * n;                                             \
+        uint64_t mask = orc_colex_unrank(k, r0);                                            \
+        int elem[MAXN];                                                                     \
+        uint64_t pred[MAXN];                                                                \
+        for (uint64_t r = r0; r < r1; ++r) {                                                \
+            preds_of(mask, k, elem, pred);                                                  \
+            T acc = ZERO;                                                                   \
+            int first = 1;                                                                  \
+            for (int p = 0; p < k; ++p) {                                                   \
+                if (elem[p] >= jmax) break;                                                 \
+                const T t = MUL(row[elem[p]], prev[pred[p]]);                               \
+                acc = first ? t : ADD(acc, t);                                              \
+                first = 0;                                                                  \
+            }                                                                               \
+            cur[r] = acc;                                                                   \
+            if (r + 1 < r1) mask = gosper_next(mask);                                       \
+        }                                                                                   \
+        return 0;                                                                           \
+    }
+#define DEFINE_TOPTERMS(NAME, T, MUL, ADD)                                                  \
+    int NAME(int n, const T* a, int k, const T* prev, T* cur, uint64_t base, uint64_t len,  \
+             int nsrc, const int* cols, const uint64_t* sbase, int init) {                  \
+        const T* row = a + (size_t)(k - 1) * n;                                             \
+        for (uint64_t i = 0; i < len; ++i) {                                                \
+            T acc = cur[base + i];                                                          \
+            for (int s = 0; s < nsrc; ++s) {                                                \
+                const T t = MUL(row[cols[s]], prev[sbase[s] + i]);                          \
+                acc = (init && s == 0) ? t : ADD(acc, t);                                   \
+            }                                                                               \
+            cur[base + i] = acc;                                                            \
+        }                                                                                   \
+        return 0;                                                                           \
+    }
+static const cplx kCZero = {0.0, 0.0};
+DEFINE_PARTIAL(orc_sz_layer_partial_f64, double, DMUL, DADD, 0.0)
+DEFINE_PARTIAL(orc_sz_layer_partial_c128_, cplx, cmul, cadd, kCZero)
+DEFINE_TOPTERMS(orc_sz_top_terms_f64, double, DMUL, DADD)
+DEFINE_TOPTERMS(orc_sz_top_terms_c128_, cplx, cmul, cadd)
+
+int orc_sz_layer_partial_c128(int n, const double* a, int k, const double* prev, double* cur, uint64_t r0,
+                              uint64_t r1, int jmax) {
+    return orc_sz_layer_partial_c128_(n, (const cplx*)a, k, (const cplx*)prev, (cplx*)cur, r0, r1, jmax);
+}
+int orc_sz_top_terms_c128(int n, const double* a, int k, const double* prev, double* cur, uint64_t base, uint64_t len,
+                          int nsrc, const int* cols, const uint64_t* sbase, int init) {
+    return orc_sz_top_terms_c128_(n, (const cplx*)a, k, (const cplx*)prev, (cplx*)cur, base, len, nsrc, cols, sbase,
+                                  init);
+}

@@ -64,6 +64,8 @@ EXPORTED_SYMBOLS = (
     "pl_boson_distribution",
     "pl_ryser_permanent",
     "pl_ryser_counts",
+    "pl_shard_block_partial",
+    "pl_shard_block_top_terms",
 )
 
 
@@ -128,6 +130,10 @@ def _load():
     L.pl_ryser_permanent.restype = C.c_int
     L.pl_ryser_counts.argtypes = [i32, C.POINTER(u64), C.POINTER(u64)]
     L.pl_ryser_counts.restype = C.c_int
+    L.pl_shard_block_partial.argtypes = [C.c_int, i32, vp, i32, vp, vp, i32, i32, u32, vp, vp, vp]
+    L.pl_shard_block_partial.restype = C.c_int
+    L.pl_shard_block_top_terms.argtypes = [C.c_int, i32, vp, i32, vp, vp, i32, i32, u32, vp, vp]
+    L.pl_shard_block_top_terms.restype = C.c_int
     return L
 
 

@@ -594,7 +594,7 @@ struct Unchecked<pl::RI64<true>> {
 template <class R>
 pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur, uint64_t r0, uint64_t r1,
                        uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st, uint32_t nmat = 1,
-                       uint64_t lstride = 0) {
+                       uint64_t lstride = 0, int top_cut = 0) {
     using T = typename R::T;
     if (r1 <= r0) return PL_OK;
     if (k == 2) {
@@ -647,7 +647,7 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
         PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                    static_cast<T*>(cur), r0, r1, flist + tk.rank0, tk.ntiles, nmat, lstride,
                                    static_cast<const uint4*>(lt.ltab), static_cast<const uint32_t*>(lt.offs),
-                                   static_cast<const uint2*>(qb.binom_pairs), guard, status));
+                                   static_cast<const uint2*>(qb.binom_pairs), guard, status, top_cut));
         return PL_OK;
     }
     const int D = tile_window(sizeof(T), n);
@@ -701,7 +701,8 @@ pl_status launch_layer(int n, const void* a, int k, const void* prev, void* cur,
     PL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a), n, k, D, static_cast<const T*>(prev),
                                static_cast<T*>(cur), r0, r1, tickets, flist + tk.rank0, tk.ntiles,
                                static_cast<const uint4*>(q.ltab), static_cast<const uint32_t*>(q.offs),
-                               static_cast<const uint2*>(q.binom_pairs), guard, status, ws_hints()));
+                               static_cast<const uint2*>(q.binom_pairs), guard, status,
+                               ws_hints() | (uint32_t)(top_cut & 7) << 28));
     if (trace) {
         PL_CUDA(cudaStreamSynchronize(st));
         std::vector<unsigned long long> hb((size_t)4 * pl::kWsTraceCap * 2);
@@ -1041,9 +1042,30 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
 pl_status check_order_limits(int n, const pl_limits* lim) { return check_order(n, lim); }
 pl_status check_budget_limits(pl_dtype dt, int n, const pl_limits* lim) { return check_budget(dt, n, lim); }
 pl_status layer(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t r0,
-                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st) {
+                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st, int top_cut) {
     return with_ring(dt, fma, [&](auto r) {
-        return launch_layer<decltype(r)>(n, a, k, prev, cur, r0, r1, tickets, guard, status, st);
+        return launch_layer<decltype(r)>(n, a, k, prev, cur, r0, r1, tickets, guard, status, st, 1, 0, top_cut);
+    });
+}
+pl_status top_terms(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t base,
+                    uint64_t len, int nsrc, const int* cols, const uint64_t* src_bases, bool init_first, int32_t* status,
+                    cudaStream_t st) {
+    if (len == 0 || nsrc == 0) return PL_OK;
+    if (nsrc > 8) return fail(PL_ERR_ARG, "at most 8 top columns");
+    pl::TopSrc src{};
+    for (int i = 0; i < nsrc; ++i) {
+        src.col[i] = cols[i];
+        src.base[i] = src_bases[i];
+    }
+    return with_ring(dt, fma, [&](auto r) {
+        using R = decltype(r);
+        using T = typename R::T;
+        const unsigned blocks = (unsigned)std::min<uint64_t>((len + 255) / 256, (uint64_t)num_sms() * 8);
+        pl::sz_top_terms_kernel<R><<<blocks, 256, 0, st>>>(static_cast<const T*>(a), n, k, static_cast<const T*>(prev),
+                                                           static_cast<T*>(cur), base, len, nsrc, src, init_first ? 1 : 0,
+                                                           status);
+        PL_CUDA(cudaGetLastError());
+        return PL_OK;
     });
 }
 pl_status top(pl_dtype dt, bool fma, int n, const void* a, const void* last, void* out, const int32_t* guard,

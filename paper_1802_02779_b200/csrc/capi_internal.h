@@ -30,8 +30,16 @@ pl_status check_order_limits(int n, const pl_limits* lim);
 pl_status check_budget_limits(pl_dtype dt, int n, const pl_limits* lim);
 // One layer range / the top level / the int64 guard on the current device (see pl_sz_layer;
 // `tickets` a zeroed device word for k > 2).
+// top_cut > 0: a partial layer without the terms of the top `top_cut` columns
+// (the multi-GPU block plan adds them with top_terms once the exchange landed).
 pl_status layer(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t r0,
-                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st);
+                uint64_t r1, uint32_t* tickets, const int32_t* guard, int32_t* status, cudaStream_t st,
+                int top_cut = 0);
+// out[base + i] (+)= sum_s a(k-1, cols[s]) * prev[src_bases[s] + i], i < len, s ascending
+// (init_first: the first term initialises). See sz_top_terms_kernel.
+pl_status top_terms(pl_dtype dt, bool fma, int n, const void* a, int k, const void* prev, void* cur, uint64_t base,
+                    uint64_t len, int nsrc, const int* cols, const uint64_t* src_bases, bool init_first, int32_t* status,
+                    cudaStream_t st);
 pl_status top(pl_dtype dt, bool fma, int n, const void* a, const void* last, void* out, const int32_t* guard,
               int32_t* status, cudaStream_t st);
 pl_status guard_i64(int n, const void* a, int32_t* guard, cudaStream_t st);

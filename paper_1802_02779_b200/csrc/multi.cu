@@ -106,6 +106,49 @@ int block_exchange(int n, int k, int world, int g, Xop* ops) {
     return c;
 }
 
+// Top-column terms of device g's block of layer k (block plan): its range,
+// the columns c in P_g ascending and the bases of the blocks P_g \ {c} of
+// layer k - 1 (same offsets, received from their owners); init_first when the
+// block has no other term (lower part empty: S = P_g).
+struct TopTerms {
+    uint64_t base = 0, len = 0;
+    int nsrc = 0;
+    int cols[8];
+    uint64_t sbase[8];
+    bool init_first = false;
+};
+
+TopTerms block_top_terms(int n, int k, int world, int g) {
+    TopTerms tt;
+    const int t = top_columns(world);
+    uint64_t r0, r1;
+    top_block(n, k, world, g, &r0, &r1);
+    tt.base = r0;
+    tt.len = r1 - r0;
+    int bits = 0;
+    for (int i = 0; i < t; ++i) {
+        if (!((g >> i) & 1)) continue;
+        ++bits;
+        uint64_t s0, s1;
+        top_block(n, k - 1, world, g & ~(1 << i), &s0, &s1);
+        tt.cols[tt.nsrc] = n - t + i;
+        tt.sbase[tt.nsrc] = s0;
+        ++tt.nsrc;
+    }
+    tt.init_first = k == bits;
+    return tt;
+}
+
+// PL_SHARD_OVERLAP=0: the block plan exchanges each layer before the next
+// one starts (no partial layers).
+bool shard_overlap() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_SHARD_OVERLAP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // ---------------------------------------------------------------- NCCL (dlopen)
 
 struct Nccl {
@@ -166,6 +209,8 @@ struct DeviceGroup {
     std::vector<int> devs;
     std::vector<ncclComm_t> comms;
     std::vector<cudaStream_t> streams;
+    std::vector<cudaStream_t> xstreams;  // exchange streams (block plan, overlapped)
+    std::vector<cudaEvent_t> done, xdone;  // layer final on streams[g] / exchange landed on xstreams[g]
     std::mutex run;  // one sharded DP at a time per device set (NCCL ops must be issued in the same order)
 };
 
@@ -184,11 +229,17 @@ pl_status device_group(const std::vector<int>& devs, DeviceGroup** out) {
     g->devs = devs;
     g->comms.resize(devs.size());
     g->streams.resize(devs.size());
+    g->xstreams.resize(devs.size());
+    g->done.resize(devs.size());
+    g->xdone.resize(devs.size());
     int cur = 0;
     PLC_CUDA(cudaGetDevice(&cur));
     for (size_t i = 0; i < devs.size(); ++i) {
         PLC_CUDA(cudaSetDevice(devs[i]));
         PLC_CUDA(cudaStreamCreateWithFlags(&g->streams[i], cudaStreamNonBlocking));
+        PLC_CUDA(cudaStreamCreateWithFlags(&g->xstreams[i], cudaStreamNonBlocking));
+        PLC_CUDA(cudaEventCreateWithFlags(&g->done[i], cudaEventDisableTiming));
+        PLC_CUDA(cudaEventCreateWithFlags(&g->xdone[i], cudaEventDisableTiming));
     }
     PLC_CUDA(cudaSetDevice(cur));
     PL_NCCL(api.CommInitAll(g->comms.data(), (int)devs.size(), devs.data()));
@@ -262,7 +313,76 @@ pl_status sharded_dp(DeviceGroup& G, pl_dtype dt, int n, const void* a, void* ou
         bufs[g][1] = dev_ptr(g, kHead + stride);
     }
     int pi = 0;  // layer k lands in bufs[.][pi ^ 1] ... prev = bufs[.][pi]
-    for (int k = 2; k <= n - 1 && s == PL_OK; ++k) {
+    const bool overlap = blocks && shard_overlap() && n - 1 >= 3;
+    const int tcols = top_columns(world);
+    for (int k = 2; overlap && k <= n - 1 && s == PL_OK; ++k) {
+        // Overlapped block plan. Layer k of device g: the partial layer (every
+        // term but the top columns', from g's own block of layer k - 1) runs on
+        // streams[g] while the exchange of layer k - 1 runs on xstreams[g];
+        // then the top-column terms from the received blocks. The top columns
+        // are the highest, so their terms come last in the reference's
+        // ascending order: partial + top terms is the same rounding sequence.
+        const int ci = k == 2 ? 0 : (pi ^ 1);
+        if (k >= 3) {
+            // exchange of layer k - 1 (final on streams[g], event done[g])
+            PL_NCCL(api.GroupStart());
+            for (int g = 0; g < world; ++g) {
+                PLC_CUDA(cudaSetDevice(G.devs[g]));
+                PLC_CUDA(cudaStreamWaitEvent(G.xstreams[g], G.done[g], 0));
+                Xop ops[32];
+                const int no = block_exchange(n, k - 1, world, g, ops);
+                for (int i = 0; i < no; ++i) {
+                    char* p = bufs[g][pi] + ops[i].r0 * es;
+                    const size_t bytes = (ops[i].r1 - ops[i].r0) * es;
+                    if (ops[i].recv) PL_NCCL(api.Recv(p, bytes, ncclUint8, ops[i].peer, G.comms[g], G.xstreams[g]));
+                    else PL_NCCL(api.Send(p, bytes, ncclUint8, ops[i].peer, G.comms[g], G.xstreams[g]));
+                }
+            }
+            PL_NCCL(api.GroupEnd());
+            for (int g = 0; g < world; ++g) {
+                PLC_CUDA(cudaSetDevice(G.devs[g]));
+                PLC_CUDA(cudaEventRecord(G.xdone[g], G.xstreams[g]));
+            }
+        }
+        for (int g = 0; g < world && s == PL_OK; ++g) {
+            uint64_t r0, r1;
+            top_block(n, k, world, g, &r0, &r1);
+            PLC_CUDA(cudaSetDevice(G.devs[g]));
+            if (r1 > r0) {
+                s = plc::layer(dt, fma, n, dev_ptr(g, mat_off), k, k == 2 ? nullptr : bufs[g][pi], bufs[g][ci], r0, r1,
+                               reinterpret_cast<uint32_t*>(dev_ptr(g, kTickets)) + k,
+                               reinterpret_cast<const int32_t*>(dev_ptr(g, kGuard)),
+                               reinterpret_cast<int32_t*>(dev_ptr(g, kStatus)), G.streams[g], k == 2 ? 0 : tcols);
+            }
+            if (s != PL_OK) break;
+            if (k >= 3) {
+                PLC_CUDA(cudaStreamWaitEvent(G.streams[g], G.xdone[g], 0));
+                const TopTerms tt = block_top_terms(n, k, world, g);
+                if (tt.len) {
+                    s = plc::top_terms(dt, fma, n, dev_ptr(g, mat_off), k, bufs[g][pi], bufs[g][ci], tt.base, tt.len,
+                                       tt.nsrc, tt.cols, tt.sbase, tt.init_first,
+                                       reinterpret_cast<int32_t*>(dev_ptr(g, kStatus)), G.streams[g]);
+                }
+            }
+            PLC_CUDA(cudaEventRecord(G.done[g], G.streams[g]));
+        }
+        if (s != PL_OK) break;
+        if (k == n - 1) {  // layer n - 1: every owner sends its entries to device 0
+            PL_NCCL(api.GroupStart());
+            for (int g = 0; g < world; ++g) {
+                for (int h = 1; h < world; ++h) {
+                    uint64_t r0, r1;
+                    top_block(n, k, world, h, &r0, &r1);
+                    if (r1 <= r0) continue;
+                    if (g == 0) PL_NCCL(api.Recv(bufs[0][ci] + r0 * es, (r1 - r0) * es, ncclUint8, h, G.comms[0], G.streams[0]));
+                    if (g == h) PL_NCCL(api.Send(bufs[h][ci] + r0 * es, (r1 - r0) * es, ncclUint8, 0, G.comms[h], G.streams[h]));
+                }
+            }
+            PL_NCCL(api.GroupEnd());
+        }
+        pi = ci;
+    }
+    for (int k = 2; !overlap && k <= n - 1 && s == PL_OK; ++k) {
         const int ci = k == 2 ? 0 : (pi ^ 1);
         for (int g = 0; g < world && s == PL_OK; ++g) {
             uint64_t r0, r1;
@@ -459,6 +579,41 @@ int32_t pl_shard_exchange(int32_t n, int32_t world, int32_t rank, int32_t k, uin
         }
     }
     return c;
+}
+
+pl_status pl_shard_block_partial(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,
+                                 void* cur_dev, int32_t world, int32_t rank, uint32_t flags, const int32_t* guard_dev,
+                                 int32_t* status_dev, void* stream) {
+    if (!block_plan(n, world) || rank < 0 || rank >= world) return plc::fail_msg(PL_ERR_ARG, "not a block-plan rank");
+    if (k < 3 || k > n - 1) return plc::fail_msg(PL_ERR_ARG, "layer index k must be in [3, n-1]");
+    if (!a_dev || !prev_dev || !cur_dev || !status_dev) return plc::fail_msg(PL_ERR_ARG, "null device pointer");
+    if (dtype == PL_I64 && !guard_dev) return plc::fail_msg(PL_ERR_ARG, "int64 layers need the guard flag");
+    pl_status s = plc::device_ready();
+    if (s != PL_OK) return s;
+    uint64_t r0, r1;
+    top_block(n, k, world, rank, &r0, &r1);
+    if (r1 <= r0) return PL_OK;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* tickets = nullptr;
+    PLC_CUDA(cudaMallocAsync((void**)&tickets, sizeof(uint32_t), st));
+    PLC_CUDA(cudaMemsetAsync(tickets, 0, sizeof(uint32_t), st));
+    s = plc::layer(dtype, flags & PL_FLAG_FMA, n, a_dev, k, prev_dev, cur_dev, r0, r1, tickets, guard_dev, status_dev,
+                   st, top_columns(world));
+    cudaFreeAsync(tickets, st);
+    return s;
+}
+
+pl_status pl_shard_block_top_terms(pl_dtype dtype, int32_t n, const void* a_dev, int32_t k, const void* prev_dev,
+                                   void* cur_dev, int32_t world, int32_t rank, uint32_t flags, int32_t* status_dev,
+                                   void* stream) {
+    if (!block_plan(n, world) || rank < 0 || rank >= world) return plc::fail_msg(PL_ERR_ARG, "not a block-plan rank");
+    if (k < 3 || k > n - 1) return plc::fail_msg(PL_ERR_ARG, "layer index k must be in [3, n-1]");
+    if (!a_dev || !prev_dev || !cur_dev || !status_dev) return plc::fail_msg(PL_ERR_ARG, "null device pointer");
+    pl_status s = plc::device_ready();
+    if (s != PL_OK) return s;
+    const TopTerms tt = block_top_terms(n, k, world, rank);
+    return plc::top_terms(dtype, flags & PL_FLAG_FMA, n, a_dev, k, prev_dev, cur_dev, tt.base, tt.len, tt.nsrc,
+                          tt.cols, tt.sbase, tt.init_first, status_dev, static_cast<cudaStream_t>(stream));
 }
 
 pl_status pl_sz_permanent_multi(pl_dtype dtype, int32_t n, int64_t count, const void* a, void* out, uint32_t flags,

@@ -932,6 +932,39 @@ static __global__ void sz_guard_i64_batch_kernel(const long long* __restrict__ a
     if (b < nmat) guard[b] = i64_guard_ok(a + (uint64_t)b * n * n, n) ? 0 : 1;
 }
 
+// Top-column terms of one block of layer k (multi-GPU block plan, after a
+// partial layer without them): the block's outputs S (pattern P on the top
+// columns) get, in ascending column order c in P, the terms
+// a(k-1, c) * per(S \ {c}), whose predecessors sit at the same offset i in
+// the block of pattern P \ {c} of layer k-1 (received from its owner). The top
+// columns are the highest, so these terms come last in the reference's
+// ascending order (permanent.cpp:164-174): partial + these is rounding-exact.
+// init_first: the block's outputs have no other term (S = P).
+struct TopSrc {
+    int col[8];
+    uint64_t base[8];
+};
+
+template <class R>
+__global__ void sz_top_terms_kernel(const typename R::T* __restrict__ a, int n, int k,
+                                    const typename R::T* __restrict__ prev, typename R::T* __restrict__ cur,
+                                    uint64_t base, uint64_t len, int nsrc, TopSrc src, int init_first,
+                                    int32_t* __restrict__ status) {
+    using T = typename R::T;
+    bool ov = false;
+    const T* row = a + (size_t)(k - 1) * n;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
+        T acc = init_first ? R::zero() : cur[base + i];
+        for (int s = 0; s < nsrc; ++s) {
+            const T c = row[src.col[s]];
+            const T x = prev[src.base[s] + i];
+            acc = (init_first && s == 0) ? R::mul(c, x, ov) : R::mac(acc, c, x, ov);
+        }
+        cur[base + i] = acc;
+    }
+    if (ov) atomicOr(status, 1);
+}
+
 static __global__ void sz_guard_i64_kernel(const long long* __restrict__ a, int n, int32_t* __restrict__ guard) {
     if (threadIdx.x == 0 && blockIdx.x == 0) guard[0] = i64_guard_ok(a, n) ? 0 : 1;
 }

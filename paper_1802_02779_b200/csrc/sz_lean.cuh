@@ -282,7 +282,7 @@ __device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, u
                                            int n, int k, int D, int H, const T* __restrict__ prev_all,
                                            T* __restrict__ cur_all, uint64_t lstride, uint64_t r0, uint64_t r1,
                                            const uint4* __restrict__ ltab, const uint32_t* __restrict__ ltab_off,
-                                           const int32_t* __restrict__ guard, int lane) {
+                                           const int32_t* __restrict__ guard, int tcut, int lane) {
     LnHdr<T>& h = w.hdr[s];
     if (t >= total) {
         if (lane == 0) {
@@ -323,7 +323,8 @@ __device__ __forceinline__ bool ln_prepare(LnSmem<T>& sm, LnWarp<T>& w, int s, u
     if (lane == 0) {
         h.checked = guard != nullptr ? guard[b] : 0;
         h.m = m;
-        h.f = f;
+        // tcut > 0: a partial layer without the top `tcut` columns' terms (see sz_ws.cuh)
+        h.f = tcut ? __popc(F & ((1u << (H - tcut)) - 1u)) : f;
         h.q0 = q0;
         h.q1 = q1;
         h.out = cur + cur_base;
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(LnGeom<(int)sizeof(typename R::T)>::kThreads,
                    typename R::T* __restrict__ cur, uint64_t r0, uint64_t r1, const uint32_t* __restrict__ flist,
                    uint32_t ntiles, uint32_t nmat, uint64_t lstride, const uint4* __restrict__ ltab,
                    const uint32_t* __restrict__ ltab_off, const uint2* __restrict__ binom_pairs,
-                   const int32_t* __restrict__ guard, int32_t* __restrict__ status) {
+                   const int32_t* __restrict__ guard, int32_t* __restrict__ status, int top_cut) {
     using T = typename R::T;
     constexpr int WPB = LnGeom<(int)sizeof(T)>::WPB;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(LnGeom<(int)sizeof(typename R::T)>::kThreads,
     uint64_t t = (uint64_t)blockIdx.x * WPB + warp;
     auto prep = [&](int slot) {
         return ln_prepare(sm, w, slot, t, ntiles, total, flist, a, n, k, D, H, prev, cur, lstride, r0, r1, ltab,
-                          ltab_off, guard, lane);
+                          ltab_off, guard, top_cut, lane);
     };
     while (!prep(0)) t += W;
     for (uint32_t it = 0;; ++it) {

@@ -822,7 +822,11 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
             }
             if (lane == 0) {
                 h.m = m;
-                h.f = f;
+                // hints bits 28-30: a partial layer without the terms of the top
+                // `tcut` columns (they come last in the reference order; the
+                // multi-GPU block plan adds them once the exchange has landed)
+                const int tcut = (int)((hints >> 28) & 7u);
+                h.f = tcut ? __popc(F & ((1u << (H - tcut)) - 1u)) : f;
                 h.q1 = q1;
                 h.nchunks = nchunks;
                 h.cb = q0;

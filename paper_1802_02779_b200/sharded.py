@@ -30,6 +30,7 @@ step as the stand-in compute) and on GPUs (NCCL, with the CUDA kernels).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from math import comb
 from typing import Callable, List, Tuple
@@ -103,9 +104,11 @@ def top_block(n: int, k: int, world: int, g: int) -> Tuple[int, int]:
     return base, base + comb(n - t, m)
 
 
-def exchange_blocks(buf: torch.Tensor, n: int, k: int, rank: int, world: int, group=None):
+def exchange_blocks(buf: torch.Tensor, n: int, k: int, rank: int, world: int, group=None, wait: bool = True):
     """After layer k: hand rank `rank`'s block of layer k to the ranks that add
-    one top column to its pattern, and receive the blocks with one column less."""
+    one top column to its pattern, and receive the blocks with one column less.
+    wait=False returns the pending requests (the overlapped plan waits for them
+    after the next layer's partial compute)."""
     t = top_columns(world)
     ops = []
     for i in range(t):
@@ -119,19 +122,21 @@ def exchange_blocks(buf: torch.Tensor, n: int, k: int, rank: int, world: int, gr
             if r1 > r0:
                 ops.append(("send", partner, r0, r1))
     if not ops:
-        return
+        return []
     if buf.is_cuda:
         p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, _as_gather_view(buf[r0:r1]), peer,
                           group=group) for kind, peer, r0, r1 in ops]
-        for req in dist.batch_isend_irecv(p2p):
-            req.wait()
+        reqs = dist.batch_isend_irecv(p2p)
     else:
         reqs = []
         for kind, peer, r0, r1 in ops:
             view = _as_gather_view(buf[r0:r1])
             reqs.append(dist.isend(view, peer, group=group) if kind == "send" else dist.irecv(view, peer, group=group))
+    if wait:
         for req in reqs:
             req.wait()
+        return []
+    return reqs
 
 
 def gather_last_layer(buf: torch.Tensor, n: int, rank: int, world: int, group=None):
@@ -157,7 +162,7 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
                      layer_fn: Callable[[int, torch.Tensor, torch.Tensor, int, int], None],
                      top_fn: Callable[[torch.Tensor, torch.Tensor], object],
                      group=None, on_layer: Callable[[int], None] | None = None, plan: str = "auto",
-                 status: torch.Tensor | None = None):
+                     status: torch.Tensor | None = None, partial_fn=None, top_terms_fn=None):
     """Run the layer DP of matrix `a` (n x n, already on this rank's device)
     sharded over `world` ranks. `layer_fn(k, prev, cur, r0, r1)` fills
     cur[r0:r1] of layer k; `top_fn(a, last)` returns the permanent.
@@ -166,7 +171,14 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
     status word written by its layer kernels: before the top level it is
     combined over the group (MAX), so either every rank sees an int64
     overflow and raises, or none does (a wrapped value exchanged by one rank
-    never reaches a result silently)."""
+    never reaches a result silently).
+
+    Overlap (block plan, when `partial_fn(k, prev, cur)` and
+    `top_terms_fn(k, prev, cur)` are given): the exchange of layer k-1 runs
+    while the rank computes layer k without its top-column terms from its own
+    block; the top-column terms follow once the blocks have landed. The top
+    columns are the highest, so their terms come last in the reference's
+    ascending order and the result is bit-for-bit the non-overlapped one."""
     n = a.shape[0]
     if n < 3:
         raise ValueError("sharded DP needs n >= 3")
@@ -182,12 +194,24 @@ def sharded_layer_dp(a: torch.Tensor, rank: int, world: int,
             # NCCL: batched P2P among a subset of ranks is only defined once the
             # group has run a collective
             dist.barrier(group=group)
+        overlap = partial_fn is not None and top_terms_fn is not None and world > 1
+        pending = []
         for k in range(2, n):
             r0, r1 = top_block(n, k, world, rank)
-            if r1 > r0:
-                layer_fn(k, prev, cur, r0, r1)
+            if not overlap or k == 2:
+                if r1 > r0:
+                    layer_fn(k, prev, cur, r0, r1)
+            else:
+                # layer k-1's exchange (started below in the previous iteration) is in flight
+                if r1 > r0:
+                    partial_fn(k, prev, cur)
+                for req in pending:
+                    req.wait()
+                pending = []
+                if r1 > r0:
+                    top_terms_fn(k, prev, cur)
             if k < n - 1:
-                exchange_blocks(cur, n, k, rank, world, group)
+                pending = exchange_blocks(cur, n, k, rank, world, group, wait=not overlap)
             if on_layer is not None:
                 on_layer(k)
             prev, cur = cur, prev
@@ -243,8 +267,32 @@ def device_hooks(a: torch.Tensor, fma: bool = False, stream=None):
             raise DomainError("int64 overflow: an intermediate sub-permanent does not fit the exact int64 ring")
         return out.item()
 
+    layer_fn.guard = guard
     layer_fn.status = status  # the rank's overflow word (combined over ranks by sharded_layer_dp)
     return layer_fn, top_fn
+
+
+def device_overlap_hooks(a: torch.Tensor, layer_fn, rank: int, world: int, fma: bool = False, stream=None):
+    """partial_fn / top_terms_fn of the overlapped block plan (pl_shard_block_partial / _top_terms)."""
+    from . import _native as N
+    from .api import _check, _torch_dtype_code
+
+    code = _torch_dtype_code(a)
+    n = a.shape[0]
+    flags = N.PL_FLAG_FMA if fma else 0
+    st = (stream or torch.cuda.current_stream(a.device)).cuda_stream
+    status = layer_fn.status
+    guard = layer_fn.guard
+
+    def partial_fn(k, prev, cur):
+        _check(N.lib.pl_shard_block_partial(code, n, a.data_ptr(), k, prev.data_ptr(), cur.data_ptr(), world, rank,
+                                            flags, guard.data_ptr(), status.data_ptr(), st))
+
+    def top_terms_fn(k, prev, cur):
+        _check(N.lib.pl_shard_block_top_terms(code, n, a.data_ptr(), k, prev.data_ptr(), cur.data_ptr(), world, rank,
+                                              flags, status.data_ptr(), st))
+
+    return partial_fn, top_terms_fn
 
 
 def sharded_permanent(a: torch.Tensor, group=None, fma: bool = False):
@@ -253,4 +301,8 @@ def sharded_permanent(a: torch.Tensor, group=None, fma: bool = False):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     layer_fn, top_fn = device_hooks(a, fma=fma)
-    return sharded_layer_dp(a, rank, world, layer_fn, top_fn, group=group, status=layer_fn.status)
+    partial_fn = top_terms_fn = None
+    if world > 1 and block_plan_applies(a.shape[0], world) and os.environ.get("PL_SHARD_OVERLAP", "1") != "0":
+        partial_fn, top_terms_fn = device_overlap_hooks(a, layer_fn, rank, world, fma=fma)
+    return sharded_layer_dp(a, rank, world, layer_fn, top_fn, group=group, status=layer_fn.status,
+                            partial_fn=partial_fn, top_terms_fn=top_terms_fn)

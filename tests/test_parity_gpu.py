@@ -380,6 +380,62 @@ def test_top_block_plan_on_device_virtual_ranks(world, cplx):
     assert (hexf(got.real), hexf(got.imag)) == (hexf(want.real), hexf(want.imag))
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_overlapped_block_plan_on_device_virtual_ranks(world, cplx):
+    # the overlapped form (pl_shard_block_partial, then pl_shard_block_top_terms
+    # once the blocks P \ {c} of layer k-1 have "arrived"): the partial step
+    # runs BEFORE the exchange copies (the received regions are NaN when it
+    # runs, so reading them would show), the top terms after; bitwise the
+    # oracle. Both the lean (small layers) and ws (large layers) kernels cut.
+    import torch
+    from math import comb
+
+    from paper_1802_02779_b200.sharded import device_hooks, device_overlap_hooks, top_block
+
+    n = 24
+    t = world.bit_length() - 1
+    a_np = configs.complex_uniform((n, n), seed=40 + world) if cplx else configs.uniform((n, n), seed=40 + world)
+    a = torch.from_numpy(a_np).cuda()
+    layer_fn, top_fn = device_hooks(a)
+    hooks = [device_overlap_hooks(a, layer_fn, g, world) for g in range(world)]
+    size = max(comb(n, k) for k in range(2, n)) + 64
+    nan = complex("nan") if cplx else float("nan")
+    reps = [[torch.full((size,), nan, dtype=a.dtype, device="cuda") for _ in range(2)] for _ in range(world)]
+    for k in range(2, n):
+        for g in range(world):
+            prev, cur = reps[g]
+            cur.fill_(nan)
+            r0, r1 = top_block(n, k, world, g)
+            if k == 2:
+                if r1 > r0:
+                    layer_fn(k, prev, cur, r0, r1)
+            elif r1 > r0:
+                hooks[g][0](k, prev, cur)  # partial: own block of layer k-1 only
+        if k >= 3:
+            # the exchange of layer k-1 lands now, then the top-column terms
+            for g in range(world):
+                for i in range(t):
+                    if g >> i & 1:
+                        h = g ^ (1 << i)
+                        h0, h1 = top_block(n, k - 1, world, h)
+                        reps[g][0][h0:h1] = reps[h][0][h0:h1]
+            for g in range(world):
+                r0, r1 = top_block(n, k, world, g)
+                if r1 > r0:
+                    hooks[g][1](k, reps[g][0], reps[g][1])
+        for g in range(world):
+            reps[g].reverse()
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    last = reps[0][0].clone()
+    for h in range(world):
+        h0, h1 = top_block(n, n - 1, world, h)
+        last[h0:h1] = reps[h][0][h0:h1]
+    got = complex(top_fn(a, last))
+    want = complex(want)
+    assert (hexf(got.real), hexf(got.imag)) == (hexf(want.real), hexf(want.imag))
+
+
 def test_cpp_device_suite():
     exe = ROOT / "tests" / "cpp" / "test_permanent_device"
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)

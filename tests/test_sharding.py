@@ -61,6 +61,33 @@ def cpu_hooks(a: torch.Tensor):
     return layer_fn, top_fn
 
 
+def cpu_overlap_hooks(a: torch.Tensor, rank: int, world: int):
+    """CPU stand-ins of pl_shard_block_partial / pl_shard_block_top_terms (oracle C code)."""
+    L = _bind()
+    n = a.shape[0]
+    cplx = a.is_complex()
+    _i32p, _u64p = C.POINTER(C.c_int), C.POINTER(C.c_uint64)
+    part = L.orc_sz_layer_partial_c128 if cplx else L.orc_sz_layer_partial_f64
+    part.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, C.c_uint64, C.c_uint64, C.c_int]
+    tt = L.orc_sz_top_terms_c128 if cplx else L.orc_sz_top_terms_f64
+    tt.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, C.c_uint64, C.c_uint64, C.c_int, _i32p, _u64p, C.c_int]
+    t = world.bit_length() - 1
+
+    def partial_fn(k, prev, cur):
+        r0, r1 = top_block(n, k, world, rank)
+        assert part(n, _dptr(a), k, _dptr(prev), _dptr(cur), r0, r1, n - t) == 0
+
+    def top_terms_fn(k, prev, cur):
+        r0, r1 = top_block(n, k, world, rank)
+        bits = [i for i in range(t) if rank >> i & 1]
+        cols = (C.c_int * 8)(*[n - t + i for i in bits])
+        bases = (C.c_uint64 * 8)(*[top_block(n, k - 1, world, rank & ~(1 << i))[0] for i in bits])
+        assert tt(n, _dptr(a), k, _dptr(prev), _dptr(cur), r0, r1 - r0, len(bits), cols, bases,
+                  int(k == len(bits))) == 0
+
+    return partial_fn, top_terms_fn
+
+
 def test_layer_slices_cover_exactly():
     for n in (5, 9, 26, 32):
         for world in (1, 2, 3, 4, 8):
@@ -154,7 +181,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, cplx, q):
+def _worker(rank, world, port, n, cplx, q, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -162,7 +189,10 @@ def _worker(rank, world, port, n, cplx, q):
         a_np = configs.complex_uniform((n, n), seed=31) if cplx else configs.uniform((n, n), seed=31)
         a = torch.from_numpy(a_np)
         layer_fn, top_fn = cpu_hooks(a)
-        v = sharded_layer_dp(a, rank, world, layer_fn, top_fn)
+        pf = tf = None
+        if overlap:
+            pf, tf = cpu_overlap_hooks(a, rank, world)
+        v = sharded_layer_dp(a, rank, world, layer_fn, top_fn, partial_fn=pf, top_terms_fn=tf)
         q.put((rank, v))
     finally:
         dist.destroy_process_group()
@@ -176,6 +206,27 @@ def test_gloo_sharded_dp_bitwise(world, cplx):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, cplx, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a_np = configs.complex_uniform((n, n), seed=31) if cplx else configs.uniform((n, n), seed=31)
+    want = O.sz_c128(a_np) if cplx else O.sz_f64(a_np)
+    assert set(results.values()) == {want}
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gloo_overlapped_block_plan_bitwise(world, cplx):
+    # the exchange of layer k-1 in flight while layer k is computed without its
+    # top-column terms, which are added once the blocks have landed
+    n = 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, cplx, q, True)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=120) for _ in range(world))
