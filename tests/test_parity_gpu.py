@@ -546,3 +546,21 @@ def test_large_order_batch_groups():
     want = O.sz_batch(a)
     for o in outs:
         assert np.array_equal(o.view(np.uint64), want.view(np.uint64))
+
+
+def test_round2_kernels_repeatable():
+    # races show as run-to-run differences (round 1f's stage-ring race did): the lean
+    # kernel (batched large orders and a single matrix's outer layers), the FP32 packs
+    # and the overlapped-plan kernels, each run several times bitwise identical and
+    # equal to the oracle
+    rng = np.random.default_rng(9900)
+    b = rng.standard_normal((48, 18, 18)) + 1j * rng.standard_normal((48, 18, 18))
+    runs = [pl.store_zechin_permanent_batch(b).view(np.uint64) for _ in range(4)]
+    assert all(np.array_equal(r, runs[0]) for r in runs)
+    assert np.array_equal(runs[0][:6], O.sz_batch(b[:3]).view(np.uint64))  # 3 complex = 6 words
+    c3 = configs.c3(4000)
+    r3 = [pl.store_zechin_permanent_batch(c3) for _ in range(4)]
+    assert all(np.array_equal(r, r3[0]) for r in r3)
+    f = rng.uniform(-1, 1, (23, 23))
+    v = {struct.pack(">d", pl.store_zechin_permanent(f).value) for _ in range(4)}
+    assert v == {struct.pack(">d", O.sz_f64(f))}
