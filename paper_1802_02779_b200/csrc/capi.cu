@@ -871,10 +871,27 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
 // direction) overlap; the call then costs about the upload alone.
 constexpr size_t kPipeMinBytes = size_t(8) << 20;
 constexpr size_t kPipeChunkBytes = size_t(8) << 20;
+#ifndef PL_HOST_UP_DEFAULT
+#define PL_HOST_UP_DEFAULT 1
+#endif
+constexpr int kDefaultUpStreams = PL_HOST_UP_DEFAULT;
+
+constexpr int kMaxUpStreams = 4;
 
 struct CopyStreams {
-    cudaStream_t up = nullptr, down = nullptr;
+    cudaStream_t up[kMaxUpStreams] = {};
+    cudaStream_t down = nullptr;
 };
+
+// Upload streams of the host pipeline: chunk c goes up on stream c mod N, so N
+// copies can be in flight on different copy engines (PL_HOST_UP_STREAMS).
+int host_up_streams() {
+    static const int nup = [] {
+        const char* e = std::getenv("PL_HOST_UP_STREAMS");
+        return e ? std::max(1, std::min(kMaxUpStreams, atoi(e))) : kDefaultUpStreams;
+    }();
+    return nup;
+}
 
 pl_status copy_streams(CopyStreams* out) {
     static thread_local std::map<int, CopyStreams> cache;  // per thread and device
@@ -883,7 +900,7 @@ pl_status copy_streams(CopyStreams* out) {
     auto it = cache.find(dev);
     if (it == cache.end()) {
         CopyStreams cs;
-        PL_CUDA(cudaStreamCreateWithFlags(&cs.up, cudaStreamNonBlocking));
+        for (int i = 0; i < kMaxUpStreams; ++i) PL_CUDA(cudaStreamCreateWithFlags(&cs.up[i], cudaStreamNonBlocking));
         PL_CUDA(cudaStreamCreateWithFlags(&cs.down, cudaStreamNonBlocking));
         it = cache.emplace(dev, cs).first;
     }
@@ -910,19 +927,22 @@ pl_status pipelined_host_batch(pl_dtype dt, int n, int64_t count, const void* a,
         evs.push_back(*e);
         return PL_OK;
     };
+    const int nup = (int)std::min<int64_t>(host_up_streams(), nchunks);
     cudaEvent_t start;
     s = make_event(&start);
     if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(start, st), "cudaEventRecord");
-    if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(cs.up, start, 0), "cudaStreamWaitEvent");
+    for (int i = 0; i < nup && s == PL_OK; ++i)
+        s = cuda_fail_if(cudaStreamWaitEvent(cs.up[i], start, 0), "cudaStreamWaitEvent");
     if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(cs.down, start, 0), "cudaStreamWaitEvent");
     for (int64_t c = 0; c < nchunks && s == PL_OK; ++c) {
         const int64_t b0 = c * per, b1 = std::min<int64_t>(count, b0 + per);
         const size_t off_in = (size_t)b0 * mat_bytes, len_in = (size_t)(b1 - b0) * mat_bytes;
         cudaEvent_t up_done, k_done;
         if ((s = make_event(&up_done)) != PL_OK || (s = make_event(&k_done)) != PL_OK) break;
+        cudaStream_t up = cs.up[c % nup];
         s = cuda_fail_if(cudaMemcpyAsync(static_cast<char*>(a_dev) + off_in, static_cast<const char*>(a) + off_in,
-                                         len_in, cudaMemcpyHostToDevice, cs.up), "cudaMemcpyAsync(in)");
-        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(up_done, cs.up), "cudaEventRecord");
+                                         len_in, cudaMemcpyHostToDevice, up), "cudaMemcpyAsync(in)");
+        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(up_done, up), "cudaEventRecord");
         if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, up_done, 0), "cudaStreamWaitEvent");
         if (s == PL_OK)
             s = enqueue_batch(dt, n, b1 - b0, static_cast<const char*>(a_dev) + off_in,
@@ -936,11 +956,15 @@ pl_status pipelined_host_batch(pl_dtype dt, int n, int64_t count, const void* a,
                              "cudaMemcpyAsync(out)");
     }
     // the caller's stream continues after every download (and every upload)
-    cudaEvent_t up_all, down_all;
-    if (s == PL_OK && (s = make_event(&up_all)) == PL_OK && (s = make_event(&down_all)) == PL_OK) {
-        s = cuda_fail_if(cudaEventRecord(up_all, cs.up), "cudaEventRecord");
-        if (s == PL_OK) s = cuda_fail_if(cudaEventRecord(down_all, cs.down), "cudaEventRecord");
+    for (int i = 0; i < nup && s == PL_OK; ++i) {
+        cudaEvent_t up_all;
+        if ((s = make_event(&up_all)) != PL_OK) break;
+        s = cuda_fail_if(cudaEventRecord(up_all, cs.up[i]), "cudaEventRecord");
         if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, up_all, 0), "cudaStreamWaitEvent");
+    }
+    cudaEvent_t down_all;
+    if (s == PL_OK && (s = make_event(&down_all)) == PL_OK) {
+        s = cuda_fail_if(cudaEventRecord(down_all, cs.down), "cudaEventRecord");
         if (s == PL_OK) s = cuda_fail_if(cudaStreamWaitEvent(st, down_all, 0), "cudaStreamWaitEvent");
     }
     for (cudaEvent_t e : evs) cudaEventDestroy(e);  // destruction is deferred until the event completes
