@@ -36,11 +36,15 @@ $(BUILD)/batch.o: $(CSRC)/batch.cu $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/batch.cu
 
+$(BUILD)/blk.o: $(CSRC)/blk.cu $(CSRC)/sz_blk.cuh $(CSRC)/sz_ws.cuh $(CSRC)/ring.cuh $(CSRC)/capi_internal.h include/permlab_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/blk.cu
+
 $(BUILD)/ryser.o: $(CSRC)/ryser.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh include/permlab_b200.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/ryser.cu
 
-$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/batch.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o
+$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/batch.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o $(BUILD)/blk.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c

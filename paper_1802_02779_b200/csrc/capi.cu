@@ -833,6 +833,22 @@ pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, vo
             return run_layers_batch<decltype(r)>(n, count, a_dev, out_dev, status_dev, st, held);
         });
     }
+    if (plc::blk_supported(dt, n)) {
+        // float rings: the register-blocked engine (sz_blk.cuh), one launch per super-layer
+        ScratchBlock blk;
+        pl_status s = scratch_acquire_on(plc::blk_scratch_bytes(dt, n), st, &blk);
+        if (s != PL_OK) return s;
+        for (int64_t b = 0; b < count && s == PL_OK; ++b) {
+            s = plc::run_blocks(dt, fma, n, static_cast<const char*>(a_dev) + (size_t)b * n * n * es,
+                                static_cast<char*>(out_dev) + (size_t)b * es, blk.ptr, status_dev, st);
+        }
+        if (held) {
+            *held = blk;
+            return s;
+        }
+        const pl_status s2 = scratch_release_on_stream(blk, st);
+        return s != PL_OK ? s : s2;
+    }
     // Head: tile tickets of every layer (64 words) and the int64 guard flag.
     // Layer buffers carry 64 bytes of slack: 8-byte rings stage 16-byte aligned
     // spans that may read one element past a layer's last entry.
@@ -1258,6 +1274,7 @@ void pl_release_scratch(void) {
             cudaFree(kv.second.buf);
         }
         lists_cache().clear();
+        plc::blk_release_tables();  // every device was synchronised above (or has no tables)
     }
     cudaSetDevice(cur);
     cudaGetLastError();

@@ -52,6 +52,13 @@ struct ScratchBlock {
 };
 pl_status scratch_get(size_t bytes, cudaStream_t st, ScratchBlock* out);
 pl_status scratch_put(const ScratchBlock& b, cudaStream_t st);
+// Register-blocked layer engine for one large float matrix (blk.cu, sz_blk.cuh):
+// `scratch` of blk_scratch_bytes() bytes, 256-byte aligned.
+bool blk_supported(pl_dtype dt, int n);
+size_t blk_scratch_bytes(pl_dtype dt, int n);
+pl_status run_blocks(pl_dtype dt, bool fma, int n, const void* a_dev, void* out_dev, void* scratch, int32_t* status,
+                     cudaStream_t st);
+void blk_release_tables();
 // The multi-GPU path (multi.cu): limits->num_gpus >= 1, devices NULL = 0..g-1.
 pl_status run_multi(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,
                     const pl_limits* lim, const int32_t* devices, cudaStream_t caller);

@@ -564,3 +564,56 @@ def test_round2_kernels_repeatable():
     f = rng.uniform(-1, 1, (23, 23))
     v = {struct.pack(">d", pl.store_zechin_permanent(f).value) for _ in range(4)}
     assert v == {struct.pack(">d", O.sz_f64(f))}
+
+
+_BLK_SCRIPT = r"""
+import sys, json
+import numpy as np
+import paper_1802_02779_b200 as pl
+from paper_1802_02779_b200 import configs
+out = {}
+for n in (15, 16, 19, 21):
+    a = configs.uniform((n, n), seed=3000 + n)
+    out["f%d" % n] = float(pl.store_zechin_permanent(a).value).hex()
+    out["F%d" % n] = float(pl.store_zechin_permanent(a, fma=True).value)
+    c = configs.complex_uniform((n, n), seed=2000 + n)
+    v = complex(pl.store_zechin_permanent(c).value)
+    out["c%d" % n] = [v.real.hex(), v.imag.hex()]
+z = configs.uniform((16, 16), seed=5)
+z[3] = 0.0
+z[:, 7] = -0.0
+out["zero"] = float(pl.store_zechin_permanent(z).value).hex()
+a = configs.c4()
+out["c4"] = [float(pl.store_zechin_permanent(a).value).hex() for _ in range(3)]
+print(json.dumps(out))
+"""
+
+
+def test_register_blocked_engine_bitwise():
+    # the opt-in register-blocked engine (sz_blk.cuh, PL_BLK=1): super-layers of
+    # 32- (f64) or 16-value (c128) blocks; bitwise the oracle's fold for single
+    # matrices of every order it takes, repeatable, and C4 equal to the golden value
+    import json
+    import os
+    import sys
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PL_BLK="1", PYTHONPATH=str(root))
+    r = subprocess.run([sys.executable, "-c", _BLK_SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for n in (15, 16, 19, 21):
+        a = configs.uniform((n, n), seed=3000 + n)
+        want = O.sz_f64(a)
+        assert got["f%d" % n] == float(want).hex()
+        assert rel_err(got["F%d" % n], want) <= REL_TOL
+        c = configs.complex_uniform((n, n), seed=2000 + n)
+        w = complex(O.sz_batch(c[None])[0])
+        assert got["c%d" % n] == [w.real.hex(), w.imag.hex()]
+    z = configs.uniform((16, 16), seed=5)
+    z[3] = 0.0
+    z[:, 7] = -0.0
+    assert got["zero"] == float(O.sz_f64(z)).hex()
+    g = json.loads((root / "tests/golden/goldens.json").read_text())
+    assert len(set(got["c4"])) == 1
+    assert struct.pack(">d", float.fromhex(got["c4"][0])).hex() == g["c4"]["value_hex"]
