@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude
 CUDA_HOME ?= /usr/local/cuda
 
-KERNEL_HDRS := $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh $(CSRC)/sz_ws.cuh $(CSRC)/sz_lean.cuh $(CSRC)/sz_batch.cuh $(CSRC)/capi_internal.h include/permlab_b200.h
+KERNEL_HDRS := $(CSRC)/ring.cuh $(CSRC)/sz_kernels.cuh $(CSRC)/sz_ws.cuh $(CSRC)/sz_lean.cuh $(CSRC)/sz_batch.cuh $(CSRC)/capi_internal.h include/permlab_b200.h $(CSRC)/sz_blk.cuh $(CSRC)/sz_batch_blk.cuh
 
 all: $(PKG)/libpermlab_b200.so $(PKG)/libpermlab_gen.so $(PKG)/libpermlab.so tests/cpp/test_permanent_device oracle
 

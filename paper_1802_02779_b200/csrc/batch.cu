@@ -22,6 +22,7 @@
 #include "capi_internal.h"
 #include "sz_batch.cuh"
 #include "sz_kernels.cuh"
+#include "sz_batch_blk.cuh"
 
 namespace {
 
@@ -310,6 +311,39 @@ pl_status launch_f32_pack_n(const void* a, void* out, int64_t count, int32_t* st
     return PL_OK;
 }
 
+// int64, 10 <= n <= 12: the register-blocked FP32-exact pack kernel (sz_batch_blk.cuh);
+// opt-in with PL_BATCH_F32_BLK=1 (measured slower than the subset-per-thread pack kernel
+// above: C3 171 vs 121 us per call, profiles/r2c/NOTES.md).
+bool use_f32_blk() {
+    static const bool on = [] {
+        const char* e = std::getenv("PL_BATCH_F32_BLK");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+template <int N>
+pl_status launch_f32_blk_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st,
+                           const Ptab& pt) {
+    const uint4* wtab = nullptr;
+    pl_status s = plc::blk_wtab(&wtab);
+    if (s != PL_OK) return s;
+    const int maxc = (int)max_layer(N);
+    constexpr size_t smem = pl::f32_blk_smem_bytes<N>();
+    auto kern = pl::sz_batch_f32_blk_kernel<N>;
+    PL_CUDA(set_smem_once(kern, smem));
+    int per_sm = 1;
+    PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kF32BlkThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    const int64_t packs = (count + 3) / 4;
+    const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
+    kern<<<(unsigned)blocks, pl::kF32BlkThreads, smem, st>>>(static_cast<const long long*>(a),
+                                                            static_cast<long long*>(out), count, maxc, pt.tab,
+                                                            pt.off, pt.t32(8), wtab, status);
+    PL_CUDA(cudaGetLastError());
+    return PL_OK;
+}
+
 // Warp-per-matrix kernel for 8-byte rings, 6 <= n <= 9 (PL_BATCH_SMEM=cta forces the CTA
 // kernel). Measured (profiles/c3_ab.py): n = 8 x 50k int64 104 -> 74 us; equal at n = 10;
 // slower at n = 12 (C3: 205 -> 293 us), where a matrix's layers take ~16 KB and a warp per
@@ -368,6 +402,13 @@ pl_status launch_smem(pl_dtype dt, int n, const void* a, void* out, int64_t coun
                         case 11: return launch_f32_pack_n<11, 8>(a, out, count, status, st, pt);
                         case 12: return launch_f32_pack_n<12, 8>(a, out, count, status, st, pt);
                         case 13: return launch_f32_pack_n<13, 8>(a, out, count, status, st, pt);
+                    }
+                }
+                if (n <= 12 && use_f32_blk()) {
+                    switch (n) {
+                        case 10: return launch_f32_blk_n<10>(a, out, count, status, st, pt);
+                        case 11: return launch_f32_blk_n<11>(a, out, count, status, st, pt);
+                        case 12: return launch_f32_blk_n<12>(a, out, count, status, st, pt);
                     }
                 }
                 switch (n) {

@@ -230,6 +230,11 @@ pl_status run_blocks(pl_dtype dt, bool fma, int n, const void* a_dev, void* out_
     return fail_msg(PL_ERR_ARG, "block engine: unsupported dtype");
 }
 
+pl_status blk_wtab(const uint4** out) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    return get_wtab(out);
+}
+
 void blk_release_tables() {
     std::lock_guard<std::mutex> lock(g_mu);
     for (auto& kv : tables_cache()) {

@@ -59,6 +59,9 @@ size_t blk_scratch_bytes(pl_dtype dt, int n);
 pl_status run_blocks(pl_dtype dt, bool fma, int n, const void* a_dev, void* out_dev, void* scratch, int32_t* status,
                      cudaStream_t st);
 void blk_release_tables();
+// Window table of the block kernels (sz_blk.cuh / sz_batch_blk.cuh): for the m-subset V of nine
+// columns of colex rank q, entry t = rank9(V \ {w_t}) | w_t << 7 in 12-bit fields (uint4 per V).
+pl_status blk_wtab(const uint4** out);
 // The multi-GPU path (multi.cu): limits->num_gpus >= 1, devices NULL = 0..g-1.
 pl_status run_multi(pl_dtype dt, int n, int64_t count, const void* a, void* out, uint32_t flags,
                     const pl_limits* lim, const int32_t* devices, cudaStream_t caller);

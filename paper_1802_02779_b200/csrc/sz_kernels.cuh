@@ -687,6 +687,57 @@ __global__ void __launch_bounds__(pack_threads<N>()) sz_batch_smem_pack_kernel(
     }
 }
 
+// Members of a pack that is not jointly FP32-exact: one matrix at a time on the
+// exact-double / int64 / checked-int64 paths (mode[h] from warp_i64_mode_f32).
+template <int N>
+__device__ __forceinline__ void f32_pack_members(const long long* g, int have, const int* mode, int& flag,
+                                                 unsigned char* smem_raw, int maxc, const uint16_t* __restrict__ ptab,
+                                                 const uint32_t* __restrict__ poff,
+                                                 const uint32_t* __restrict__ ptab32_8, long long* __restrict__ out,
+                                                 int64_t b0, int32_t* __restrict__ status) {
+    constexpr int n = N, E = N * N;
+    const int tid = threadIdx.x;
+    for (int h = 0; h < have; ++h) {
+        const long long* gh = g + (size_t)h * E;
+        long long* mat = reinterpret_cast<long long*>(smem_raw);
+        long long* buf0 = mat + ((E + 1) & ~1);
+        long long* buf1 = buf0 + ((maxc + 1) & ~1);
+        for (int e = tid; e < E; e += blockDim.x) mat[e] = gh[e];
+        if (tid == 0) flag = 0;
+        __syncthreads();
+        bool ov = false;
+        long long total = 0;
+        const int md = mode[h];
+        if (md == 0 || md == 3) {
+            double* dm = reinterpret_cast<double*>(mat);
+            for (int e = tid; e < E; e += blockDim.x) dm[e] = (double)mat[e];
+            __syncthreads();
+            const double* last = smem_dp<RF64<true>, double, N>(dm, reinterpret_cast<double*>(buf0),
+                                                                 reinterpret_cast<double*>(buf1), n, ptab,
+                                                                 poff, ptab32_8, ov);
+            if (tid == 0) total = (long long)smem_top<RF64<true>, double, N>(dm, last, n, ov);
+        } else if (md == 1) {
+            const long long* last = smem_dp<RI64<false>, long long, N>(mat, buf0, buf1, n, ptab, poff,
+                                                                       ptab32_8, ov);
+            if (tid == 0) total = smem_top<RI64<false>, long long, N>(mat, last, n, ov);
+        } else {
+            const long long* last = smem_dp<RI64<true>, long long, N>(mat, buf0, buf1, n, ptab, poff,
+                                                                      ptab32_8, ov);
+            if (ov) atomicOr(&flag, 1);
+            __syncthreads();
+            if (tid == 0 && !(flag & 1)) total = smem_top<RI64<true>, long long, N>(mat, last, n, ov);
+        }
+        if (tid == 0) {
+            if ((flag & 1) || ov) {
+                atomicOr(status, 1);
+                total = 0;
+            }
+            out[b0 + h] = total;
+        }
+        __syncthreads();
+    }
+}
+
 // int64 batches, 10 <= n <= 14: four matrices per CTA in lockstep on the FP32
 // pipe when all four are FP32-exact (warp_i64_mode_f32 == 3): a pack is 16
 // bytes (the same byte offsets as a pair of doubles), so a term is one table
@@ -741,45 +792,7 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
                 for (int i = 0; i < P; ++i) out[b0 + i] = (long long)t.v[i];
             }
         } else {
-            for (int h = 0; h < have; ++h) {
-                const long long* gh = g + (size_t)h * E;
-                long long* mat = reinterpret_cast<long long*>(smem_raw);
-                long long* buf0 = mat + ((E + 1) & ~1);
-                long long* buf1 = buf0 + ((maxc + 1) & ~1);
-                for (int e = tid; e < E; e += blockDim.x) mat[e] = gh[e];
-                if (tid == 0) flag = 0;
-                __syncthreads();
-                bool ov = false;
-                long long total = 0;
-                const int md = mode[h];
-                if (md == 0 || md == 3) {
-                    double* dm = reinterpret_cast<double*>(mat);
-                    for (int e = tid; e < E; e += blockDim.x) dm[e] = (double)mat[e];
-                    __syncthreads();
-                    const double* last = smem_dp<RF64<true>, double, N>(dm, reinterpret_cast<double*>(buf0),
-                                                                         reinterpret_cast<double*>(buf1), n, ptab,
-                                                                         poff, ptab32_8, ov);
-                    if (tid == 0) total = (long long)smem_top<RF64<true>, double, N>(dm, last, n, ov);
-                } else if (md == 1) {
-                    const long long* last = smem_dp<RI64<false>, long long, N>(mat, buf0, buf1, n, ptab, poff,
-                                                                               ptab32_8, ov);
-                    if (tid == 0) total = smem_top<RI64<false>, long long, N>(mat, last, n, ov);
-                } else {
-                    const long long* last = smem_dp<RI64<true>, long long, N>(mat, buf0, buf1, n, ptab, poff,
-                                                                              ptab32_8, ov);
-                    if (ov) atomicOr(&flag, 1);
-                    __syncthreads();
-                    if (tid == 0 && !(flag & 1)) total = smem_top<RI64<true>, long long, N>(mat, last, n, ov);
-                }
-                if (tid == 0) {
-                    if ((flag & 1) || ov) {
-                        atomicOr(status, 1);
-                        total = 0;
-                    }
-                    out[b0 + h] = total;
-                }
-                __syncthreads();
-            }
+            f32_pack_members<N>(g, have, mode, flag, smem_raw, maxc, ptab, poff, ptab32_8, out, b0, status);
         }
         __syncthreads();
     }

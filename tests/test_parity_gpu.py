@@ -617,3 +617,28 @@ def test_register_blocked_engine_bitwise():
     g = json.loads((root / "tests/golden/goldens.json").read_text())
     assert len(set(got["c4"])) == 1
     assert struct.pack(">d", float.fromhex(got["c4"][0])).hex() == g["c4"]["value_hex"]
+
+
+def test_blocked_f32_pack_kernel_opt_in():
+    # the opt-in register-blocked FP32-exact pack kernel (sz_batch_blk.cuh,
+    # PL_BATCH_F32_BLK=1) for int64 batches 10 <= n <= 12: exact integers equal to the
+    # oracle's, including packs that fall back member by member and a ragged tail
+    import os
+    import sys
+
+    root = Path(__file__).resolve().parents[1]
+    script = (
+        "import numpy as np, paper_1802_02779_b200 as pl\n"
+        "from paper_1802_02779_b200 import configs\n"
+        "for n in (10, 11, 12):\n"
+        "    a = configs.int_matrices(n, 203, seed=77 + n, lo=-1, hi=2)\n"
+        "    a[5] *= 3\n"
+        "    np.save('/tmp/_blk_f32_%d.npy' % n, pl.store_zechin_permanent_batch(a))\n"
+    )
+    env = dict(os.environ, PL_BATCH_F32_BLK="1", PYTHONPATH=str(root))
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for n in (10, 11, 12):
+        a = configs.int_matrices(n, 203, seed=77 + n, lo=-1, hi=2)
+        a[5] *= 3  # its pack leaves the FP32 bound: member-by-member fallback
+        assert np.array_equal(np.load("/tmp/_blk_f32_%d.npy" % n), O.sz_batch(a))
