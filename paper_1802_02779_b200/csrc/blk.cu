@@ -144,7 +144,8 @@ pl_status run_ring(int n, const void* a_dev, void* out_dev, void* scratch, int32
                  reinterpret_cast<T*>(static_cast<char*>(scratch) + kHead + max_rows * pl::kBlkRowBytes)};
     PLC_CUDA(cudaMemsetAsync(scratch, 0, kHead, st));
     auto kern = pl::sz_blk_kernel<R, LC>;
-    constexpr size_t smem = 2 * (size_t)pl::kBlkWarps * pl::kBlkRowBytes;
+    constexpr size_t smem = (size_t)pl::kBlkWarps * pl::kBlkRowBytes +
+                            (size_t)pl::kBlkWarps * pl::kBlkSlots * pl::BlkRing<T, LC>::kSlotBytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -157,7 +158,7 @@ pl_status run_ring(int n, const void* a_dev, void* out_dev, void* scratch, int32
     }();
     static const int per_sm = [] {
         const char* e = std::getenv("PL_BLK_CTAS");  // tuning: CTAs per SM in the grid
-        return e ? std::max(1, atoi(e)) : 3;
+        return e ? std::max(1, atoi(e)) : 4;
     }();
     static const uint32_t hints = [] {
         const char* e = std::getenv("PL_BLK_HINTS");  // timing probes (wrong results), see sz_blk.cuh

@@ -29,19 +29,23 @@
 // term initialising the accumulator; the non-FMA rings are bitwise equal to it.
 //
 // Storage of a super-layer: tile after tile (increasing F); a tile is padded
-// to whole ROWS of 32 blocks; a row stores its 2^LC x 32 values as [L][lane]
-// (8 KB), so a warp's load of one L of 32 neighbouring blocks is one coalesced
-// 256/512-byte access. tb[j][F] = the tile's first row (blk_tables_kernel).
+// to whole ROWS of 32 blocks; a row stores its 2^LC x 32 values as
+// [position of L][lane] (8 KB), L ordered by level |L| (BlkOrder), so the values
+// one level needs from 32 neighbouring blocks are one contiguous run.
+// tb[j][F] = the tile's first row (blk_tables_kernel).
 //   window terms: the tile's window source = tile (F, j - 1), at most 4 rows
-//                 (32 KB), staged whole in shared memory by one bulk copy,
-//                 double buffered across tiles; gathered by block index from
-//                 the window table (wtab: 9 x 12-bit entries per block);
-//   high terms:   block q of tile (F \ {h}, j - 1): same row and lane, read
-//                 straight from global memory (L2) into registers, a group of
-//                 predecessors ahead of the arithmetic.
-// One CTA = 4 warps = the (at most) 4 rows of a tile; CTAs claim tiles from a
-// ticket counter in increasing F; warp 3 (the lightest row) also prepares the
-// next tile's header and source copy.
+//                 (32 KB), staged whole in shared memory by one bulk copy;
+//                 gathered by block index from the window table (wtab: 9 x
+//                 12-bit entries per block);
+//   high terms:   block q of tile (F \ {h}, j - 1): same row and lane. Each warp
+//                 stages them through its own ring of kBlkSlots shared-memory
+//                 slots: lane 0 issues one bulk copy per (piece of a level,
+//                 stream), three chunks ahead of the reads (version 1 read them
+//                 straight into registers, one group ahead: every group exposed
+//                 an L2 round trip, profiles/r2c/NOTES.md).
+// One CTA = 4 warps = the (at most) 4 rows of a tile, four CTAs per SM; CTAs
+// claim tiles from a ticket counter in increasing F; warp 3 (the lightest row)
+// also prepares the next tile's header.
 #pragma once
 
 #include <cstdint>
@@ -136,36 +140,98 @@ static __global__ void blk_tables_kernel(int H, uint32_t* __restrict__ tb, uint3
 
 // ---------------------------------------------------------------- kernel
 
-template <class T>
-__device__ __forceinline__ T blk_ld_global(const T* p) {
-    if constexpr (sizeof(T) == 16) {
-        double2 v;
-        asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
-        return v;
-    } else {
-        unsigned long long v;
-        asm volatile("ld.global.L1::no_allocate.b64 %0, [%1];\n" : "=l"(v) : "l"(p));
-        return *reinterpret_cast<T*>(&v);
+// In-row order of a block's values: by level |L|, then by L. Level P holds the
+// positions [off[P], off[P + 1]), so the values one level needs from a
+// predecessor block row are one contiguous run (one bulk copy).
+template <int LC>
+struct BlkOrder {
+    int pos[1 << LC];
+    int off[LC + 2];
+};
+template <int LC>
+__host__ __device__ constexpr BlkOrder<LC> blk_order() {
+    BlkOrder<LC> t{};
+    int n = 0;
+    for (int P = 0; P <= LC; ++P) {
+        t.off[P] = n;
+        for (int L = 0; L < (1 << LC); ++L) {
+            int c = 0;
+            for (int b = 0; b < LC; ++b) c += (L >> b) & 1;
+            if (c == P) t.pos[L] = n++;
+        }
     }
+    t.off[LC + 1] = n;
+    return t;
 }
 
-// One level (|L| = P) of a block: val[L] for every L of popcount P.
+// A level is processed in pieces of at most SUB outputs (5 for 8-byte rings, 3
+// for complex): eight pieces per block for both. Piece ip covers the in-row
+// positions [first, first + count): packed 8 bits per piece for the issue side.
+template <int LC>
+struct BlkPieces;
+template <>
+struct BlkPieces<5> {  // counts 1 | 5 | 5 5 | 5 5 | 5 | 1
+    static constexpr uint64_t kFirst = 0x1f1a15100b060100ull;
+    static constexpr uint64_t kCount = 0x0105050505050501ull;
+    static constexpr int kSub = 5;
+};
+template <>
+struct BlkPieces<4> {  // counts 1 | 2 2 | 3 3 | 2 2 | 1
+    static constexpr uint64_t kFirst = 0x0f0d0b0805030100ull;
+    static constexpr uint64_t kCount = 0x0102020303020201ull;
+    static constexpr int kSub = 3;
+};
+constexpr int kBlkPieces = 8;
+constexpr int kBlkSlots = 3;  // stream-ring slots per warp
+
+// The warp's stream ring: slot s holds one (piece, stream) chunk, count x 32
+// values; lane 0 issues the bulk copies kBlkSlots chunks ahead of the reads.
+template <class T, int LC>
+struct BlkRing {
+    static constexpr uint32_t kSlotBytes = BlkPieces<LC>::kSub * 32 * sizeof(T);
+    unsigned char* base;  // this warp's slots
+    uint64_t* full;       // [kBlkSlots]
+    uint32_t slot, par;   // read cursor: slot, phase parity bits per slot
+    int ip, il;           // issue cursor: piece, stream
+    uint32_t left;        // chunks not yet issued
+    uint32_t islot;       // next slot to fill
+};
+
+template <class T, int LC>
+__device__ __forceinline__ void blk_issue(BlkRing<T, LC>& rg, const BlkHdr& h, const T* __restrict__ rowp, int f,
+                                          uint32_t dep) {
+    // lane 0 only. rowp = prev + row r of the tile: stream l's block row is rowp + sb[l] * RE
+    constexpr int RE = (1 << LC) * 32;
+    const uint32_t first = (uint32_t)(BlkPieces<LC>::kFirst >> (8 * rg.ip)) & 0xffu;
+    const uint32_t cnt = (uint32_t)(BlkPieces<LC>::kCount >> (8 * rg.ip)) & 0xffu;
+    const uint32_t bytes = cnt * 32u * (uint32_t)sizeof(T);
+    const T* src = rowp + (size_t)h.sb[rg.il] * RE + first * 32u;
+    uint64_t* bar = rg.full + rg.islot;
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(rg.base + rg.islot * BlkRing<T, LC>::kSlotBytes + dep, src, bytes, bar);
+    rg.islot = rg.islot + 1 == kBlkSlots ? 0 : rg.islot + 1;
+    if (++rg.il == f) {
+        rg.il = 0;
+        ++rg.ip;
+    }
+    --rg.left;
+}
+
+// One piece of a block: the outputs of level P at in-level ordinals
+// [O0, O0 + CN): register terms, window terms, then the high terms from the
+// stream ring, in this order per output (ascending columns).
 //   ar      a(j + P - 1, .) in shared memory
 //   row0    the level's row is 0: a single-column subset, per = a(0, c)
 //   pr[t]   window predecessor t: byte offset of its block in the source | column << 20
-//   srcb    the tile's window source in shared memory
-//   sp      prev + lane (+ row r): stream tile l's block is at sp + sb[l] * ROW
-template <class R, int LC, int P, class T>
-__device__ __forceinline__ void blk_level(T (&val)[1 << LC], const T* __restrict__ ar, bool row0, int m,
+template <class R, int LC, int P, int O0, int CN, class T>
+__device__ __forceinline__ void blk_piece(T (&val)[1 << LC], const T* __restrict__ ar, bool row0, int m,
                                           const uint32_t (&pr)[kBlkDW], const unsigned char* __restrict__ srcb, int f,
-                                          const BlkHdr& h, const T* __restrict__ sp, bool& ov) {
+                                          const BlkHdr& h, BlkRing<T, LC>& rg, const T* __restrict__ rowp, int lane,
+                                          uint32_t rt_zero, bool& ov) {
     constexpr int NL = 1 << LC;
-    constexpr uint32_t LSTRIDE = 32 * sizeof(T);  // bytes between consecutive L of one block
-    constexpr int CNT = (int)binom_u64(LC, P);
-    // predecessors per group of stream loads (issued one group ahead)
-    // (at most 10 8-byte or 6 16-byte values per group: two groups live in registers)
-    constexpr int GV = sizeof(T) == 16 ? 6 : 10;
-    constexpr int UL = GV / CNT >= 4 ? 4 : (GV / CNT >= 1 ? GV / CNT : 1);
+    constexpr uint32_t LSTRIDE = 32 * sizeof(T);  // bytes between consecutive in-row positions
+    constexpr BlkOrder<LC> ord = blk_order<LC>();
+    constexpr int P0 = ord.off[P] + O0;  // first in-row position of the piece
     // register terms
     if constexpr (P >= 1) {
         T cl[LC];
@@ -173,7 +239,7 @@ __device__ __forceinline__ void blk_level(T (&val)[1 << LC], const T* __restrict
         for (int v = 0; v < LC; ++v) cl[v] = ar[v];
 #pragma unroll
         for (int L = 0; L < NL; ++L) {
-            if (__builtin_popcount(L) != P) continue;
+            if (ord.pos[L] < P0 || ord.pos[L] >= P0 + CN) continue;
             bool first = true;
 #pragma unroll
             for (int v = 0; v < LC; ++v) {
@@ -199,82 +265,67 @@ __device__ __forceinline__ void blk_level(T (&val)[1 << LC], const T* __restrict
         const unsigned char* p = srcb + (pr[t] & 0xfffffu);
 #pragma unroll
         for (int L = 0; L < NL; ++L) {
-            if (__builtin_popcount(L) != P) continue;
-            const T x = *reinterpret_cast<const T*>(p + L * LSTRIDE);
+            if (ord.pos[L] < P0 || ord.pos[L] >= P0 + CN) continue;
+            const T x = *reinterpret_cast<const T*>(p + ord.pos[L] * LSTRIDE);
             if (P == 0 && t == 0)
                 val[L] = row0 ? c : R::mul(c, x, ov);
             else
                 val[L] = R::mac(val[L], c, x, ov);
         }
     }
-    // high terms: groups of UL predecessors, the next group's loads in flight
-    if (f > 0) {
-        T nx[UL][CNT];
-        auto issue = [&](int l0) {
+    // high terms: chunk (piece, l) from the ring
+    for (int l = 0; l < f; ++l) {
+        const T c = ar[h.hcol[l]];
+        mbar_wait(rg.full + rg.slot, (rg.par >> rg.slot) & 1u);
+        const unsigned char* sp = rg.base + rg.slot * BlkRing<T, LC>::kSlotBytes + lane * sizeof(T);
+        T xs[CN];
 #pragma unroll
-            for (int u = 0; u < UL; ++u) {
-                if (l0 + u < f) {
-                    const T* p = sp + (size_t)h.sb[l0 + u] * (NL * 32);
-                    int o = 0;
+        for (int o = 0; o < CN; ++o) xs[o] = *reinterpret_cast<const T*>(sp + o * LSTRIDE);
+        // the slot is refilled only after this warp's loads have returned (loaded_dep, sz_ws.cuh)
+        const uint32_t dep = loaded_dep(xs, CN, rt_zero);
+        rg.par ^= 1u << rg.slot;
+        rg.slot = rg.slot + 1 == kBlkSlots ? 0 : rg.slot + 1;
+        if (lane == 0 && rg.left) blk_issue<T, LC>(rg, h, rowp, f, dep);
+        int o = 0;
 #pragma unroll
-                    for (int L = 0; L < NL; ++L) {
-                        if (__builtin_popcount(L) != P) continue;
-                        nx[u][o++] = blk_ld_global(p + L * 32);
-                    }
-                }
-            }
-        };
-        issue(0);
-        for (int l0 = 0; l0 < f; l0 += UL) {
-            T cx[UL][CNT];
-            T cc[UL];
-#pragma unroll
-            for (int u = 0; u < UL; ++u) {
-#pragma unroll
-                for (int o = 0; o < CNT; ++o) cx[u][o] = nx[u][o];
-                cc[u] = ar[h.hcol[min(l0 + u, f - 1)]];
-            }
-            issue(l0 + UL);
-#pragma unroll
-            for (int u = 0; u < UL; ++u) {
-                if (l0 + u < f) {
-                    int o = 0;
-#pragma unroll
-                    for (int L = 0; L < NL; ++L) {
-                        if (__builtin_popcount(L) != P) continue;
-                        if (P == 0 && m == 0 && l0 + u == 0)
-                            val[L] = row0 ? cc[u] : R::mul(cc[u], cx[u][o], ov);
-                        else
-                            val[L] = R::mac(val[L], cc[u], cx[u][o], ov);
-                        ++o;
-                    }
-                }
-            }
+        for (int L = 0; L < NL; ++L) {
+            if (ord.pos[L] < P0 || ord.pos[L] >= P0 + CN) continue;
+            if (P == 0 && m == 0 && l == 0)
+                val[L] = row0 ? c : R::mul(c, xs[o], ov);
+            else
+                val[L] = R::mac(val[L], c, xs[o], ov);
+            ++o;
         }
     }
 }
 
 template <class R, int LC>
-__global__ void __launch_bounds__(32 * kBlkWarps, 3)
+__global__ void __launch_bounds__(32 * kBlkWarps, 4)
     sz_blk_kernel(const typename R::T* __restrict__ a, int n, int j, const typename R::T* __restrict__ prev,
                   typename R::T* __restrict__ cur, typename R::T* __restrict__ out, uint32_t* __restrict__ ticket,
                   const uint32_t* __restrict__ flist, uint32_t ntiles, const uint32_t* __restrict__ tb_cur,
                   const uint32_t* __restrict__ tb_prev, const uint4* __restrict__ wtab, int32_t* __restrict__ status,
                   uint32_t hints) {
     using T = typename R::T;
+    using Ring = BlkRing<T, LC>;
     constexpr int NL = 1 << LC;
     constexpr int RE = NL * 32;  // elements per row
+    constexpr BlkOrder<LC> ord = blk_order<LC>();
     static_assert(RE * sizeof(T) == kBlkRowBytes, "row size");
-    extern __shared__ __align__(128) unsigned char blk_smem[];  // two window sources, 4 rows each
+    // dynamic shared memory: the tile's window source (4 rows), then the warps' stream rings
+    extern __shared__ __align__(128) unsigned char blk_smem[];
     __shared__ BlkHdr hdr[2];
-    __shared__ __align__(8) uint64_t full[2];
+    __shared__ __align__(8) uint64_t src_full;
+    __shared__ __align__(8) uint64_t ring_full[kBlkWarps][kBlkSlots];
     __shared__ T arow[LC + 1][kMaxOrder];  // a(j + p - 1, .), p = 0 .. LC
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* srcb = blk_smem;
 
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+        mbar_init(&src_full, 1);
+        for (int w = 0; w < kBlkWarps; ++w)
+            for (int s = 0; s < kBlkSlots; ++s) mbar_init(&ring_full[w][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     for (int e = threadIdx.x; e < (LC + 1) * n; e += blockDim.x) {
@@ -286,7 +337,7 @@ __global__ void __launch_bounds__(32 * kBlkWarps, 3)
 
     // producer state (warp 3): the next tile to publish
     uint32_t t_next = 0, F_next = 0;
-    auto publish = [&](int b) {  // whole warp 3
+    auto publish = [&](int b) {  // whole warp 3: header of the next tile
         const uint32_t t = __shfl_sync(0xffffffffu, t_next, 0);
         BlkHdr& h = hdr[b];
         if (t >= ntiles) {
@@ -306,14 +357,8 @@ __global__ void __launch_bounds__(32 * kBlkWarps, 3)
             h.nb = blk_c9(m);
             h.nrows = blk_rows9(m);
             h.cur_row = __ldg(tb_cur + F);
-            const uint32_t sbytes = m >= 1 ? blk_rows9(m - 1) * kBlkRowBytes : 0u;
-            h.src_bytes = sbytes;
-            if (sbytes) {
-                const uint32_t srow = __ldg(tb_prev + F);
-                h.src_row = srow;
-                mbar_arrive_expect_tx(&full[b], sbytes);
-                bulk_g2s(blk_smem + (size_t)b * kBlkWarps * kBlkRowBytes, prev + (size_t)srow * RE, sbytes, &full[b]);
-            }
+            h.src_bytes = m >= 1 ? blk_rows9(m - 1) * kBlkRowBytes : 0u;
+            h.src_row = m >= 1 ? __ldg(tb_prev + F) : 0u;
             // claim the tile after
             t_next = atomicAdd(ticket, 1u);
             F_next = t_next < ntiles ? __ldg(flist + t_next) : 0u;
@@ -327,22 +372,43 @@ __global__ void __launch_bounds__(32 * kBlkWarps, 3)
         publish(0);
     }
 
+    Ring rg;
+    rg.base = blk_smem + kBlkWarps * kBlkRowBytes + (size_t)warp * kBlkSlots * Ring::kSlotBytes;
+    rg.full = &ring_full[warp][0];
+    rg.slot = 0;
+    rg.par = 0;
+    rg.islot = 0;
+    const uint32_t rt_zero = hints >> 31;  // bit 31 is never set
     bool ov = false;
-    uint32_t phbits = 0;
+    uint32_t src_phase = 0;
     for (uint32_t i = 0;; ++i) {
         const int b = (int)(i & 1u);
-        __syncthreads();  // tile i - 1 done everywhere (its source buffer is free); hdr[b] visible
+        __syncthreads();  // tile i - 1 done everywhere (the source buffer is free); hdr[b] visible
         const BlkHdr& h = hdr[b];
         if (h.m < 0) break;
         const int m = (hints & 2u) ? 0 : h.m;  // hints bit 1: timing probe without the window terms
-        if (warp == 3) publish(b ^ 1);
         const bool has_src = h.src_bytes != 0;
+        if (threadIdx.x == 96 && has_src) {
+            mbar_arrive_expect_tx(&src_full, h.src_bytes);
+            bulk_g2s(srcb, prev + (size_t)h.src_row * RE, h.src_bytes, &src_full);
+        }
+        if (warp == 3) publish(b ^ 1);
         if ((uint32_t)warp < h.nrows) {
             const int f = (hints & 1u) ? 0 : h.f;  // hints bit 0: timing probe without the high terms
             const uint32_t nb = h.nb;
             const uint32_t q = (uint32_t)warp * 32u + (uint32_t)lane;
             const bool valid = q < nb;
             const uint32_t qc = valid ? q : nb - 1u;
+            const T* rowp = prev + (size_t)warp * RE + lane;
+            // start the stream ring: the first chunks of this row
+            rg.ip = 0;
+            rg.il = 0;
+            rg.left = (uint32_t)(kBlkPieces * f);
+            if (lane == 0) {
+#pragma unroll
+                for (int s = 0; s < kBlkSlots; ++s)
+                    if (rg.left) blk_issue<T, LC>(rg, h, rowp - lane, f, 0u);
+            }
             uint32_t pr[kBlkDW];
             if (m >= 1) {
                 const uint4 e = __ldg(wtab + blk_moff9(m) + qc);
@@ -357,41 +423,56 @@ __global__ void __launch_bounds__(32 * kBlkWarps, 3)
 #pragma unroll
                 for (int t = 0; t < kBlkDW; ++t) pr[t] = 0;
             }
-            const unsigned char* srcb = blk_smem + (size_t)b * kBlkWarps * kBlkRowBytes;
-            const T* sp = prev + (size_t)warp * RE + lane;
             T* dst = cur + ((size_t)h.cur_row + warp) * RE + lane;
-            if (has_src) mbar_wait(&full[b], (phbits >> b) & 1u);
+            if (has_src) mbar_wait(&src_full, src_phase);
             T val[NL];
             auto store_level = [&](int P) {
                 if (valid) {
 #pragma unroll
                     for (int L = 0; L < NL; ++L)
-                        if (__builtin_popcount(L) == P) dst[L * 32] = val[L];
+                        if (__builtin_popcount(L) == P) dst[ord.pos[L] * 32] = val[L];
                 }
             };
+#define PL_BLK_PIECE(P, O0, CN, R0) \
+    blk_piece<R, LC, P, O0, CN>(val, arow[P], R0, m, pr, srcb, f, h, rg, rowp - lane, lane, rt_zero, ov)
             // level 0 (j = 0: the empty set, never used as a factor: row0 below)
             if (j == 0) {
                 val[0] = R::zero();
             } else {
-                blk_level<R, LC, 0>(val, arow[0], j == 1, m, pr, srcb, f, h, sp, ov);
+                PL_BLK_PIECE(0, 0, 1, j == 1);
             }
             store_level(0);
-            blk_level<R, LC, 1>(val, arow[1], j == 0, m, pr, srcb, f, h, sp, ov);
-            store_level(1);
-            blk_level<R, LC, 2>(val, arow[2], false, m, pr, srcb, f, h, sp, ov);
-            store_level(2);
-            blk_level<R, LC, 3>(val, arow[3], false, m, pr, srcb, f, h, sp, ov);
-            store_level(3);
-            blk_level<R, LC, 4>(val, arow[4], false, m, pr, srcb, f, h, sp, ov);
-            store_level(4);
-            if constexpr (LC >= 5) {
-                blk_level<R, LC, 5>(val, arow[LC >= 5 ? 5 : 0], false, m, pr, srcb, f, h, sp, ov);
+            if constexpr (LC == 5) {
+                PL_BLK_PIECE(1, 0, 5, j == 0);
+                store_level(1);
+                PL_BLK_PIECE(2, 0, 5, false);
+                PL_BLK_PIECE(2, 5, 5, false);
+                store_level(2);
+                PL_BLK_PIECE(3, 0, 5, false);
+                PL_BLK_PIECE(3, 5, 5, false);
+                store_level(3);
+                PL_BLK_PIECE(4, 0, 5, false);
+                store_level(4);
+                PL_BLK_PIECE(5, 0, 1, false);
                 store_level(5);
+            } else {
+                PL_BLK_PIECE(1, 0, 2, j == 0);
+                PL_BLK_PIECE(1, 2, 2, j == 0);
+                store_level(1);
+                PL_BLK_PIECE(2, 0, 3, false);
+                PL_BLK_PIECE(2, 3, 3, false);
+                store_level(2);
+                PL_BLK_PIECE(3, 0, 2, false);
+                PL_BLK_PIECE(3, 2, 2, false);
+                store_level(3);
+                PL_BLK_PIECE(4, 0, 1, false);
+                store_level(4);
             }
+#undef PL_BLK_PIECE
             // the last super-layer is the single block of every column: its top value is the permanent
             if (j == n - LC && q == 0) out[0] = val[NL - 1];
         }
-        if (has_src) phbits ^= 1u << b;
+        if (has_src) src_phase ^= 1u;
     }
     if (ov) atomicOr(status, 1);
 }
