@@ -62,13 +62,18 @@ constexpr uint32_t kBlkRowBytes = 8192;
 constexpr uint32_t kBlkInvalid = 0xffffffffu;
 
 __host__ __device__ constexpr int blk_reg_cols(int elem_bytes) { return elem_bytes == 16 ? 4 : 5; }
-__host__ __device__ constexpr uint32_t blk_c9(int m) { return m < 0 || m > 9 ? 0u : (uint32_t)binom_u64(9, m); }
-__host__ __device__ constexpr uint32_t blk_rows9(int m) { return (blk_c9(m) + 31u) / 32u; }
-// first wtab entry of the m-subsets of the window
-__host__ __device__ constexpr uint32_t blk_moff9(int m) {
-    uint32_t s = 0;
-    for (int i = 0; i < m; ++i) s += blk_c9(i);
-    return s;
+// C(9, m), rows of 32 blocks per tile, first wtab entry of the m-subsets of the window:
+// 4-, 4- and 10-bit fields of packed constants (a run-time binomial loop was 7 % of the
+// kernel's instructions, profiles/r2c)
+__host__ __device__ constexpr uint32_t blk_c9(int m) {  // 1 9 36 84 126 126 84 36 9 1
+    return m < 0 || m > 9 ? 0u : (uint32_t)((0x7e54240901ull >> (8 * (m > 4 ? 9 - m : m))) & 0xffu);
+}
+__host__ __device__ constexpr uint32_t blk_rows9(int m) {  // 1 1 2 3 4 4 3 2 1 1
+    return m < 0 || m > 9 ? 0u : (uint32_t)((0x1123443211ull >> (4 * m)) & 0xfu);
+}
+__host__ __device__ constexpr uint32_t blk_moff9(int m) {  // 0 1 10 46 130 256 | 382 466 502 511 512
+    return m < 6 ? (uint32_t)((0x400820b80a00400ull >> (10 * (m < 0 ? 0 : m))) & 0x3ffu)
+                 : (uint32_t)((0x2007fdf67497eull >> (10 * ((m > 10 ? 10 : m) - 6))) & 0x3ffu);
 }
 
 struct BlkHdr {
@@ -182,7 +187,10 @@ struct BlkPieces<4> {  // counts 1 | 2 2 | 3 3 | 2 2 | 1
     static constexpr int kSub = 3;
 };
 constexpr int kBlkPieces = 8;
-constexpr int kBlkSlots = 3;  // stream-ring slots per warp
+#ifndef PL_BLK_SLOTS
+#define PL_BLK_SLOTS 3
+#endif
+constexpr int kBlkSlots = PL_BLK_SLOTS;  // stream-ring slots per warp
 
 // The warp's stream ring: slot s holds one (piece, stream) chunk, count x 32
 // values; lane 0 issues the bulk copies kBlkSlots chunks ahead of the reads.
@@ -299,8 +307,11 @@ __device__ __forceinline__ void blk_piece(T (&val)[1 << LC], const T* __restrict
     }
 }
 
+#ifndef PL_BLK_MINCTAS
+#define PL_BLK_MINCTAS 4
+#endif
 template <class R, int LC>
-__global__ void __launch_bounds__(32 * kBlkWarps, 4)
+__global__ void __launch_bounds__(32 * kBlkWarps, PL_BLK_MINCTAS)
     sz_blk_kernel(const typename R::T* __restrict__ a, int n, int j, const typename R::T* __restrict__ prev,
                   typename R::T* __restrict__ cur, typename R::T* __restrict__ out, uint32_t* __restrict__ ticket,
                   const uint32_t* __restrict__ flist, uint32_t ntiles, const uint32_t* __restrict__ tb_cur,
