@@ -473,15 +473,38 @@ __device__ __forceinline__ uint32_t ltab_entry(const uint4& a, const uint4& b, i
     return (i & 1) ? word >> 16 : word & 0xffffu;
 }
 
+// Low-term coefficient a(k-1, v). PL_WS_COEF_SPLIT=1 (build-time experiment,
+// round 2c): complex rows kept as two double arrays (re[32], im[32]) and read
+// by two 8-byte loads -- 14 columns x 8 bytes fall in distinct banks, whereas a
+// gathered 16-byte load makes columns v and v + 8 collide within a quarter
+// warp. Measured equal on C5 (110.6-111.2 ms either way, profiles/r2c/
+// coef_split.txt): the saved bank conflicts cost one more issue slot per low term.
+#ifndef PL_WS_COEF_SPLIT
+#define PL_WS_COEF_SPLIT 0
+#endif
+template <class T>
+__device__ __forceinline__ T ws_coef_low(const T* __restrict__ row_low, uint32_t v) {
+    if constexpr (sizeof(T) == 16 && PL_WS_COEF_SPLIT) {
+        const double* p = reinterpret_cast<const double*>(row_low);
+        T c;
+        c.x = p[v];
+        c.y = p[32 + v];
+        return c;
+    } else {
+        return row_low[v];
+    }
+}
+
 template <class RR, int M, class T>
 __device__ __forceinline__ T ws_low(const uint4& ea, const uint4& eb, const T* __restrict__ src,
                                     const T* __restrict__ row_low, bool& ov) {
     T x[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) x[i] = src[ltab_entry(ea, eb, i) & ((1u << kWsLtabRankBits) - 1)];
-    T acc = RR::mul(row_low[ltab_entry(ea, eb, 0) >> kWsLtabRankBits], x[0], ov);
+    T acc = RR::mul(ws_coef_low(row_low, ltab_entry(ea, eb, 0) >> kWsLtabRankBits), x[0], ov);
 #pragma unroll
-    for (int i = 1; i < M; ++i) acc = RR::mac(acc, row_low[ltab_entry(ea, eb, i) >> kWsLtabRankBits], x[i], ov);
+    for (int i = 1; i < M; ++i)
+        acc = RR::mac(acc, ws_coef_low(row_low, ltab_entry(ea, eb, i) >> kWsLtabRankBits), x[i], ov);
     return acc;
 }
 
@@ -498,7 +521,7 @@ __device__ __forceinline__ void ws_low_interleaved(const uint4 (&ea)[PER], const
         for (int p = 0; p < PER; ++p) {
             const uint32_t e = ltab_entry(ea[p], eb[p], i);
             const T x = src[e & ((1u << kWsLtabRankBits) - 1)];
-            const T c = row_low[e >> kWsLtabRankBits];
+            const T c = ws_coef_low(row_low, e >> kWsLtabRankBits);
             acc[p] = i == 0 ? RR::mul(c, x, ov[p]) : RR::mac(acc[p], c, x, ov[p]);
         }
     }
@@ -691,7 +714,16 @@ __global__ void __launch_bounds__(WsGeom<(int)sizeof(typename R::T)>::kThreads, 
     // read below by TMA bulk copies (async proxy): order the two proxies after
     // the grid-dependency wait.
     if (PL_WS_PROXY_FENCE) asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    for (int v = threadIdx.x; v < D; v += blockDim.x) sm.row_low[v] = row[v];
+    for (int v = threadIdx.x; v < D; v += blockDim.x) {
+        if constexpr (sizeof(T) == 16 && PL_WS_COEF_SPLIT) {
+            double* p = reinterpret_cast<double*>(sm.row_low);
+            const T c = row[v];
+            p[v] = *reinterpret_cast<const double*>(&c);
+            p[32 + v] = *(reinterpret_cast<const double*>(&c) + 1);
+        } else {
+            sm.row_low[v] = row[v];
+        }
+    }
     for (int v = threadIdx.x; v < n; v += blockDim.x) row_sh[v] = row[v];
     __syncthreads();
 
