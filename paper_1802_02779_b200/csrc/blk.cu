@@ -144,7 +144,8 @@ pl_status run_ring(int n, const void* a_dev, void* out_dev, void* scratch, int32
                  reinterpret_cast<T*>(static_cast<char*>(scratch) + kHead + max_rows * pl::kBlkRowBytes)};
     PLC_CUDA(cudaMemsetAsync(scratch, 0, kHead, st));
     auto kern = pl::sz_blk_kernel<R, LC>;
-    constexpr size_t smem = (size_t)pl::kBlkSlots * pl::BlkChunks<T, LC>::kSlotBytes;
+    constexpr size_t smem = (size_t)pl::kBlkWarps * pl::kBlkRowBytes +
+                            (size_t)pl::kBlkWarps * pl::kBlkSlots * pl::BlkRing<T, LC>::kSlotBytes;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -163,16 +164,11 @@ pl_status run_ring(int n, const void* a_dev, void* out_dev, void* scratch, int32
         const char* e = std::getenv("PL_BLK_HINTS");  // timing probes (wrong results), see sz_blk.cuh
         return e ? (uint32_t)std::strtoul(e, nullptr, 0) : 0u;
     }();
-    static const int grid_override = [] {
-        const char* e = std::getenv("PL_BLK_GRID");  // debug: a fixed grid (many tiles per CTA)
-        return e ? std::max(1, atoi(e)) : 0;
-    }();
     const size_t nF = (size_t)1 << tabs->H;
     for (int j = 0; j <= tabs->NW; ++j) {
         const uint32_t ntiles = (uint32_t)(tabs->fl_off[j + 1] - tabs->fl_off[j]);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)std::max<uint32_t>(1, std::min<uint32_t>(ntiles, (uint32_t)(plc::sm_count() * per_sm))));
-        if (grid_override) cfg.gridDim = dim3((unsigned)std::min<uint32_t>(std::max<uint32_t>(ntiles, 1), (uint32_t)grid_override));
         cfg.blockDim = dim3(32 * pl::kBlkWarps);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;

@@ -49,7 +49,6 @@
 #pragma once
 
 #include <cstdint>
-#include <cstdio>
 
 #include "ring.cuh"
 #include "sz_ws.cuh"  // mbarrier / bulk-copy PTX helpers
@@ -78,9 +77,8 @@ __host__ __device__ constexpr uint32_t blk_moff9(int m) {  // 0 1 10 46 130 256 
 }
 
 struct BlkHdr {
-    int32_t m, f;  // window / high terms used (m < 0: no more tiles)
-    uint32_t nb, nrows, nsrc_rows, cur_row, src_row;
-    uint32_t g0, nch;           // the tile's chunks in the CTA's chunk sequence: [g0, g0 + nch)
+    int32_t m, f;  // m < 0: no more tiles
+    uint32_t nb, nrows, cur_row, src_row, src_bytes;
     uint32_t sb[kBlkMaxHigh];   // first row of the stream tile (F \ {F_l}, j - 1)
     uint8_t hcol[kBlkMaxHigh];  // column of F_l
 };
@@ -190,126 +188,58 @@ struct BlkPieces<4> {  // counts 1 | 2 2 | 3 3 | 2 2 | 1
 };
 constexpr int kBlkPieces = 8;
 #ifndef PL_BLK_SLOTS
-#define PL_BLK_SLOTS 4
+#define PL_BLK_SLOTS 3
 #endif
-constexpr int kBlkSlots = PL_BLK_SLOTS;  // chunk-ring slots per CTA
-constexpr int kBlkHdrs = 4;              // tile headers in flight per CTA
+constexpr int kBlkSlots = PL_BLK_SLOTS;  // stream-ring slots per warp
 
-// A chunk: the values of one piece (<= kSub in-row positions) of every row of
-// one predecessor tile -- contiguous in the tile-major layout [position][row][lane]
-// -- staged by one bulk copy. The chunks of a tile, in the order they are read:
-// per piece, the window source (tile (F, j - 1), if the tile has window terms),
-// then the stream tiles l = 0 .. f - 1.
+// The warp's stream ring: slot s holds one (piece, stream) chunk, count x 32
+// values; lane 0 issues the bulk copies kBlkSlots chunks ahead of the reads.
 template <class T, int LC>
-struct BlkChunks {
-    static constexpr uint32_t kSlotBytes = BlkPieces<LC>::kSub * kBlkWarps * 32 * sizeof(T);
+struct BlkRing {
+    static constexpr uint32_t kSlotBytes = BlkPieces<LC>::kSub * 32 * sizeof(T);
+    unsigned char* base;  // this warp's slots
+    uint64_t* full;       // [kBlkSlots]
+    uint32_t slot, par;   // read cursor: slot, phase parity bits per slot
+    int ip, il;           // issue cursor: piece, stream
+    uint32_t left;        // chunks not yet issued
+    uint32_t islot;       // next slot to fill
 };
 
-// Shared state of the CTA's chunk ring.
-struct BlkRingSh {
-    uint64_t full[kBlkSlots];  // chunk landed (transaction bytes)
-    uint32_t readers[kBlkSlots];  // warps that have finished reading the slot's chunk
-    uint64_t hdr_full[kBlkHdrs];   // header published (publisher arrives)
-    uint64_t hdr_empty[kBlkHdrs];  // every warp has left the tile (kBlkWarps arrivals)
-};
-
-// mbarrier wait of the block kernel; -DPL_BLK_DEBUG: a watchdog that reports a wait that never ends.
-__device__ __forceinline__ void blk_wait(uint64_t* bar, unsigned parity, int tag, uint32_t a, uint32_t b) {
-#ifdef PL_BLK_DEBUG
-    for (unsigned long long spins = 0;; ++spins) {
-        if (mbar_test(bar, parity)) return;
-        if (spins == 50000000ull && (threadIdx.x & 31) == 0)
-            printf("blk stuck: cta %d warp %d tag %d a %u b %u parity %u\n", (int)blockIdx.x, (int)(threadIdx.x >> 5), tag,
-                   a, b, parity);
-        if (spins == 200000000ull) __trap();
-    }
-#else
-    (void)tag;
-    (void)a;
-    (void)b;
-    mbar_wait(bar, parity);
-#endif
-}
-
-// Issue chunk gi of the CTA's sequence into its slot (one thread). `ti` is a
-// tile whose header is known to be published and whose chunks start at or
-// before gi; the chunk lies in tile ti or ti + 1 (a tile has 0 or >= 8 chunks).
 template <class T, int LC>
-__device__ __forceinline__ void blk_issue_chunk(uint32_t gi, uint32_t ti, const BlkHdr* hdr, BlkRingSh& rs,
-                                                unsigned char* ring, const T* __restrict__ prev, uint32_t hints) {
+__device__ __forceinline__ void blk_issue(BlkRing<T, LC>& rg, const BlkHdr& h, const T* __restrict__ rowp, int f,
+                                          uint32_t dep) {
+    // lane 0 only. rowp = prev + row r of the tile: stream l's block row is rowp + sb[l] * RE
     constexpr int RE = (1 << LC) * 32;
-    const BlkHdr* h = &hdr[ti % kBlkHdrs];
-    if (h->m < 0) return;  // the CTA has no (more) tiles
-    if (gi >= h->g0 + h->nch) {
-        ++ti;
-        blk_wait(&rs.hdr_full[ti % kBlkHdrs], (ti / kBlkHdrs) & 1u, 1, ti, gi);
-        h = &hdr[ti % kBlkHdrs];
-        if (h->m < 0 || gi >= h->g0 + h->nch) return;  // past the last tile (or an empty one)
+    const uint32_t first = (uint32_t)(BlkPieces<LC>::kFirst >> (8 * rg.ip)) & 0xffu;
+    const uint32_t cnt = (uint32_t)(BlkPieces<LC>::kCount >> (8 * rg.ip)) & 0xffu;
+    const uint32_t bytes = cnt * 32u * (uint32_t)sizeof(T);
+    const T* src = rowp + (size_t)h.sb[rg.il] * RE + first * 32u;
+    uint64_t* bar = rg.full + rg.islot;
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(rg.base + rg.islot * BlkRing<T, LC>::kSlotBytes + dep, src, bytes, bar);
+    rg.islot = rg.islot + 1 == kBlkSlots ? 0 : rg.islot + 1;
+    if (++rg.il == f) {
+        rg.il = 0;
+        ++rg.ip;
     }
-    const uint32_t local = gi - h->g0;
-    const uint32_t s = h->m >= 1 ? 1u : 0u, per = (uint32_t)h->f + s;
-    const uint32_t ip = local / per, idx = local - ip * per;
-    const uint32_t first = (uint32_t)(BlkPieces<LC>::kFirst >> (8 * ip)) & 0xffu;
-    const uint32_t cnt = (uint32_t)(BlkPieces<LC>::kCount >> (8 * ip)) & 0xffu;
-    uint32_t rows, base;
-    bool skip;  // timing probes (hints bit 0: no high terms, bit 1: no window terms): the chunk stays empty
-    if (s && idx == 0) {
-        rows = h->nsrc_rows;
-        base = h->src_row;
-        skip = hints & 2u;
-    } else {
-        rows = h->nrows;
-        base = h->sb[idx - s];
-        skip = hints & 1u;
-    }
-    const uint32_t slot = gi % kBlkSlots;
-    if (skip) {
-        mbar_arrive(&rs.full[slot]);
-        return;
-    }
-    const uint32_t bytes = cnt * rows * 32u * (uint32_t)sizeof(T);
-    const T* src = prev + (size_t)base * RE + (size_t)first * rows * 32u;
-    mbar_arrive_expect_tx(&rs.full[slot], bytes);
-    bulk_g2s(ring + slot * BlkChunks<T, LC>::kSlotBytes, src, bytes, &rs.full[slot]);
+    --rg.left;
 }
 
-// A warp has finished reading chunk g (its loads have returned: `dep` is
-// computed from them, see loaded_dep): the last of the CTA's warps refills the
-// slot with chunk g + kBlkSlots. Every warp passes every chunk, also the warps
-// without a row in the tile (they wait for the chunk and release it unread):
-// a warp that skipped ahead would wait two phases ahead of a slot's barrier,
-// which a one-bit phase parity cannot tell from the phase already completed.
-template <class T, int LC>
-__device__ __forceinline__ void blk_release(uint32_t g, uint32_t ti, uint32_t nrows, const BlkHdr* hdr, BlkRingSh& rs,
-                                            unsigned char* ring, const T* __restrict__ prev, int lane, uint32_t dep,
-                                            uint32_t hints) {
-    if (lane == 0) {
-        const uint32_t slot = g % kBlkSlots;
-        const uint32_t old = atomicAdd(&rs.readers[slot + dep], 1u);
-        if (old + 1u == (uint32_t)kBlkWarps) {
-            rs.readers[slot] = 0;
-            blk_issue_chunk<T, LC>(g + kBlkSlots, ti, hdr, rs, ring, prev, hints);
-        }
-    }
-}
-
-// One piece of a block row: the outputs of level P at in-level ordinals
-// [O0, O0 + CN): register terms, window terms, then the high terms, in this
-// order per output (ascending columns). `g` is the CTA's chunk counter.
+// One piece of a block: the outputs of level P at in-level ordinals
+// [O0, O0 + CN): register terms, window terms, then the high terms from the
+// stream ring, in this order per output (ascending columns).
 //   ar      a(j + P - 1, .) in shared memory
 //   row0    the level's row is 0: a single-column subset, per = a(0, c)
-//   pr[t]   window predecessor t: byte offset of its block inside one position of the source chunk | column << 20
+//   pr[t]   window predecessor t: byte offset of its block in the source | column << 20
 template <class R, int LC, int P, int O0, int CN, class T>
 __device__ __forceinline__ void blk_piece(T (&val)[1 << LC], const T* __restrict__ ar, bool row0, int m,
-                                          const uint32_t (&pr)[kBlkDW], int f, const BlkHdr& h, uint32_t ti,
-                                          const BlkHdr* hdr, BlkRingSh& rs, unsigned char* ring,
-                                          const T* __restrict__ prev, uint32_t& g, int warp, int lane,
-                                          uint32_t hints, bool& ov) {
+                                          const uint32_t (&pr)[kBlkDW], const unsigned char* __restrict__ srcb, int f,
+                                          const BlkHdr& h, BlkRing<T, LC>& rg, const T* __restrict__ rowp, int lane,
+                                          uint32_t rt_zero, bool& ov) {
     constexpr int NL = 1 << LC;
+    constexpr uint32_t LSTRIDE = 32 * sizeof(T);  // bytes between consecutive in-row positions
     constexpr BlkOrder<LC> ord = blk_order<LC>();
     constexpr int P0 = ord.off[P] + O0;  // first in-row position of the piece
-    const uint32_t nrows = h.nrows;
-    const uint32_t rt_zero = hints >> 31;  // bit 31 is never set: a run-time zero (loaded_dep)
     // register terms
     if constexpr (P >= 1) {
         T cl[LC];
@@ -335,53 +265,35 @@ __device__ __forceinline__ void blk_piece(T (&val)[1 << LC], const T* __restrict
             }
         }
     }
-    // window terms: the piece's positions of the source tile, one chunk
-    if (m >= 1) {
-        const uint32_t slot = g % kBlkSlots;
-        blk_wait(&rs.full[slot], (g / kBlkSlots) & 1u, 2, ti, g);
-        const unsigned char* sb = ring + slot * BlkChunks<T, LC>::kSlotBytes;
-        const uint32_t pstride = h.nsrc_rows * 32u * (uint32_t)sizeof(T);  // bytes between positions
+    // window terms (m is uniform over the tile)
 #pragma unroll
-        for (int t = 0; t < kBlkDW; ++t) {
-            if (t >= m || (hints & 2u)) break;
-            const T c = ar[pr[t] >> 20];
-            const unsigned char* p = sb + (pr[t] & 0xfffffu);
-            int o = 0;
-#pragma unroll
-            for (int L = 0; L < NL; ++L) {
-                if (ord.pos[L] < P0 || ord.pos[L] >= P0 + CN) continue;
-                const T x = *reinterpret_cast<const T*>(p + o * pstride);
-                if (P == 0 && t == 0)
-                    val[L] = row0 ? c : R::mul(c, x, ov);
-                else
-                    val[L] = R::mac(val[L], c, x, ov);
-                ++o;
-            }
-        }
-        // every load of the chunk feeds these accumulators
-        uint32_t d = 0;
+    for (int t = 0; t < kBlkDW; ++t) {
+        if (t >= m) break;
+        const T c = ar[pr[t] >> 20];
+        const unsigned char* p = srcb + (pr[t] & 0xfffffu);
 #pragma unroll
         for (int L = 0; L < NL; ++L) {
             if (ord.pos[L] < P0 || ord.pos[L] >= P0 + CN) continue;
-            d ^= *reinterpret_cast<const uint32_t*>(&val[L]);
+            const T x = *reinterpret_cast<const T*>(p + ord.pos[L] * LSTRIDE);
+            if (P == 0 && t == 0)
+                val[L] = row0 ? c : R::mul(c, x, ov);
+            else
+                val[L] = R::mac(val[L], c, x, ov);
         }
-        blk_release<T, LC>(g, ti, nrows, hdr, rs, ring, prev, lane, (uint32_t)(d == 0x9e3779b9u) & rt_zero, hints);
-        ++g;
     }
-    // high terms: chunk (piece, l)
-    const uint32_t rstride = 32u * (uint32_t)sizeof(T);
+    // high terms: chunk (piece, l) from the ring
     for (int l = 0; l < f; ++l) {
         const T c = ar[h.hcol[l]];
-        const uint32_t slot = g % kBlkSlots;
-        blk_wait(&rs.full[slot], (g / kBlkSlots) & 1u, 3, ti, g);
-        const unsigned char* sp =
-            ring + slot * BlkChunks<T, LC>::kSlotBytes + (uint32_t)warp * rstride + (uint32_t)lane * (uint32_t)sizeof(T);
+        mbar_wait(rg.full + rg.slot, (rg.par >> rg.slot) & 1u);
+        const unsigned char* sp = rg.base + rg.slot * BlkRing<T, LC>::kSlotBytes + lane * sizeof(T);
         T xs[CN];
 #pragma unroll
-        for (int o = 0; o < CN; ++o) xs[o] = *reinterpret_cast<const T*>(sp + o * nrows * rstride);
-        blk_release<T, LC>(g, ti, nrows, hdr, rs, ring, prev, lane, loaded_dep(xs, CN, rt_zero), hints);
-        ++g;
-        if (hints & 1u) continue;
+        for (int o = 0; o < CN; ++o) xs[o] = *reinterpret_cast<const T*>(sp + o * LSTRIDE);
+        // the slot is refilled only after this warp's loads have returned (loaded_dep, sz_ws.cuh)
+        const uint32_t dep = loaded_dep(xs, CN, rt_zero);
+        rg.par ^= 1u << rg.slot;
+        rg.slot = rg.slot + 1 == kBlkSlots ? 0 : rg.slot + 1;
+        if (lane == 0 && rg.left) blk_issue<T, LC>(rg, h, rowp, f, dep);
         int o = 0;
 #pragma unroll
         for (int L = 0; L < NL; ++L) {
@@ -406,26 +318,25 @@ __global__ void __launch_bounds__(32 * kBlkWarps, PL_BLK_MINCTAS)
                   const uint32_t* __restrict__ tb_prev, const uint4* __restrict__ wtab, int32_t* __restrict__ status,
                   uint32_t hints) {
     using T = typename R::T;
+    using Ring = BlkRing<T, LC>;
     constexpr int NL = 1 << LC;
     constexpr int RE = NL * 32;  // elements per row
     constexpr BlkOrder<LC> ord = blk_order<LC>();
     static_assert(RE * sizeof(T) == kBlkRowBytes, "row size");
-    extern __shared__ __align__(128) unsigned char ring[];  // kBlkSlots chunk slots
-    __shared__ BlkHdr hdr[kBlkHdrs];
-    __shared__ __align__(8) BlkRingSh rs;
+    // dynamic shared memory: the tile's window source (4 rows), then the warps' stream rings
+    extern __shared__ __align__(128) unsigned char blk_smem[];
+    __shared__ BlkHdr hdr[2];
+    __shared__ __align__(8) uint64_t src_full;
+    __shared__ __align__(8) uint64_t ring_full[kBlkWarps][kBlkSlots];
     __shared__ T arow[LC + 1][kMaxOrder];  // a(j + p - 1, .), p = 0 .. LC
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* srcb = blk_smem;
 
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kBlkSlots; ++s) {
-            mbar_init(&rs.full[s], 1);
-            rs.readers[s] = 0;
-        }
-        for (int s = 0; s < kBlkHdrs; ++s) {
-            mbar_init(&rs.hdr_full[s], 1);
-            mbar_init(&rs.hdr_empty[s], kBlkWarps);
-        }
+        mbar_init(&src_full, 1);
+        for (int w = 0; w < kBlkWarps; ++w)
+            for (int s = 0; s < kBlkSlots; ++s) mbar_init(&ring_full[w][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     for (int e = threadIdx.x; e < (LC + 1) * n; e += blockDim.x) {
@@ -434,92 +345,81 @@ __global__ void __launch_bounds__(32 * kBlkWarps, PL_BLK_MINCTAS)
     }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the previous super-layer is complete and visible
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    __syncthreads();
 
-    // publisher state (warp 3): the next tile to publish, its place in the chunk sequence
-    uint32_t t_next = 0, F_next = 0, g_next = 0, pub = 0;
-    bool pub_end = false;
-    auto publish = [&]() {  // whole warp 3: header of tile `pub`
-        if (pub_end) return;
-        const uint32_t hs = pub % kBlkHdrs;
-        if (pub >= (uint32_t)kBlkHdrs) blk_wait(&rs.hdr_empty[hs], ((pub / kBlkHdrs) - 1u) & 1u, 4, pub, 0u);
+    // producer state (warp 3): the next tile to publish
+    uint32_t t_next = 0, F_next = 0;
+    auto publish = [&](int b) {  // whole warp 3: header of the next tile
         const uint32_t t = __shfl_sync(0xffffffffu, t_next, 0);
-        BlkHdr& h = hdr[hs];
+        BlkHdr& h = hdr[b];
         if (t >= ntiles) {
-            if (lane == 0) {
-                h.m = -1;
-                h.g0 = g_next;
-                h.nch = 0;
-                __threadfence_block();
-                mbar_arrive(&rs.hdr_full[hs]);
-            }
-            pub_end = true;
-            ++pub;
+            if (lane == 0) h.m = -1;
             return;
         }
         const uint32_t F = __shfl_sync(0xffffffffu, F_next, 0);
-        const int fr = __popc(F), mr = j - fr;
-        const int f = fr, m = mr;
-        if (lane < fr) {
+        const int f = __popc(F), m = j - f;
+        if (lane < f) {
             const int bit = __fns(F, 0, lane + 1);
             h.sb[lane] = __ldg(tb_prev + (F & ~(1u << bit)));
             h.hcol[lane] = (uint8_t)(LC + kBlkDW + bit);
         }
-        const uint32_t nch = (uint32_t)kBlkPieces * (uint32_t)(f + (m >= 1 ? 1 : 0));
         if (lane == 0) {
             h.m = m;
             h.f = f;
-            h.nb = blk_c9(mr);
-            h.nrows = blk_rows9(mr);
-            h.nsrc_rows = mr >= 1 ? blk_rows9(mr - 1) : 0u;
+            h.nb = blk_c9(m);
+            h.nrows = blk_rows9(m);
             h.cur_row = __ldg(tb_cur + F);
-            h.src_row = mr >= 1 ? __ldg(tb_prev + F) : 0u;
-            h.g0 = g_next;
-            h.nch = nch;
+            h.src_bytes = m >= 1 ? blk_rows9(m - 1) * kBlkRowBytes : 0u;
+            h.src_row = m >= 1 ? __ldg(tb_prev + F) : 0u;
             // claim the tile after
             t_next = atomicAdd(ticket, 1u);
             F_next = t_next < ntiles ? __ldg(flist + t_next) : 0u;
         }
-        g_next += nch;
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();
-            mbar_arrive(&rs.hdr_full[hs]);
-        }
-        ++pub;
     };
     if (warp == 3) {
         if (lane == 0) {
             t_next = atomicAdd(ticket, 1u);
             F_next = t_next < ntiles ? __ldg(flist + t_next) : 0u;
         }
-        publish();
-        publish();
-        if (lane == 0) {  // start the ring
-            for (uint32_t gi = 0; gi < (uint32_t)kBlkSlots; ++gi)
-                blk_issue_chunk<T, LC>(gi, 0u, hdr, rs, ring, prev, hints);
-        }
-        __syncwarp();
+        publish(0);
     }
 
+    Ring rg;
+    rg.base = blk_smem + kBlkWarps * kBlkRowBytes + (size_t)warp * kBlkSlots * Ring::kSlotBytes;
+    rg.full = &ring_full[warp][0];
+    rg.slot = 0;
+    rg.par = 0;
+    rg.islot = 0;
+    const uint32_t rt_zero = hints >> 31;  // bit 31 is never set
     bool ov = false;
-    for (uint32_t ti = 0;; ++ti) {
-        const uint32_t hs = ti % kBlkHdrs;
-        blk_wait(&rs.hdr_full[hs], (ti / kBlkHdrs) & 1u, 5, ti, 0u);
-        const BlkHdr& h = hdr[hs];
-#ifdef PL_BLK_DEBUG
-        if (lane == 0 && blockIdx.x == 0)
-            printf("cta0 warp %d tile %u: m %d f %d nrows %u g0 %u nch %u\n", warp, ti, h.m, h.f, h.nrows, h.g0, h.nch);
-#endif
+    uint32_t src_phase = 0;
+    for (uint32_t i = 0;; ++i) {
+        const int b = (int)(i & 1u);
+        __syncthreads();  // tile i - 1 done everywhere (the source buffer is free); hdr[b] visible
+        const BlkHdr& h = hdr[b];
         if (h.m < 0) break;
-        if (warp == 3) publish();  // tile ti + 2
+        const int m = (hints & 2u) ? 0 : h.m;  // hints bit 1: timing probe without the window terms
+        const bool has_src = h.src_bytes != 0;
+        if (threadIdx.x == 96 && has_src) {
+            mbar_arrive_expect_tx(&src_full, h.src_bytes);
+            bulk_g2s(srcb, prev + (size_t)h.src_row * RE, h.src_bytes, &src_full);
+        }
+        if (warp == 3) publish(b ^ 1);
         if ((uint32_t)warp < h.nrows) {
-            const int m = h.m, f = h.f;
-            const uint32_t nb = h.nb, nrows = h.nrows;
+            const int f = (hints & 1u) ? 0 : h.f;  // hints bit 0: timing probe without the high terms
+            const uint32_t nb = h.nb;
             const uint32_t q = (uint32_t)warp * 32u + (uint32_t)lane;
             const bool valid = q < nb;
             const uint32_t qc = valid ? q : nb - 1u;
-            uint32_t g = h.g0;
+            const T* rowp = prev + (size_t)warp * RE + lane;
+            // start the stream ring: the first chunks of this row
+            rg.ip = 0;
+            rg.il = 0;
+            rg.left = (uint32_t)(kBlkPieces * f);
+            if (lane == 0) {
+#pragma unroll
+                for (int s = 0; s < kBlkSlots; ++s)
+                    if (rg.left) blk_issue<T, LC>(rg, h, rowp - lane, f, 0u);
+            }
             uint32_t pr[kBlkDW];
             if (m >= 1) {
                 const uint4 e = __ldg(wtab + blk_moff9(m) + qc);
@@ -527,25 +427,25 @@ __global__ void __launch_bounds__(32 * kBlkWarps, PL_BLK_MINCTAS)
 #pragma unroll
                 for (int t = 0; t < kBlkDW; ++t) {
                     const uint32_t fld = (uint32_t)((t < 5 ? lo >> (12 * t) : hi >> (12 * (t - 5))) & 0xfffu);
-                    const uint32_t bi = fld & 127u, w = fld >> 7;  // block bi of the source tile: row bi / 32, lane bi % 32
-                    pr[t] = (bi * (uint32_t)sizeof(T)) | (uint32_t)(LC + w) << 20;
+                    const uint32_t bi = fld & 127u, w = fld >> 7;
+                    pr[t] = ((bi >> 5) * kBlkRowBytes + (bi & 31u) * (uint32_t)sizeof(T)) | (uint32_t)(LC + w) << 20;
                 }
             } else {
 #pragma unroll
                 for (int t = 0; t < kBlkDW; ++t) pr[t] = 0;
             }
-            T* dst = cur + (size_t)h.cur_row * RE + (size_t)warp * 32 + lane;
+            T* dst = cur + ((size_t)h.cur_row + warp) * RE + lane;
+            if (has_src) mbar_wait(&src_full, src_phase);
             T val[NL];
             auto store_level = [&](int P) {
                 if (valid) {
 #pragma unroll
                     for (int L = 0; L < NL; ++L)
-                        if (__builtin_popcount(L) == P) dst[(size_t)ord.pos[L] * nrows * 32] = val[L];
+                        if (__builtin_popcount(L) == P) dst[ord.pos[L] * 32] = val[L];
                 }
             };
-#define PL_BLK_PIECE(P, O0, CN, R0)                                                                              \
-    blk_piece<R, LC, P, O0, CN>(val, arow[P], R0, m, pr, f, h, ti, hdr, rs, ring, prev, g, warp, lane, hints, \
-                                ov)
+#define PL_BLK_PIECE(P, O0, CN, R0) \
+    blk_piece<R, LC, P, O0, CN>(val, arow[P], R0, m, pr, srcb, f, h, rg, rowp - lane, lane, rt_zero, ov)
             // level 0 (j = 0: the empty set, never used as a factor: row0 below)
             if (j == 0) {
                 val[0] = R::zero();
@@ -582,15 +482,8 @@ __global__ void __launch_bounds__(32 * kBlkWarps, PL_BLK_MINCTAS)
 #undef PL_BLK_PIECE
             // the last super-layer is the single block of every column: its top value is the permanent
             if (j == n - LC && q == 0) out[0] = val[NL - 1];
-        } else {
-            // no row in this tile: pass its chunks
-            for (uint32_t g = h.g0; g != h.g0 + h.nch; ++g) {
-                blk_wait(&rs.full[g % kBlkSlots], (g / kBlkSlots) & 1u, 6, ti, g);
-                blk_release<T, LC>(g, ti, h.nrows, hdr, rs, ring, prev, lane, 0u, hints);
-            }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rs.hdr_empty[hs]);
+        if (has_src) src_phase ^= 1u;
     }
     if (ov) atomicOr(status, 1);
 }
