@@ -296,7 +296,8 @@ template <int N, int P>
 pl_status launch_f32_pack_n(const void* a, void* out, int64_t count, int32_t* status, cudaStream_t st,
                             const Ptab& pt) {
     const int maxc = (int)max_layer(N);
-    const size_t smem = (size_t)(N * N + 2 * maxc) * 4 * P + 64;  // 4P-byte packs (the single layout fits inside)
+    // 4P-byte packs (the single layout fits inside) + the byte-packed coefficient words
+    const size_t smem = (size_t)(N * N + 2 * maxc) * 4 * P + (size_t)N * N * 4 + 64;
     auto kern = pl::sz_batch_f32_pack_kernel<N, P>;
     PL_CUDA(set_smem_once(kern, smem));
     int per_sm = 1;

@@ -738,6 +738,71 @@ __device__ __forceinline__ void f32_pack_members(const long long* g, int have, c
     }
 }
 
+// The layer DP of a jointly FP32-exact four-matrix pack whose entries all fit a
+// signed byte (C3's 0/1 matrices and most small-integer batches): the
+// coefficient pack a(k-1, col) is read as ONE 32-bit word of four biased bytes
+// (mat8) instead of a gathered 16-byte load, and expanded exactly: the byte
+// placed in the mantissa of 2^23 gives the float 2^23 + b, minus 2^23 + 128.
+// A 16-byte shared load costs four cycles of the L1TEX data pipe whatever its
+// address pattern, a 4-byte one one cycle; the pack kernel is bound by that
+// pipe (89 % busy, profiles/r2/full_c3.md), not by issue slots.
+__device__ __forceinline__ void f32_coef4(uint32_t w, float (&c)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u + i)) - 8388736.0f;
+}
+
+template <int N, class PT>
+__device__ __forceinline__ const PT* smem_dp_f32c(const PT* mat, const uint32_t* __restrict__ mat8, PT* buf0, PT* buf1,
+                                                  const uint16_t* __restrict__ ptab,
+                                                  const uint32_t* __restrict__ poff,
+                                                  const uint32_t* __restrict__ ptab32) {
+    using PR = PackRing<RF32X, 4>;
+    const int tid = (int)threadIdx.x, nt = (int)blockDim.x;
+    bool ov = false;
+    const uint32_t c2 = poff[3] - poff[2];
+    for (uint32_t r = tid; r < c2; r += nt) {
+        const uint32_t e = __ldg(ptab + poff[2] + r);
+        buf0[r] = base_pair<PR>(mat, N, (int)(e & 0xffu), (int)(e >> 8), ov);
+    }
+    __syncthreads();
+    PT* prev = buf0;
+    PT* cur = buf1;
+#pragma unroll
+    for (int k = 3; k < N; ++k) {
+        const uint32_t ck = (uint32_t)binom_u64(N, k);
+        const uint32_t* pt = ptab32 + poff[k];
+        const uint32_t* row8 = mat8 + (k - 1) * N;
+        const char* pv = reinterpret_cast<const char*>(prev);
+        auto term = [&](PT& acc, uint32_t e, bool first) {
+            float c[4];
+            f32_coef4(row8[e >> 20], c);  // e >> 16 = 16 * column
+            const PT x = *reinterpret_cast<const PT*>(pv + (e & 0xffffu));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc.v[i] = first ? __fmul_rn(c[i], x.v[i]) : __fmaf_rn(c[i], x.v[i], acc.v[i]);
+        };
+        for (uint32_t r = tid; r < ck; r += nt) {
+            PT acc;
+            term(acc, __ldg(pt + r), true);
+            int i = 1;
+            for (; i + 4 <= k; i += 4) {
+                const uint32_t e0 = __ldg(pt + (i + 0) * ck + r), e1 = __ldg(pt + (i + 1) * ck + r);
+                const uint32_t e2 = __ldg(pt + (i + 2) * ck + r), e3 = __ldg(pt + (i + 3) * ck + r);
+                term(acc, e0, false);
+                term(acc, e1, false);
+                term(acc, e2, false);
+                term(acc, e3, false);
+            }
+            for (; i < k; ++i) term(acc, __ldg(pt + i * ck + r), false);
+            cur[r] = acc;
+        }
+        __syncthreads();
+        PT* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    return prev;
+}
+
 // int64 batches, 10 <= n <= 14: four matrices per CTA in lockstep on the FP32
 // pipe when all four are FP32-exact (warp_i64_mode_f32 == 3): a pack is 16
 // bytes (the same byte offsets as a pair of doubles), so a term is one table
@@ -748,6 +813,10 @@ __device__ __forceinline__ void f32_pack_members(const long long* g, int have, c
 #define PL_F32_THREADS 256
 #endif
 constexpr int kF32Threads = PL_F32_THREADS;  // threads per four-matrix pack CTA
+#ifndef PL_F32_BYTE_COEF
+#define PL_F32_BYTE_COEF 1
+#endif
+constexpr bool kF32ByteCoef = PL_F32_BYTE_COEF;  // byte-packed coefficients when every entry fits (smem_dp_f32c)
 
 template <int N, int P>
 __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
@@ -777,15 +846,30 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
             PT* mat = reinterpret_cast<PT*>(smem_raw);
             PT* buf0 = mat + E;
             PT* buf1 = buf0 + maxc;
+            uint32_t* mat8 = reinterpret_cast<uint32_t*>(buf1 + maxc);  // P = 4: biased-byte coefficient packs
+            bool bytes_ok = true;
             for (int e = tid; e < E; e += blockDim.x) {
                 PT x;
+                uint32_t w = 0;
 #pragma unroll
-                for (int i = 0; i < P; ++i) x.v[i] = (float)g[(size_t)i * E + e];
+                for (int i = 0; i < P; ++i) {
+                    const long long v = g[(size_t)i * E + e];
+                    x.v[i] = (float)v;
+                    bytes_ok &= v >= -128 && v <= 127;
+                    if (i < 4) w |= (uint32_t)((v + 128) & 0xff) << (8 * i);
+                }
                 mat[e] = x;
+                if (P == 4 && kF32ByteCoef) mat8[e] = w;
             }
-            __syncthreads();
+            bytes_ok = __syncthreads_and(bytes_ok) != 0;
             bool ov = false;
-            const PT* last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);  // 4P-byte offsets
+            const PT* last;
+            if constexpr (P == 4 && kF32ByteCoef) {
+                last = bytes_ok ? smem_dp_f32c<N, PT>(mat, mat8, buf0, buf1, ptab, poff, ptab32_16)
+                                : smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
+            } else {
+                last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);  // 4P-byte offsets
+            }
             if (tid == 0) {
                 const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
 #pragma unroll
