@@ -175,6 +175,10 @@ struct Ptab {
     uint32_t* off = nullptr;
     uint32_t* tab32[3] = {nullptr, nullptr, nullptr};  // byte-offset entries for 8-, 16- and 32-byte elements
     const uint32_t* t32(size_t es) const { return tab32[es == 32 ? 2 : es == 16 ? 1 : 0]; }
+    // layers >= 3 with two terms per word (the byte-coefficient FP32 packs): word p * C(n,k) + r of
+    // layer k (first word off2[k]) = entry 2p | entry 2p + 1 << 16 of subset r, entries as in `tab`
+    uint32_t* tab2 = nullptr;
+    uint32_t* off2 = nullptr;
 };
 
 // Predecessor table of order n (see sz_batch_smem_kernel), built once per
@@ -222,6 +226,22 @@ pl_status get_ptab(int n, Ptab* out) {
                 t32[x] = (uint32_t)(tab[x] & 0xfffu) * es | ((uint32_t)(tab[x] >> 12) * es) << 16;
         PL_CUDA(cudaMalloc(&p.tab32[w], t32.size() * sizeof(uint32_t)));
         PL_CUDA(cudaMemcpy(p.tab32[w], t32.data(), t32.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    {
+        std::vector<uint32_t> off2(n + 2, 0);
+        for (int k = 3; k <= n; ++k)
+            off2[k + 1] = off2[k] + (k < n ? (uint32_t)(((k + 1) / 2) * pl::binom_u64(n, k)) : 0u);
+        std::vector<uint32_t> t2(off2[n + 1] ? off2[n + 1] : 1, 0);
+        for (int k = 3; k < n; ++k) {
+            const uint64_t ck = pl::binom_u64(n, k);
+            for (int i = 0; i < k; ++i)
+                for (uint64_t r = 0; r < ck; ++r)
+                    t2[off2[k] + (i / 2) * ck + r] |= (uint32_t)tab[off[k] + i * ck + r] << (16 * (i & 1));
+        }
+        PL_CUDA(cudaMalloc(&p.tab2, t2.size() * sizeof(uint32_t)));
+        PL_CUDA(cudaMalloc(&p.off2, off2.size() * sizeof(uint32_t)));
+        PL_CUDA(cudaMemcpy(p.tab2, t2.data(), t2.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        PL_CUDA(cudaMemcpy(p.off2, off2.data(), off2.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
     PL_CUDA(cudaMalloc(&p.tab, tab.size() * sizeof(uint16_t)));
     PL_CUDA(cudaMalloc(&p.off, off.size() * sizeof(uint32_t)));
@@ -307,7 +327,7 @@ pl_status launch_f32_pack_n(const void* a, void* out, int64_t count, int32_t* st
     const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
     kern<<<(unsigned)blocks, pl::kF32Threads, smem, st>>>(static_cast<const long long*>(a),
                                                          static_cast<long long*>(out), count, maxc, pt.tab,
-                                                               pt.off, pt.t32(8), pt.t32(4 * P), status);
+                                                               pt.off, pt.t32(8), pt.t32(4 * P), pt.tab2, pt.off2, status);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

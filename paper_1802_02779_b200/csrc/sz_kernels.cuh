@@ -751,11 +751,14 @@ __device__ __forceinline__ void f32_coef4(uint32_t w, float (&c)[4]) {
     for (int i = 0; i < 4; ++i) c[i] = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u + i)) - 8388736.0f;
 }
 
+// tab2 / off2: the predecessor entries (rank | column << 12) two terms per
+// 32-bit word (batch.cu, Ptab::tab2), so a pair of terms costs one table load.
 template <int N, class PT>
 __device__ __forceinline__ const PT* smem_dp_f32c(const PT* mat, const uint32_t* __restrict__ mat8, PT* buf0, PT* buf1,
                                                   const uint16_t* __restrict__ ptab,
                                                   const uint32_t* __restrict__ poff,
-                                                  const uint32_t* __restrict__ ptab32) {
+                                                  const uint32_t* __restrict__ tab2,
+                                                  const uint32_t* __restrict__ off2) {
     using PR = PackRing<RF32X, 4>;
     const int tid = (int)threadIdx.x, nt = (int)blockDim.x;
     bool ov = false;
@@ -770,29 +773,22 @@ __device__ __forceinline__ const PT* smem_dp_f32c(const PT* mat, const uint32_t*
 #pragma unroll
     for (int k = 3; k < N; ++k) {
         const uint32_t ck = (uint32_t)binom_u64(N, k);
-        const uint32_t* pt = ptab32 + poff[k];
+        const uint32_t* pt = tab2 + off2[k];
         const uint32_t* row8 = mat8 + (k - 1) * N;
-        const char* pv = reinterpret_cast<const char*>(prev);
-        auto term = [&](PT& acc, uint32_t e, bool first) {
+        auto term = [&](PT& acc, uint32_t e, bool first) {  // e = rank | column << 12 (16 bits)
             float c[4];
-            f32_coef4(row8[e >> 20], c);  // e >> 16 = 16 * column
-            const PT x = *reinterpret_cast<const PT*>(pv + (e & 0xffffu));
+            f32_coef4(row8[(e >> 12) & 0xfu], c);
+            const PT x = prev[e & 0xfffu];
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc.v[i] = first ? __fmul_rn(c[i], x.v[i]) : __fmaf_rn(c[i], x.v[i], acc.v[i]);
         };
         for (uint32_t r = tid; r < ck; r += nt) {
             PT acc;
-            term(acc, __ldg(pt + r), true);
-            int i = 1;
-            for (; i + 4 <= k; i += 4) {
-                const uint32_t e0 = __ldg(pt + (i + 0) * ck + r), e1 = __ldg(pt + (i + 1) * ck + r);
-                const uint32_t e2 = __ldg(pt + (i + 2) * ck + r), e3 = __ldg(pt + (i + 3) * ck + r);
-                term(acc, e0, false);
-                term(acc, e1, false);
-                term(acc, e2, false);
-                term(acc, e3, false);
-            }
-            for (; i < k; ++i) term(acc, __ldg(pt + i * ck + r), false);
+            uint32_t w[(N + 1) / 2];
+#pragma unroll
+            for (int p = 0; p < (k + 1) / 2; ++p) w[p] = __ldg(pt + p * ck + r);
+#pragma unroll
+            for (int i = 0; i < k; ++i) term(acc, (i & 1) ? w[i / 2] >> 16 : w[i / 2] & 0xffffu, i == 0);
             cur[r] = acc;
         }
         __syncthreads();
@@ -822,7 +818,8 @@ template <int N, int P>
 __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
     const long long* __restrict__ a, long long* __restrict__ out, int64_t count, int maxc,
     const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
-    const uint32_t* __restrict__ ptab32_16, int32_t* __restrict__ status) {
+    const uint32_t* __restrict__ ptab32_16, const uint32_t* __restrict__ tab2, const uint32_t* __restrict__ off2,
+    int32_t* __restrict__ status) {
     constexpr int n = N, E = N * N;
     using PR = PackRing<RF32X, P>;
     using PT = typename PR::T;
@@ -865,7 +862,7 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
             bool ov = false;
             const PT* last;
             if constexpr (P == 4 && kF32ByteCoef) {
-                last = bytes_ok ? smem_dp_f32c<N, PT>(mat, mat8, buf0, buf1, ptab, poff, ptab32_16)
+                last = bytes_ok ? smem_dp_f32c<N, PT>(mat, mat8, buf0, buf1, ptab, poff, tab2, off2)
                                 : smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);
             } else {
                 last = smem_dp<PR, PT, N>(mat, buf0, buf1, n, ptab, poff, ptab32_16, ov);  // 4P-byte offsets
