@@ -630,9 +630,10 @@ def roofline_of(res, peak, peak_src, traffic):
                 "peak_source": FP32_PEAK[1], "traffic": tr, "kernel": kernel_name(n, dtype),
                 "hbm_gbs": res["algorithmic_bytes_per_step"] / res["per_step_s"] / 1e9,
                 "fp64_equivalent_frac": fp / DFMA_PEAK[0],
-                "note": "exact integers on the FP32 pipe (every value provably < 2^24); the measured limiter is "
-                        "the L1TEX/shared-memory pipe (operand and predecessor-table loads, ~89 % busy in "
-                        "profiles/r2b), not the FFMA rate"}
+                "note": "exact integers on the FP32 pipe (every value provably < 2^24); co-limited by the "
+                        "L1TEX/shared-memory data pipe (74 % busy: a 16-byte operand pack per term; the coefficient "
+                        "pack is one word of four bytes) and instruction issue (69 %), profiles/r2c/"
+                        "full_c3_byte_coef.md -- not by the FFMA rate"}
     if 6 <= n <= 14:
         return {"bound": "fp64", "achieved": fp, "peak": DFMA_PEAK[0], "unit": "TFLOP/s", "frac": fp / DFMA_PEAK[0],
                 "peak_source": DFMA_PEAK[1], "traffic": tr, "kernel": kernel_name(n, dtype),
