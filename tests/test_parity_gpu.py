@@ -508,6 +508,28 @@ def test_f32_pack_kernel_paths(n):
     assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
 
 
+@pytest.mark.parametrize("n", [10, 12, 14])
+def test_f32_pack_byte_coefficients(n):
+    # FP32-exact packs whose entries all fit a signed byte read their coefficient packs as
+    # one word of four biased bytes (smem_dp_f32c); a pack with an entry outside
+    # [-128, 127] keeps the 16-byte coefficient packs. Sparse matrices keep the row-sum
+    # bound below 2^24 with entries at the byte limits; a ragged tail runs member by member.
+    rng = np.random.default_rng(8300 + n)
+    count = 4 * 8 + 2
+    a = np.zeros((count, n, n), dtype=np.int64)
+    for b in range(count):
+        p = rng.permutation(n)
+        a[b, np.arange(n), p] = rng.integers(1, 3, n)  # a permutation pattern: one term, product <= 2^n
+        a[b, rng.integers(0, n), rng.integers(0, n)] += 1
+    a[4, 0, np.argmax(a[4, 0])] = 127
+    a[5, 1, np.argmax(a[5, 1])] = -128
+    a[8, 2, np.argmax(a[8, 2])] = 128   # outside a byte: this pack takes the float4 coefficient path
+    a[13, 3, np.argmax(a[13, 3])] = -129
+    a[16:20] = configs.int_matrices(n, 4, seed=8400 + n, lo=-1, hi=2)  # small mixed signs
+    want = O.sz_batch(a)
+    assert np.array_equal(pl.store_zechin_permanent_batch(a), want)
+
+
 @pytest.mark.parametrize("n", [15, 17, 20, 22])
 def test_large_order_batches_one_launch_per_layer(n):
     # batches of 15 <= n <= ~22 run every layer of a group of matrices in one lean
