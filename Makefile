@@ -44,7 +44,11 @@ $(BUILD)/ryser.o: $(CSRC)/ryser.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh $(CS
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/ryser.cu
 
-$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/batch.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o $(BUILD)/blk.o
+$(BUILD)/bigint.o: $(CSRC)/bigint.cu $(CSRC)/capi_internal.h $(CSRC)/ring.cuh include/permlab_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/bigint.cu
+
+$(PKG)/libpermlab_b200.so: $(BUILD)/capi.o $(BUILD)/batch.o $(BUILD)/boson.o $(BUILD)/multi.o $(BUILD)/ryser.o $(BUILD)/blk.o $(BUILD)/bigint.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -ldl
 
 $(PKG)/libpermlab_gen.so: $(CSRC)/gen/configs.c

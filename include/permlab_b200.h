@@ -105,6 +105,31 @@ pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, u
 pl_status pl_sz_permanent_batch(pl_dtype dtype, int32_t n, int64_t count, const void* a, void* out,
                                 uint32_t flags, const pl_limits* limits, void* stream, int32_t* status_dev);
 
+/* Exact integer permanent of any magnitude. The reference's Int ring is
+ * arbitrary precision (reference proj/include/permlab/ring.hpp:29-31), so its
+ * store_zechin_permanent (permanent.cpp:314-316) never overflows; PL_I64 is
+ * exact while every intermediate fits int64 and returns PL_ERR_OVERFLOW
+ * otherwise. This entry point returns the reference's value in every case:
+ * the layer DP runs on residues modulo K primes below 2^31 (K from the
+ * row-sum bound |per(A)| <= prod_i sum_j |a_ij|) and the residues are
+ * recombined on the host (CRT). `a`: n x n int64 entries (host). The result is
+ * sign (*negative = 1 for a negative value) and magnitude as *nlimbs
+ * little-endian 64-bit limbs (0 limbs = zero). If limb_cap is too small the
+ * call returns PL_ERR_ARG with *nlimbs set to the size needed
+ * (34 x 34 int64 entries need at most 37 limbs). Synchronous. */
+pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
+                                 int32_t* negative, const pl_limits* limits, void* stream);
+
+/* The residue passes on their own: out[i] = per(R_i) mod primes[i], where R_i
+ * (n x n int64 entries in [0, primes[i]), host) is the matrix reduced modulo
+ * primes[i] (any moduli in [2, 2^31); pairwise coprime for a CRT). For callers
+ * whose entries exceed int64 and who recombine themselves (the Python API does,
+ * for Python integers). pl_bigint_primes writes the first `count` primes the
+ * engine itself uses (descending from 2^31 - 1) and returns count. */
+pl_status pl_sz_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* primes, const int64_t* residues,
+                               uint32_t* out, const pl_limits* limits, void* stream);
+int32_t pl_bigint_primes(int32_t count, uint32_t* out);
+
 /* Operation counts of the Store-zechin recurrence (reference measures them
  * through Counted<T>, op_count.hpp:52-70; closed form cost_model.cpp:176-181):
  * n = 1 -> (0, 0); n = 2 -> (2, 1); n >= 3 -> (n*2^(n-1) - n, n*2^(n-1) - 2^n + 1). */

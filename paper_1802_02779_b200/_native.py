@@ -66,6 +66,9 @@ EXPORTED_SYMBOLS = (
     "pl_ryser_counts",
     "pl_shard_block_partial",
     "pl_shard_block_top_terms",
+    "pl_sz_permanent_bigint",
+    "pl_sz_permanent_modp",
+    "pl_bigint_primes",
 )
 
 
@@ -134,6 +137,13 @@ def _load():
     L.pl_shard_block_partial.restype = C.c_int
     L.pl_shard_block_top_terms.argtypes = [C.c_int, i32, vp, i32, vp, vp, i32, i32, u32, vp, vp]
     L.pl_shard_block_top_terms.restype = C.c_int
+    L.pl_sz_permanent_bigint.argtypes = [i32, vp, vp, C.c_size_t, C.POINTER(C.c_size_t), C.POINTER(i32),
+                                         C.POINTER(pl_limits), vp]
+    L.pl_sz_permanent_bigint.restype = C.c_int
+    L.pl_sz_permanent_modp.argtypes = [i32, i32, vp, vp, vp, C.POINTER(pl_limits), vp]
+    L.pl_sz_permanent_modp.restype = C.c_int
+    L.pl_bigint_primes.argtypes = [i32, vp]
+    L.pl_bigint_primes.restype = i32
     return L
 
 

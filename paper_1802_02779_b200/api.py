@@ -130,8 +130,16 @@ def _as_matrix(a) -> np.ndarray:
         raise DomainError("entry count does not match order^2")
     if arr.shape[0] < 1:
         raise DomainError("matrix order must be >= 1")
-    if arr.dtype.kind in "iub":
+    if arr.dtype.kind in "ib" or (arr.dtype.kind == "u" and arr.dtype.itemsize < 8):
         arr = arr.astype(np.int64)
+    elif arr.dtype.kind == "u" or (arr.dtype == object and all(isinstance(v, (int, np.integer)) for v in arr.flat)):
+        # Python integers / uint64: int64 when they fit, else an object matrix for the residue path
+        vals = [int(v) for v in arr.flat]
+        if all(-(1 << 63) <= v < (1 << 63) for v in vals):
+            arr = np.array(vals, dtype=np.int64).reshape(arr.shape)
+        else:
+            arr = np.array(vals, dtype=object).reshape(arr.shape)
+            return arr
     elif arr.dtype.kind == "f":
         arr = arr.astype(np.float64)
     elif arr.dtype.kind == "c":
@@ -139,6 +147,43 @@ def _as_matrix(a) -> np.ndarray:
     else:
         raise DomainError(f"unsupported entry type {arr.dtype}")
     return np.ascontiguousarray(arr)
+
+
+def _bigint_from_int64(m: np.ndarray, lim) -> int:
+    """Exact permanent of an int64 matrix whose intermediates leave int64
+    (``pl_sz_permanent_bigint``: residue passes on the device, CRT in the library)."""
+    n = m.shape[0]
+    cap = 40
+    limbs = np.zeros(cap, dtype=np.uint64)
+    nl, neg = C.c_size_t(0), C.c_int32(0)
+    _check(N.lib.pl_sz_permanent_bigint(n, m.ctypes.data, limbs.ctypes.data, cap, C.byref(nl), C.byref(neg),
+                                        C.byref(lim), None))
+    v = 0
+    for i in reversed(range(nl.value)):
+        v = (v << 64) | int(limbs[i])
+    return -v if neg.value else v
+
+
+def _bigint_from_objects(m: np.ndarray, lim) -> int:
+    """Exact permanent of a matrix of Python integers of any size: residues modulo the
+    engine's primes go through ``pl_sz_permanent_modp``; the CRT runs on Python integers."""
+    n = m.shape[0]
+    rows = [[int(v) for v in r] for r in m]
+    bound = 1
+    for r in rows:
+        bound *= sum(abs(v) for v in r)
+    k = max(1, (bound.bit_length() + 2 + 29) // 30)
+    primes = np.zeros(k, dtype=np.uint32)
+    if N.lib.pl_bigint_primes(k, primes.ctypes.data) != k:
+        raise DeviceError("pl_bigint_primes failed")
+    res = np.array([[[v % int(p) for v in r] for r in rows] for p in primes], dtype=np.int64)
+    out = np.zeros(k, dtype=np.uint32)
+    _check(N.lib.pl_sz_permanent_modp(n, k, primes.ctypes.data, res.ctypes.data, out.ctypes.data, C.byref(lim), None))
+    x, mod = 0, 1
+    for p, r in zip((int(p) for p in primes), (int(r) for r in out)):
+        x += mod * (((r - x) * pow(mod, -1, p)) % p)
+        mod *= p
+    return x - mod if 2 * x > mod else x
 
 
 def _py_value(arr: np.ndarray, i: int = 0):
@@ -151,13 +196,24 @@ def _py_value(arr: np.ndarray, i: int = 0):
 
 
 def store_zechin_permanent(a, limits: Optional[Limits] = None, fma: bool = False) -> PermanentResult:
-    """Permanent of one square matrix (reference ``permanent.hpp:90``)."""
+    """Permanent of one square matrix (reference ``permanent.hpp:90``).
+
+    Integer matrices are exact at any magnitude, like the reference's
+    arbitrary-precision Int ring (``ring.hpp:29-31``): when the int64 guard
+    reports an overflow (or the entries themselves exceed int64) the layer DP
+    runs on residues modulo enough 31-bit primes and the result is recombined
+    (``csrc/bigint.cu``)."""
     m = _as_matrix(a)
     n = m.shape[0]
     lim = (limits or Limits()).to_c()
+    if m.dtype == object:
+        return PermanentResult(_bigint_from_objects(m, lim), store_zechin_counts(n))
     out = np.zeros(1, dtype=m.dtype)
     flags = N.PL_FLAG_FMA if fma else 0
-    _check(N.lib.pl_sz_permanent(_DTYPES[m.dtype], n, m.ctypes.data, out.ctypes.data, flags, C.byref(lim), None))
+    status = N.lib.pl_sz_permanent(_DTYPES[m.dtype], n, m.ctypes.data, out.ctypes.data, flags, C.byref(lim), None)
+    if status == N.PL_ERR_OVERFLOW and m.dtype == np.int64:
+        return PermanentResult(_bigint_from_int64(m, lim), store_zechin_counts(n))
+    _check(status)
     return PermanentResult(_py_value(out), store_zechin_counts(n))
 
 

@@ -282,6 +282,8 @@ pl_status with_ring(pl_dtype dt, bool fma, F&& f) {
         case PL_C128:
             return fma ? f(pl::RC128<true>{}) : f(pl::RC128<false>{});
     }
+    // internal: the residue passes of the exact big-integer path (bigint.cu)
+    if (dt == plc::kModDtype) return f(pl::RModP{});
     return fail(PL_ERR_ARG, "unknown dtype");
 }
 
@@ -1075,6 +1077,10 @@ pl_status fail_msg(pl_status s, const char* msg) { return fail(s, "%s", msg); }
 pl_status cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
 pl_status device_ready() { return have_device(); }
 int sm_count() { return num_sms(); }
+pl_status set_modulus(const pl::ModParams* mp, cudaStream_t st) {
+    PL_CUDA(cudaMemcpyToSymbolAsync(pl::c_modp, mp, sizeof(pl::ModParams), 0, cudaMemcpyHostToDevice, st));
+    return PL_OK;
+}
 pl_status enqueue_batch(pl_dtype dt, int n, int64_t count, const void* a_dev, void* out_dev, bool fma,
                         int32_t* status_dev, cudaStream_t st) {
     return ::enqueue_batch(dt, n, count, a_dev, out_dev, fma, status_dev, st);

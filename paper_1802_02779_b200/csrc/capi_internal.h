@@ -8,7 +8,18 @@
 
 #include "../../include/permlab_b200.h"
 
+namespace pl {
+struct ModParams;
+}
+
 namespace plc {
+
+// Internal dtype of the residue passes (ring RModP, ring.cuh): 8-byte entries in
+// [0, p), large orders only (n >= 15; bigint.cu runs the small ones itself).
+constexpr pl_dtype kModDtype = static_cast<pl_dtype>(3);
+// Set the modulus of the following RModP launches, ordered on `st` (`mp` must
+// stay valid until the stream gets there).
+pl_status set_modulus(const pl::ModParams* mp, cudaStream_t st);
 
 // Set the thread-local pl_last_error() message and return `s`.
 pl_status fail_msg(pl_status s, const char* msg);

@@ -17,6 +17,13 @@
 //   RC128<FMA>   complex double as double2 (re, im). FMA=false reproduces
 //                GCC's inline complex product (ac - bd, ad + bc) and the
 //                componentwise sum, each operation individually rounded.
+//   RModP        residues modulo a prime p < 2^31 (entries and values in
+//                [0, p), stored as long long): the ring of the exact big-integer
+//                path (bigint.cu) -- the layer DP runs once per prime and the
+//                host recombines the residues (CRT), which restores the
+//                reference's arbitrary-precision Int (proj/include/permlab/
+//                ring.hpp:29-31) where int64 would overflow. p and its Barrett
+//                constant live in constant memory, set per pass on the stream.
 #pragma once
 
 #include <cstdint>
@@ -84,6 +91,35 @@ struct RC128 {
         return add(acc, mul(a, b, ov), ov);
     }
     __device__ __forceinline__ static T zero() { return make_double2(0.0, 0.0); }
+};
+
+// Modulus of the RModP passes: p < 2^31 prime, m = floor(2^64 / p). One copy
+// per translation unit; only capi.cu launches RModP kernels (set_modulus).
+struct ModParams {
+    unsigned long long p;
+    unsigned long long m;
+};
+static __constant__ ModParams c_modp;
+
+struct RModP {
+    using T = long long;
+    static constexpr bool kChecked = false;
+    // a, b < p < 2^31: x = a * b < 2^62; q = floor(x * m / 2^64) is floor(x / p)
+    // or one less (x / p - x * m / 2^64 < x / 2^64 < 1), so x - q * p < 2 p
+    __device__ __forceinline__ static T mul(T a, T b, bool&) {
+        const unsigned long long x = (unsigned long long)a * (unsigned long long)b;
+        const unsigned long long q = __umul64hi(x, c_modp.m);
+        unsigned long long r = x - q * c_modp.p;
+        if (r >= c_modp.p) r -= c_modp.p;
+        return (T)r;
+    }
+    __device__ __forceinline__ static T add(T a, T b, bool&) {
+        unsigned long long s = (unsigned long long)a + (unsigned long long)b;
+        if (s >= c_modp.p) s -= c_modp.p;
+        return (T)s;
+    }
+    __device__ __forceinline__ static T mac(T acc, T a, T b, bool& ov) { return add(acc, mul(a, b, ov), ov); }
+    __device__ __forceinline__ static T zero() { return 0; }
 };
 
 // Binomial table C(s, l), s, l <= kBinomDim - 1, as uint32 (C(34,17) < 2^32).

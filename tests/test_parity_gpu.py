@@ -4,6 +4,7 @@ same seeded inputs, at the BASELINE.json config sizes and at edge cases.
 Bars (BASELINE.json north_star): int64 bit-exact; float64 / complex128 within
 relative 1e-9 — and, in the default (non-FMA) mode, bitwise equal to the
 oracle, which is bitwise the reference engine (tests/test_oracle.py)."""
+import ctypes as C
 import math
 import struct
 import subprocess
@@ -14,6 +15,7 @@ import pytest
 
 import paper_1802_02779_b200 as pl
 from oracle import oracle as O
+from paper_1802_02779_b200 import _native as N
 from paper_1802_02779_b200 import configs
 
 pytestmark = pytest.mark.gpu
@@ -184,9 +186,15 @@ def test_reference_goldens_on_device():
 def test_int64_overflow_guard():
     # every intermediate fits: the checked path computes it exactly (20! < 2^63)
     assert pl.store_zechin_permanent(np.ones((20, 20), dtype=np.int64)).value == math.factorial(20)
-    # 21! > 2^63 (layer path), 5! 10^20 (register kernel), 9! 10^27 (shared-memory kernel): never wrap
-    with pytest.raises(pl.DomainError, match="overflow"):
-        pl.store_zechin_permanent(np.ones((21, 21), dtype=np.int64))
+    # 21! > 2^63 (layer path), 5! 10^20 (register kernel), 9! 10^27 (shared-memory kernel): never wrap.
+    # The C ABI's int64 entry point reports it; the single-matrix Python call then returns the exact
+    # integer through the residue passes (tests/test_bigint_gpu.py), int64 batches raise.
+    ones21 = np.ones((21, 21), dtype=np.int64)
+    out = np.zeros(1, dtype=np.int64)
+    lim = pl.Limits().to_c()
+    assert N.lib.pl_sz_permanent(N.PL_I64, 21, ones21.ctypes.data, out.ctypes.data, 0, C.byref(lim),
+                                 None) == N.PL_ERR_OVERFLOW
+    assert pl.store_zechin_permanent(ones21).value == math.factorial(21)
     with pytest.raises(pl.DomainError, match="overflow"):
         pl.store_zechin_permanent_batch(np.full((3, 5, 5), 10 ** 4, dtype=np.int64))
     with pytest.raises(pl.DomainError, match="overflow"):
