@@ -703,6 +703,49 @@ RYSER = {"n": 22, "seed": 22, "cpu_n": 18,
                  "bitwise the reference's visit-order fold"}
 
 
+BIGINT = {"n": 24, "seed": 24,
+          "desc": "exact Int beyond int64: single 24x24 integer matrix, entries uniform in [0, 3] (seed 24), "
+                  "permanent ~2^93; int64 attempt (overflow reported) + residue passes modulo 31-bit primes + CRT"}
+
+
+def bigint_matrix():
+    return np.random.default_rng(BIGINT["seed"]).integers(0, 4, (BIGINT["n"], BIGINT["n"]), dtype=np.int64)
+
+
+def measure_bigint(steps, warmup):
+    """The public call on a matrix whose permanent leaves int64 (reference ring.hpp:29-31: Int is
+    arbitrary precision). Host call, H2D/D2H and the host-side CRT inside the timed region."""
+    import paper_1802_02779_b200 as pl
+
+    a = bigint_matrix()
+    for _ in range(warmup):
+        v = pl.store_zechin_permanent(a).value
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        v = pl.store_zechin_permanent(a).value
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    bound_bits = sum(int(r.sum()).bit_length() for r in a)
+    return {"value": 1.0 / t, "unit": "permanents/s", "time_to_permanent_ms": 1e3 * t, "steps": steps,
+            "workload": BIGINT["desc"], "result_bits": int(v).bit_length(),
+            "residue_passes": max(1, (bound_bits + 2 + 29) // 30), "result": str(v)}
+
+
+def bigint_cpu_reference(device_result):
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return {"error": "oracle/_ref not built"}
+    a = bigint_matrix()
+    t0 = time.perf_counter()
+    v, _ = O.ref_sz_int(a, memo_budget_bytes=1 << 36)  # its 2^24-slot memo table exceeds the default budget
+    t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": "permanents/s", "cores": 1, "kind": "reference",
+            "sample": f"reference store_zechin_permanent on the same matrix ({t:.2f} s, 1 thread; the engine is "
+                      "single-threaded)", "equal_to_device_result": str(v) == device_result}
+
+
 def measure_batch16(steps, warmup, device):
     """Batched large orders (callers looping store_zechin_permanent at 15 <= n <= 20):
     value device-resident, events around K back-to-back calls; CPU baseline the reference engine."""
@@ -847,6 +890,10 @@ def main():
                     suite["ryser"] = measure_ryser(5, 2)
                 except Exception as e:  # noqa: BLE001
                     suite["ryser"] = {"error": repr(e)[:300]}
+                try:
+                    suite["bigint"] = measure_bigint(5, 2)
+                except Exception as e:  # noqa: BLE001
+                    suite["bigint"] = {"error": repr(e)[:300]}
             for key, steps_b, spec_b in (("boson", 10, BOSON), ("boson_large", 3, BOSON_LARGE)):
                 try:
                     suite[key] = measure_boson(steps_b, 3, rank, world, device, flush_buf, args.fma, spec_b)
@@ -876,6 +923,11 @@ def main():
                 suite["batch_n16"]["cpu_baseline"] = {"error": repr(e)[:200]}
         if "error" not in suite.get("ryser", {"error": 1}):
             suite["ryser"]["cpu_baseline"] = ryser_cpu_reference()
+        if "error" not in suite.get("bigint", {"error": 1}):
+            try:
+                suite["bigint"]["cpu_baseline"] = bigint_cpu_reference(suite["bigint"]["result"])
+            except Exception as e:  # noqa: BLE001
+                suite["bigint"]["cpu_baseline"] = {"error": repr(e)[:200]}
 
     cpu = None
     if cpu_on:

@@ -224,6 +224,23 @@ struct BatchOptions {
 };
 
 PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limits = {});
+
+/// Arbitrary-precision integer: sign and magnitude as little-endian 64-bit limbs
+/// (no limbs = 0). The value of the reference's Int ring (cpp_int, reference
+/// ring.hpp:29-31) where it leaves int64.
+struct BigInt {
+    bool negative = false;
+    std::vector<std::uint64_t> limbs;
+    bool fits_int64() const;
+    Int to_int64() const;     // DomainError unless fits_int64()
+    std::string str() const;  // decimal, as cpp_int streams it
+};
+/// The exact integer permanent at any magnitude (reference permanent.hpp:90 on its
+/// Int ring never overflows): the int64 engine where every intermediate fits,
+/// otherwise the layer DP on residues modulo 31-bit primes, recombined on the
+/// host (pl_sz_permanent_bigint). store_zechin_permanent keeps Int = int64 and
+/// throws DomainError on overflow.
+BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits = {});
 /// Ryser's formula on the device (reference permanent.hpp:84): float rings
 /// bitwise the reference's visit-order fold, Int exact (guarded like
 /// store_zechin_permanent); counts = count_formula(Ryser, n).

@@ -229,6 +229,8 @@ def ryser_permanent(a, limits: Optional[Limits] = None) -> PermanentResult:
     ``permanent.cpp:85-136``): float rings bitwise the reference's visit-order
     fold, int64 exact (guarded)."""
     m = _as_matrix(a)
+    if m.dtype == object:
+        raise DomainError("integer entries beyond int64 are not offered by the Ryser device engine")
     n = m.shape[0]
     lim = (limits or Limits()).to_c()
     out = np.zeros(1, dtype=m.dtype)

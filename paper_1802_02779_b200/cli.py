@@ -278,7 +278,8 @@ def parse_csv(text: str, ring: str) -> np.ndarray:
 
 def _int_matrix(n: int, vals) -> np.ndarray:
     if any(v < -(1 << 63) or v >= (1 << 63) for v in vals):
-        raise DomainError("integer entries beyond int64 are not offered by the device engine")
+        # entries beyond int64: Python integers, computed by the residue passes (api.store_zechin_permanent)
+        return np.array(vals, dtype=object).reshape(n, n)
     return np.array(vals, dtype=np.int64).reshape(n, n)
 
 
@@ -391,7 +392,11 @@ def run_perm(opt) -> str:
     n = m.shape[0]
     if opt.format == "json":
         v = r.value
-        vj = int(v) if isinstance(v, (int, np.integer)) else [complex(v).real, complex(v).imag]
+        if isinstance(v, (int, np.integer)):
+            # reference tools/permlab_cli.cpp:91-99: a number inside long long, else the decimal string
+            vj = int(v) if -(1 << 63) <= int(v) < (1 << 63) else str(int(v))
+        else:
+            vj = [complex(v).real, complex(v).imag]
         return json_dump({"algorithm": opt.algorithm, "order": n, "value": vj,
                           "counts": {"multiplications": r.counts.multiplications,
                                      "additions": r.counts.additions}}, 2) + "\n"

@@ -226,6 +226,64 @@ PermanentResult store_zechin_permanent(const SquareMatrix& a, const Limits& limi
     return r;
 }
 
+bool BigInt::fits_int64() const {
+    if (limbs.empty()) return true;
+    if (limbs.size() > 1) return false;
+    return negative ? limbs[0] <= (std::uint64_t{1} << 63) : limbs[0] < (std::uint64_t{1} << 63);
+}
+
+Int BigInt::to_int64() const {
+    if (!fits_int64()) throw DomainError("integer value does not fit int64");
+    if (limbs.empty()) return 0;
+    return negative ? static_cast<Int>(~limbs[0] + 1) : static_cast<Int>(limbs[0]);
+}
+
+std::string BigInt::str() const {
+    std::vector<std::uint64_t> w = limbs;
+    while (!w.empty() && w.back() == 0) w.pop_back();
+    if (w.empty()) return "0";
+    constexpr std::uint64_t kChunk = 10000000000000000000ull;  // 10^19
+    std::vector<std::uint64_t> chunks;
+    while (!w.empty()) {
+        unsigned __int128 rem = 0;
+        for (std::size_t i = w.size(); i-- > 0;) {
+            const unsigned __int128 cur = (rem << 64) | w[i];
+            w[i] = static_cast<std::uint64_t>(cur / kChunk);
+            rem = cur % kChunk;
+        }
+        chunks.push_back(static_cast<std::uint64_t>(rem));
+        while (!w.empty() && w.back() == 0) w.pop_back();
+    }
+    std::string out = negative ? "-" : "";
+    out += std::to_string(chunks.back());
+    for (std::size_t i = chunks.size() - 1; i-- > 0;) {
+        const std::string d = std::to_string(chunks[i]);
+        out += std::string(19 - d.size(), '0') + d;
+    }
+    return out;
+}
+
+BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits) {
+    const pl_limits lim = to_c(limits);
+    BigInt r;
+    Int v = 0;
+    const pl_status s = pl_sz_permanent(PL_I64, a.order(), a.entries().data(), &v, 0, &lim, nullptr);
+    if (s == PL_OK) {
+        r.negative = v < 0;
+        if (v != 0) r.limbs.push_back(v < 0 ? ~static_cast<std::uint64_t>(v) + 1 : static_cast<std::uint64_t>(v));
+        return r;
+    }
+    if (s != PL_ERR_OVERFLOW) check(s);
+    r.limbs.resize(40);  // 34 x 34 int64 entries need at most 37
+    std::size_t nl = 0;
+    std::int32_t neg = 0;
+    check(pl_sz_permanent_bigint(a.order(), a.entries().data(), r.limbs.data(), r.limbs.size(), &nl, &neg, &lim,
+                                 nullptr));
+    r.limbs.resize(nl);
+    r.negative = neg != 0;
+    return r;
+}
+
 OpCount ryser_counts(int n) {
     OpCount c;
     check(pl_ryser_counts(n, &c.multiplications, &c.additions));

@@ -290,6 +290,17 @@ void device_run_and_batch() {
                     DomainError);
     // int64 guard: an exact value beyond int64 is a DomainError, never a wrap
     CHECK_THROWS_AS(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(22, 1000))), DomainError);
+    // ... and the exact entry point returns the reference's arbitrary-precision value: 1000^22 22!
+    {
+        const BigInt big = store_zechin_permanent_exact(Matrix<Int>::filled(22, 1000));
+        CHECK(!big.negative && !big.fits_int64());
+        CHECK(big.str() == "1124000727777607680000" + std::string(66, '0'));
+        const BigInt neg = store_zechin_permanent_exact(Matrix<Int>::filled(21, -1));
+        CHECK(neg.negative && neg.str() == "-51090942171709440000");
+        const BigInt small = store_zechin_permanent_exact(Matrix<Int>::filled(5, -2));
+        CHECK(small.fits_int64() && small.to_int64() == -3840 && small.str() == "-3840");
+        CHECK(store_zechin_permanent_exact(Matrix<Int>::filled(16, 0)).str() == "0");
+    }
     // the guard is conservative but the checked path still computes what fits
     CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(20, 1)))) == 2432902008176640000LL);
 }

@@ -42,6 +42,25 @@ def test_perm_int_json_and_text():
     assert "value: 10\n" in out
 
 
+def test_perm_int_beyond_int64(tmp_path):
+    # the reference's Int ring is arbitrary precision: text prints the decimal value, JSON carries
+    # a string once the value leaves long long (reference tools/permlab_cli.cpp:91-99, 160-169)
+    import json
+    import math
+
+    ones = tmp_path / "ones21.csv"
+    ones.write_text("\n".join(",".join("1" for _ in range(21)) for _ in range(21)) + "\n")
+    out = run("perm", "--matrix", str(ones), "--algorithm", "store-zechin")
+    assert out.splitlines()[1] == "value: %d" % math.factorial(21)
+    js = json.loads(run("perm", "--matrix", str(ones), "--algorithm", "store-zechin", "--format", "json"))
+    assert js["value"] == str(math.factorial(21)) and js["order"] == 21
+    # entries beyond int64 as well: per([[10^30, 1], [2, -10^25]]) = -10^55 + 2
+    big = tmp_path / "big2.csv"
+    big.write_text("1" + "0" * 30 + ",1\n2,-1" + "0" * 25 + "\n")
+    out = run("perm", "--matrix", str(big), "--algorithm", "store-zechin")
+    assert out.splitlines()[1] == "value: %d" % (2 - 10 ** 55)
+
+
 def test_perm_complex_matches_reference_bytes():
     assert run("perm", "--matrix", str(FIX / "c3.json"), "--algorithm", "store-zechin") == gold("perm_c3.txt")
     assert run("perm", "--matrix", str(FIX / "c3.json"), "--algorithm", "store-zechin", "--format",
