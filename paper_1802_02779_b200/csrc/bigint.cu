@@ -86,7 +86,7 @@ const std::vector<uint32_t>& primes_desc(size_t k) {
 // One CTA per prime: X[S] over all column subsets S as bit masks in shared
 // memory, X[{}] = 1, X[S] = sum_{j in S} a(|S| - 1, j) X[S \ {j}] (mod p), layer
 // by layer; per(A) = X[full]. `res`: K matrices of residues in [0, p_i).
-__global__ void __launch_bounds__(256) sz_modp_small_kernel(const long long* __restrict__ res, int n,
+__global__ void __launch_bounds__(1024) sz_modp_small_kernel(const long long* __restrict__ res, int n,
                                                              const uint32_t* __restrict__ primes,
                                                              uint32_t* __restrict__ out) {
     extern __shared__ uint32_t x[];  // 2^n values, then n * n coefficients
@@ -143,11 +143,12 @@ std::mutex& pass_mutex() {
 
 pl_status run_residues(int n, int k, const uint32_t* primes, const int64_t* res, uint32_t* out,
                        const pl_limits* lim, cudaStream_t st) {
-    pl_status s = plc::device_ready();
+    // limits and arguments reject before any device work (reference tests/test_permanent.cpp:280-294)
+    pl_status s = plc::check_order_limits(n, lim);
     if (s != PL_OK) return s;
-    if ((s = plc::check_order_limits(n, lim)) != PL_OK) return s;
-    if (n > kSmallMax && (s = plc::check_budget_limits(PL_I64, n, lim)) != PL_OK) return s;
+    if ((s = plc::check_budget_limits(PL_I64, n, lim)) != PL_OK) return s;
     if ((s = check_residues(n, k, primes, res)) != PL_OK) return s;
+    if ((s = plc::device_ready()) != PL_OK) return s;
     std::lock_guard<std::mutex> lock(pass_mutex());
     const size_t in_bytes = (size_t)k * n * n * sizeof(long long);
     long long* a_dev = nullptr;
@@ -178,7 +179,9 @@ pl_status run_residues(int n, int k, const uint32_t* primes, const int64_t* res,
         // per device; setting it again is cheap next to the launch
         PLB_TRY(cudaFuncSetAttribute(sz_modp_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)((1u << kSmallMax) * 4 + kSmallMax * kSmallMax * 4)));
-        sz_modp_small_kernel<<<(unsigned)k, 256, smem, st>>>(a_dev, n, primes_dev, static_cast<uint32_t*>(out_dev));
+        // a CTA per prime: few CTAs, so as many threads as the table has work for
+        const unsigned threads = n >= 12 ? 1024 : n >= 10 ? 512 : 256;
+        sz_modp_small_kernel<<<(unsigned)k, threads, smem, st>>>(a_dev, n, primes_dev, static_cast<uint32_t*>(out_dev));
         PLB_TRY(cudaGetLastError());
         PLB_TRY(cudaMemcpyAsync(out, out_dev, (size_t)k * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         PLB_TRY(cudaStreamSynchronize(st));
@@ -297,8 +300,10 @@ extern "C" {
 
 pl_status pl_sz_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* primes, const int64_t* residues,
                                uint32_t* out, const pl_limits* limits, void* stream) {
-    if (n < 1 || n > PL_MAX_ORDER) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1 and <= 34");
+    if (n < 1) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1");
     if (nprimes < 1 || !primes || !residues || !out) return plc::fail_msg(PL_ERR_ARG, "bad arguments to pl_sz_permanent_modp");
+    const pl_status lim_s = plc::check_order_limits(n, limits);
+    if (lim_s != PL_OK) return lim_s;
     return run_residues(n, nprimes, primes, residues, out, limits, static_cast<cudaStream_t>(stream));
 }
 
@@ -311,10 +316,12 @@ int32_t pl_bigint_primes(int32_t count, uint32_t* out) {
 
 pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
                                  int32_t* negative, const pl_limits* limits, void* stream) {
-    if (n < 1 || n > PL_MAX_ORDER) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1 and <= 34");
+    if (n < 1) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1");
     if (!a || !nlimbs || !negative || (limb_cap && !limbs)) {
         return plc::fail_msg(PL_ERR_ARG, "bad arguments to pl_sz_permanent_bigint");
     }
+    const pl_status lim_s = plc::check_order_limits(n, limits);  // also the device cap (PL_MAX_ORDER)
+    if (lim_s != PL_OK) return lim_s;
     // |per(A)| <= prod_i sum_j |a_ij| < 2^B, B = sum_i bit_length(row sum)
     int bits = 0;
     for (int i = 0; i < n; ++i) {

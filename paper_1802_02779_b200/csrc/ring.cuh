@@ -107,7 +107,8 @@ struct RModP {
     // a, b < p < 2^31: x = a * b < 2^62; q = floor(x * m / 2^64) is floor(x / p)
     // or one less (x / p - x * m / 2^64 < x / 2^64 < 1), so x - q * p < 2 p
     __device__ __forceinline__ static T mul(T a, T b, bool&) {
-        const unsigned long long x = (unsigned long long)a * (unsigned long long)b;
+        // residues are below 2^31: one 32 x 32 -> 64 multiply
+        const unsigned long long x = (unsigned long long)(unsigned)a * (unsigned long long)(unsigned)b;
         const unsigned long long q = __umul64hi(x, c_modp.m);
         unsigned long long r = x - q * c_modp.p;
         if (r >= c_modp.p) r -= c_modp.p;

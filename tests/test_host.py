@@ -126,7 +126,13 @@ def test_domain_errors_before_device_work():
     with pytest.raises(pl.DomainError):
         pl.store_zechin_permanent(np.ones((3, 4)))
     with pytest.raises(pl.DomainError):
-        pl.store_zechin_permanent(np.ones((2, 2), dtype=object))
+        pl.store_zechin_permanent(np.array([["a", "b"], ["c", "d"]], dtype=object))
+    # Python integers beyond int64 (the residue path): limits still reject before any device work
+    big = np.array([[10 ** 30, 1], [2, 3]], dtype=object)
+    with pytest.raises(pl.DomainError, match="subset_order_limit"):
+        pl.store_zechin_permanent(big, pl.Limits(subset_order_limit=1))
+    with pytest.raises(pl.DomainError, match="beyond int64"):
+        pl.ryser_permanent(big)
     with pytest.raises(pl.DomainError):
         pl.store_zechin_permanent_batch(np.ones((3, 4, 4), dtype=np.float32))
     with pytest.raises(pl.DomainError, match="subset_order_limit"):
@@ -144,6 +150,42 @@ def test_no_cpu_fallback_without_device():
         pl.store_zechin_permanent_batch(np.ones((4, 5, 5), dtype=np.int64))
     with pytest.raises(pl.DeviceError, match="NODEVICE"):
         pl.ryser_permanent(np.eye(3))
+    with pytest.raises(pl.DeviceError, match="NODEVICE"):
+        pl.store_zechin_permanent(np.array([[10 ** 30, 1], [2, 3]], dtype=object))
+
+
+def test_bigint_primes_are_the_largest_31_bit_primes():
+    # host-only part of the exact big-integer path (csrc/bigint.cu): deterministic Miller-Rabin
+    import ctypes as C
+
+    from paper_1802_02779_b200 import _native as N
+
+    k = 80  # a 34 x 34 matrix of full-range int64 entries needs 80 passes
+    primes = np.zeros(k, dtype=np.uint32)
+    assert N.lib.pl_bigint_primes(k, primes.ctypes.data) == k
+
+    def is_prime(v):
+        return v > 1 and all(v % q for q in range(2, int(v ** 0.5) + 1))
+
+    want, v = [], 2 ** 31 - 1
+    while len(want) < 6:
+        if is_prime(v):
+            want.append(v)
+        v -= 2
+    assert primes[:6].tolist() == want
+    assert all(2 ** 30 < int(p) < 2 ** 31 for p in primes) and len(set(primes.tolist())) == k
+    assert all(int(a) > int(b) for a, b in zip(primes, primes[1:]))
+    # Fermat check of the rest (base 2 and 3; Miller-Rabin inside is deterministic below 3.2e9)
+    assert all(pow(2, int(p) - 1, int(p)) == 1 and pow(3, int(p) - 1, int(p)) == 1 for p in primes)
+    assert N.lib.pl_bigint_primes(0, primes.ctypes.data) == 0
+    # argument errors come before the device check
+    lim = pl.Limits().to_c()
+    nl, neg = C.c_size_t(0), C.c_int32(0)
+    assert N.lib.pl_sz_permanent_bigint(0, primes.ctypes.data, None, 0, C.byref(nl), C.byref(neg), C.byref(lim),
+                                        None) == N.PL_ERR_ARG
+    a35 = np.ones((35, 35), dtype=np.int64)
+    assert N.lib.pl_sz_permanent_bigint(35, a35.ctypes.data, None, 0, C.byref(nl), C.byref(neg), C.byref(lim),
+                                        None) == N.PL_ERR_LIMIT
 
 
 def test_cpp_host_suite():
