@@ -241,6 +241,10 @@ struct BigInt {
 /// host (pl_sz_permanent_bigint). store_zechin_permanent keeps Int = int64 and
 /// throws DomainError on overflow.
 BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits = {});
+/// The same through Ryser's formula (reference permanent.hpp:84 on its Int ring):
+/// 128-bit wrapping sums where the guard bound allows, else inclusion-exclusion sums on
+/// residues (pl_ryser_permanent_bigint).
+BigInt ryser_permanent_exact(const Matrix<Int>& a, const Limits& limits = {});
 /// Ryser's formula on the device (reference permanent.hpp:84): float rings
 /// bitwise the reference's visit-order fold, Int exact (guarded like
 /// store_zechin_permanent); counts = count_formula(Ryser, n).

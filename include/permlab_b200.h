@@ -130,6 +130,17 @@ pl_status pl_sz_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* prime
                                uint32_t* out, const pl_limits* limits, void* stream);
 int32_t pl_bigint_primes(int32_t count, uint32_t* out);
 
+/* The same for Ryser's formula (reference permanent.hpp:84 on its Int ring,
+ * permanent.cpp:85-136): pl_ryser_permanent reports PL_ERR_OVERFLOW where the
+ * value or its guard bound leaves the 128-bit / int64 range; these return the
+ * exact integer (sign + limbs as above) from inclusion-exclusion sums on
+ * residues, and the residues alone. Any order up to PL_MAX_ORDER within
+ * subset_order_limit. Synchronous. */
+pl_status pl_ryser_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
+                                    int32_t* negative, const pl_limits* limits, void* stream);
+pl_status pl_ryser_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* primes, const int64_t* residues,
+                                  uint32_t* out, const pl_limits* limits, void* stream);
+
 /* Operation counts of the Store-zechin recurrence (reference measures them
  * through Counted<T>, op_count.hpp:52-70; closed form cost_model.cpp:176-181):
  * n = 1 -> (0, 0); n = 2 -> (2, 1); n >= 3 -> (n*2^(n-1) - n, n*2^(n-1) - 2^n + 1). */

@@ -69,6 +69,8 @@ EXPORTED_SYMBOLS = (
     "pl_sz_permanent_bigint",
     "pl_sz_permanent_modp",
     "pl_bigint_primes",
+    "pl_ryser_permanent_bigint",
+    "pl_ryser_permanent_modp",
 )
 
 
@@ -142,6 +144,10 @@ def _load():
     L.pl_sz_permanent_bigint.restype = C.c_int
     L.pl_sz_permanent_modp.argtypes = [i32, i32, vp, vp, vp, C.POINTER(pl_limits), vp]
     L.pl_sz_permanent_modp.restype = C.c_int
+    L.pl_ryser_permanent_bigint.argtypes = L.pl_sz_permanent_bigint.argtypes
+    L.pl_ryser_permanent_bigint.restype = C.c_int
+    L.pl_ryser_permanent_modp.argtypes = L.pl_sz_permanent_modp.argtypes
+    L.pl_ryser_permanent_modp.restype = C.c_int
     L.pl_bigint_primes.argtypes = [i32, vp]
     L.pl_bigint_primes.restype = i32
     return L

@@ -149,22 +149,22 @@ def _as_matrix(a) -> np.ndarray:
     return np.ascontiguousarray(arr)
 
 
-def _bigint_from_int64(m: np.ndarray, lim) -> int:
+def _bigint_from_int64(m: np.ndarray, lim, ryser: bool = False) -> int:
     """Exact permanent of an int64 matrix whose intermediates leave int64
     (``pl_sz_permanent_bigint``: residue passes on the device, CRT in the library)."""
     n = m.shape[0]
     cap = 40
     limbs = np.zeros(cap, dtype=np.uint64)
     nl, neg = C.c_size_t(0), C.c_int32(0)
-    _check(N.lib.pl_sz_permanent_bigint(n, m.ctypes.data, limbs.ctypes.data, cap, C.byref(nl), C.byref(neg),
-                                        C.byref(lim), None))
+    fn = N.lib.pl_ryser_permanent_bigint if ryser else N.lib.pl_sz_permanent_bigint
+    _check(fn(n, m.ctypes.data, limbs.ctypes.data, cap, C.byref(nl), C.byref(neg), C.byref(lim), None))
     v = 0
     for i in reversed(range(nl.value)):
         v = (v << 64) | int(limbs[i])
     return -v if neg.value else v
 
 
-def _bigint_from_objects(m: np.ndarray, lim) -> int:
+def _bigint_from_objects(m: np.ndarray, lim, ryser: bool = False) -> int:
     """Exact permanent of a matrix of Python integers of any size: residues modulo the
     engine's primes go through ``pl_sz_permanent_modp``; the CRT runs on Python integers."""
     n = m.shape[0]
@@ -178,7 +178,8 @@ def _bigint_from_objects(m: np.ndarray, lim) -> int:
         raise DeviceError("pl_bigint_primes failed")
     res = np.array([[[v % int(p) for v in r] for r in rows] for p in primes], dtype=np.int64)
     out = np.zeros(k, dtype=np.uint32)
-    _check(N.lib.pl_sz_permanent_modp(n, k, primes.ctypes.data, res.ctypes.data, out.ctypes.data, C.byref(lim), None))
+    fn = N.lib.pl_ryser_permanent_modp if ryser else N.lib.pl_sz_permanent_modp
+    _check(fn(n, k, primes.ctypes.data, res.ctypes.data, out.ctypes.data, C.byref(lim), None))
     x, mod = 0, 1
     for p, r in zip((int(p) for p in primes), (int(r) for r in out)):
         x += mod * (((r - x) * pow(mod, -1, p)) % p)
@@ -227,14 +228,18 @@ def ryser_counts(n: int) -> OpCount:
 def ryser_permanent(a, limits: Optional[Limits] = None) -> PermanentResult:
     """Permanent by Ryser's formula on the device (reference ``permanent.hpp:84``,
     ``permanent.cpp:85-136``): float rings bitwise the reference's visit-order
-    fold, int64 exact (guarded)."""
+    fold; integers exact at any magnitude (128-bit wrapping sums where the
+    guard bound allows, else inclusion-exclusion on residues, ``csrc/bigint.cu``)."""
     m = _as_matrix(a)
-    if m.dtype == object:
-        raise DomainError("integer entries beyond int64 are not offered by the Ryser device engine")
     n = m.shape[0]
     lim = (limits or Limits()).to_c()
+    if m.dtype == object:
+        return PermanentResult(_bigint_from_objects(m, lim, ryser=True), ryser_counts(n), "ryser")
     out = np.zeros(1, dtype=m.dtype)
-    _check(N.lib.pl_ryser_permanent(_DTYPES[m.dtype], n, m.ctypes.data, out.ctypes.data, 0, C.byref(lim), None))
+    status = N.lib.pl_ryser_permanent(_DTYPES[m.dtype], n, m.ctypes.data, out.ctypes.data, 0, C.byref(lim), None)
+    if status == N.PL_ERR_OVERFLOW and m.dtype == np.int64:
+        return PermanentResult(_bigint_from_int64(m, lim, ryser=True), ryser_counts(n), "ryser")
+    _check(status)
     return PermanentResult(_py_value(out), ryser_counts(n), "ryser")
 
 

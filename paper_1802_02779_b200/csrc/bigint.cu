@@ -120,6 +120,58 @@ __global__ void __launch_bounds__(1024) sz_modp_small_kernel(const long long* __
     if (threadIdx.x == 0) out[blockIdx.x] = x[total - 1];
 }
 
+// Ryser's formula on residues (reference proj/src/permanent.cpp:85-136 on its Int ring):
+// per(A) = (-1)^n sum_{S nonempty} (-1)^|S| prod_i sum_{j in S} a_ij. Grid (blocks, primes);
+// every thread walks masks S = t + 1, keeps the positive and negative terms apart (sums of
+// residues below 2^31 stay far below 2^64) and the block writes (pos - neg) mod p. The visit
+// order is immaterial: residue arithmetic is exact.
+__global__ void __launch_bounds__(256) ryser_modp_kernel(const long long* __restrict__ res, int n,
+                                                         const uint32_t* __restrict__ primes,
+                                                         uint32_t* __restrict__ partial) {
+    extern __shared__ uint32_t coef[];  // n * n residues of this prime
+    __shared__ u64 wpos[8], wneg[8];
+    const u64 p = primes[blockIdx.y];
+    const u64 m = ~0ull / p;
+    const long long* a = res + (size_t)blockIdx.y * n * n;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) coef[e] = (uint32_t)a[e];
+    __syncthreads();
+    auto reduce = [&](u64 v) {  // v < 2^62
+        const u64 q = __umul64hi(v, m);
+        u64 r = v - q * p;
+        while (r >= p) r -= p;
+        return r;
+    };
+    const u64 total = (n >= 64 ? 0 : (1ull << n)) - 1;
+    u64 pos = 0, neg = 0;
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        const u64 S = t + 1;
+        u64 prod = 1;
+        for (int i = 0; i < n && prod; ++i) {
+            u64 rs = 0;
+            for (u64 w = S; w; w &= w - 1) rs += coef[i * n + __ffsll((long long)w) - 1];
+            prod = reduce(prod * reduce(rs));
+        }
+        if (__popcll(S) & 1) neg += prod; else pos += prod;
+    }
+    for (int d = 16; d; d >>= 1) {
+        pos += __shfl_xor_sync(0xffffffffu, pos, d);
+        neg += __shfl_xor_sync(0xffffffffu, neg, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        wpos[threadIdx.x >> 5] = pos;
+        wneg[threadIdx.x >> 5] = neg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 bp = 0, bn = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            bp += wpos[w];
+            bn += wneg[w];
+        }
+        partial[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = (uint32_t)((bp % p + p - bn % p) % p);
+    }
+}
+
 constexpr int kSmallMax = 14;
 
 pl_status check_residues(int n, int k, const uint32_t* primes, const int64_t* res) {
@@ -210,6 +262,54 @@ pl_status run_residues(int n, int k, const uint32_t* primes, const int64_t* res,
     release();
 #undef PLB_TRY
     for (int i = 0; i < k; ++i) out[i] = (uint32_t)host[i];
+    return PL_OK;
+}
+
+// out[i] = per(R_i) mod primes[i] by Ryser's formula (any n <= PL_MAX_ORDER).
+pl_status run_ryser_residues(int n, int k, const uint32_t* primes, const int64_t* res, uint32_t* out,
+                             const pl_limits* lim, cudaStream_t st) {
+    pl_status s = plc::check_order_limits(n, lim);
+    if (s != PL_OK) return s;
+    if ((s = check_residues(n, k, primes, res)) != PL_OK) return s;
+    if ((s = plc::device_ready()) != PL_OK) return s;
+    const u64 total = (1ull << n) - 1;
+    const unsigned blocks = (unsigned)std::max<u64>(1, std::min<u64>((total + 255) / 256, (u64)plc::sm_count() * 8));
+    const size_t in_bytes = (size_t)k * n * n * sizeof(long long);
+    long long* a_dev = nullptr;
+    uint32_t* primes_dev = nullptr;
+    uint32_t* part_dev = nullptr;
+    auto release = [&] {
+        if (a_dev) cudaFreeAsync(a_dev, st);
+        if (primes_dev) cudaFreeAsync(primes_dev, st);
+        if (part_dev) cudaFreeAsync(part_dev, st);
+    };
+#define PLB_TRY(expr)                          \
+    do {                                       \
+        cudaError_t _e = (expr);               \
+        if (_e != cudaSuccess) {               \
+            release();                         \
+            return plc::cuda_error(_e, #expr); \
+        }                                      \
+    } while (0)
+    PLB_TRY(cudaMallocAsync((void**)&a_dev, in_bytes, st));
+    PLB_TRY(cudaMallocAsync((void**)&primes_dev, (size_t)k * sizeof(uint32_t), st));
+    PLB_TRY(cudaMallocAsync((void**)&part_dev, (size_t)k * blocks * sizeof(uint32_t), st));
+    PLB_TRY(cudaMemcpyAsync(a_dev, res, in_bytes, cudaMemcpyHostToDevice, st));
+    PLB_TRY(cudaMemcpyAsync(primes_dev, primes, (size_t)k * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    ryser_modp_kernel<<<dim3(blocks, (unsigned)k), 256, (size_t)n * n * sizeof(uint32_t), st>>>(a_dev, n, primes_dev,
+                                                                                               part_dev);
+    PLB_TRY(cudaGetLastError());
+    std::vector<uint32_t> part((size_t)k * blocks);
+    PLB_TRY(cudaMemcpyAsync(part.data(), part_dev, part.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PLB_TRY(cudaStreamSynchronize(st));
+    release();
+#undef PLB_TRY
+    for (int i = 0; i < k; ++i) {
+        const u64 p = primes[i];
+        u64 sum = 0;
+        for (unsigned b = 0; b < blocks; ++b) sum = (sum + part[(size_t)i * blocks + b]) % p;
+        out[i] = (uint32_t)((n & 1) ? (p - sum) % p : sum);
+    }
     return PL_OK;
 }
 
@@ -314,11 +414,15 @@ int32_t pl_bigint_primes(int32_t count, uint32_t* out) {
     return count;
 }
 
-pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
-                                 int32_t* negative, const pl_limits* limits, void* stream) {
+}  // extern "C"
+
+namespace {
+
+pl_status permanent_bigint(bool ryser, int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
+                           int32_t* negative, const pl_limits* limits, void* stream) {
     if (n < 1) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1");
     if (!a || !nlimbs || !negative || (limb_cap && !limbs)) {
-        return plc::fail_msg(PL_ERR_ARG, "bad arguments to pl_sz_permanent_bigint");
+        return plc::fail_msg(PL_ERR_ARG, "bad arguments to the big-integer permanent");
     }
     const pl_status lim_s = plc::check_order_limits(n, limits);  // also the device cap (PL_MAX_ORDER)
     if (lim_s != PL_OK) return lim_s;
@@ -344,7 +448,9 @@ pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, s
         }
     }
     std::vector<uint32_t> out((size_t)k);
-    pl_status s = run_residues(n, k, ps.data(), res.data(), out.data(), limits, static_cast<cudaStream_t>(stream));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pl_status s = ryser ? run_ryser_residues(n, k, ps.data(), res.data(), out.data(), limits, st)
+                        : run_residues(n, k, ps.data(), res.data(), out.data(), limits, st);
     if (s != PL_OK) return s;
     Limbs mag;
     bool neg = false;
@@ -354,6 +460,27 @@ pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, s
     if (mag.size() > limb_cap) return plc::fail_msg(PL_ERR_ARG, "limb buffer too small (see *nlimbs)");
     if (!mag.empty()) std::memcpy(limbs, mag.data(), mag.size() * sizeof(uint64_t));
     return PL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pl_status pl_sz_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
+                                 int32_t* negative, const pl_limits* limits, void* stream) {
+    return permanent_bigint(false, n, a, limbs, limb_cap, nlimbs, negative, limits, stream);
+}
+
+pl_status pl_ryser_permanent_bigint(int32_t n, const int64_t* a, uint64_t* limbs, size_t limb_cap, size_t* nlimbs,
+                                    int32_t* negative, const pl_limits* limits, void* stream) {
+    return permanent_bigint(true, n, a, limbs, limb_cap, nlimbs, negative, limits, stream);
+}
+
+pl_status pl_ryser_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* primes, const int64_t* residues,
+                                  uint32_t* out, const pl_limits* limits, void* stream) {
+    if (n < 1) return plc::fail_msg(PL_ERR_ARG, "matrix order must be >= 1");
+    if (nprimes < 1 || !primes || !residues || !out) return plc::fail_msg(PL_ERR_ARG, "bad arguments to pl_ryser_permanent_modp");
+    return run_ryser_residues(n, nprimes, primes, residues, out, limits, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

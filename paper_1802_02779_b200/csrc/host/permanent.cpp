@@ -263,11 +263,14 @@ std::string BigInt::str() const {
     return out;
 }
 
-BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits) {
+namespace {
+
+BigInt exact_int(bool ryser, const Matrix<Int>& a, const Limits& limits) {
     const pl_limits lim = to_c(limits);
     BigInt r;
     Int v = 0;
-    const pl_status s = pl_sz_permanent(PL_I64, a.order(), a.entries().data(), &v, 0, &lim, nullptr);
+    const pl_status s = ryser ? pl_ryser_permanent(PL_I64, a.order(), a.entries().data(), &v, 0, &lim, nullptr)
+                              : pl_sz_permanent(PL_I64, a.order(), a.entries().data(), &v, 0, &lim, nullptr);
     if (s == PL_OK) {
         r.negative = v < 0;
         if (v != 0) r.limbs.push_back(v < 0 ? ~static_cast<std::uint64_t>(v) + 1 : static_cast<std::uint64_t>(v));
@@ -277,12 +280,17 @@ BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits) 
     r.limbs.resize(40);  // 34 x 34 int64 entries need at most 37
     std::size_t nl = 0;
     std::int32_t neg = 0;
-    check(pl_sz_permanent_bigint(a.order(), a.entries().data(), r.limbs.data(), r.limbs.size(), &nl, &neg, &lim,
-                                 nullptr));
+    check((ryser ? pl_ryser_permanent_bigint : pl_sz_permanent_bigint)(a.order(), a.entries().data(), r.limbs.data(),
+                                                                       r.limbs.size(), &nl, &neg, &lim, nullptr));
     r.limbs.resize(nl);
     r.negative = neg != 0;
     return r;
 }
+
+}  // namespace
+
+BigInt store_zechin_permanent_exact(const Matrix<Int>& a, const Limits& limits) { return exact_int(false, a, limits); }
+BigInt ryser_permanent_exact(const Matrix<Int>& a, const Limits& limits) { return exact_int(true, a, limits); }
 
 OpCount ryser_counts(int n) {
     OpCount c;

@@ -300,6 +300,10 @@ void device_run_and_batch() {
         const BigInt small = store_zechin_permanent_exact(Matrix<Int>::filled(5, -2));
         CHECK(small.fits_int64() && small.to_int64() == -3840 && small.str() == "-3840");
         CHECK(store_zechin_permanent_exact(Matrix<Int>::filled(16, 0)).str() == "0");
+        // Ryser's formula, same integers (residue sums beyond the 128-bit guard)
+        CHECK(ryser_permanent_exact(Matrix<Int>::filled(22, 1000)).str() == big.str());
+        CHECK(ryser_permanent_exact(Matrix<Int>::filled(21, -1)).str() == neg.str());
+        CHECK(ryser_permanent_exact(Matrix<Int>::filled(5, -2)).to_int64() == -3840);
     }
     // the guard is conservative but the checked path still computes what fits
     CHECK(value_of(store_zechin_permanent(SquareMatrix(Matrix<Int>::filled(20, 1)))) == 2432902008176640000LL);

@@ -103,6 +103,23 @@ def test_python_integers_beyond_int64_entries():
     assert got > 10 ** (30 * n)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 10, 13, 18])
+def test_ryser_residue_sums_equal_store_zechin(n):
+    # Ryser's formula on the same residues (pl_ryser_permanent_bigint): the same integer
+    rng = np.random.default_rng(9400 + n)
+    a = rng.integers(-(2 ** 62), 2 ** 62, (n, n), dtype=np.int64)
+    want = pl.store_zechin_permanent(a).value
+    if n <= 10:
+        assert want == py_permanent([[int(v) for v in r] for r in a])
+    assert pl.ryser_permanent(a).value == want
+    rows = [[int(v) * 7 ** 30 + 1 for v in r] for r in a]  # entries beyond int64: Python integers
+    if n <= 10:
+        assert pl.ryser_permanent(np.array(rows, dtype=object)).value == py_permanent(rows)
+    else:
+        assert (pl.ryser_permanent(np.array(rows, dtype=object)).value
+                == pl.store_zechin_permanent(np.array(rows, dtype=object)).value)
+
+
 def test_zero_small_and_values_that_fit():
     a = np.zeros((21, 21), dtype=np.int64)
     lim = pl.Limits().to_c()

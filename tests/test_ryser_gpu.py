@@ -70,12 +70,25 @@ def test_ryser_agrees_with_store_zechin_complex():
 
 
 def test_ryser_int_overflow_guard():
-    # all-ones 21 x 21: per = 21! > 2^63 -> refused (the reference's Int is unbounded)
-    with pytest.raises(pl.DomainError, match="overflow"):
-        pl.ryser_permanent(np.ones((21, 21), dtype=np.int64))
-    # 30 x 30 with row sums 300: the 128-bit guard (300^30 > 2^126) refuses
-    with pytest.raises(pl.DomainError, match="overflow"):
-        pl.ryser_permanent(np.full((30, 30), 10, dtype=np.int64))
+    import ctypes as C
+    import math
+
+    from paper_1802_02779_b200 import _native as N
+
+    # all-ones 21 x 21: per = 21! > 2^63 -- the int64 entry point of the C ABI refuses (never wraps) ...
+    ones21 = np.ones((21, 21), dtype=np.int64)
+    out = np.zeros(1, dtype=np.int64)
+    lim = pl.Limits().to_c()
+    assert N.lib.pl_ryser_permanent(N.PL_I64, 21, ones21.ctypes.data, out.ctypes.data, 0, C.byref(lim),
+                                    None) == N.PL_ERR_OVERFLOW
+    # ... and the Python call returns the reference's unbounded Int through the residue sums
+    assert pl.ryser_permanent(ones21).value == math.factorial(21)
+    # 26 x 26 with row sums 260: the 128-bit guard (260^26 > 2^126) refuses, the residue path is exact
+    tens = np.full((26, 26), 10, dtype=np.int64)
+    assert N.lib.pl_ryser_permanent(N.PL_I64, 26, tens.ctypes.data, out.ctypes.data, 0, C.byref(lim),
+                                    None) == N.PL_ERR_OVERFLOW
+    r = pl.ryser_permanent(tens)
+    assert r.value == 10 ** 26 * math.factorial(26) and r.algorithm == "ryser" and r.counts == pl.ryser_counts(26)
     assert pl.ryser_permanent(np.ones((12, 12), dtype=np.int64)).value == 479001600
     assert pl.ryser_permanent(np.ones((20, 20), dtype=np.int64)).value == 2432902008176640000
 
