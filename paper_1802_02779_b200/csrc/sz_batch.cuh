@@ -83,8 +83,26 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
     const int64_t nbatch = (count + Gm::kBatch - 1) / Gm::kBatch;
     // batches staged by TMA: the full ones, when the input is 16-byte aligned
     const int64_t nfull = (reinterpret_cast<uintptr_t>(a) & 15u) ? 0 : count / Gm::kBatch;
+#ifndef PL_BATCH_SPLIT
+#define PL_BATCH_SPLIT 1
+#endif
+#if PL_BATCH_SPLIT
+    // Even contiguous ranges: warp w of W takes batches [w q + w r / W, (w + 1) q + (w + 1) r / W)
+    // (q, r = nbatch / W, nbatch % W), so the warps with one batch more are interleaved with the
+    // others and every CTA -- hence every SM -- carries the same load to within one batch. A
+    // strided split gives the extra round to the first CTAs only (C2: 24 against 20 warp-batches
+    // per SM).
+    const int64_t nwarps = (int64_t)gridDim.x * Gm::kWarps;
+    const int64_t wid = (int64_t)blockIdx.x * Gm::kWarps + warp;
+    const int64_t q_ = nbatch / nwarps, r_ = nbatch % nwarps;
+    const int64_t stride = 1;
+    int64_t b = wid * q_ + wid * r_ / nwarps;
+    const int64_t bend = (wid + 1) * q_ + (wid + 1) * r_ / nwarps;
+#else
     const int64_t stride = (int64_t)gridDim.x * Gm::kWarps;
     int64_t b = (int64_t)blockIdx.x * Gm::kWarps + warp;
+    const int64_t bend = nbatch;
+#endif
     // programmatic dependent launch: the next grid on the stream may be
     // scheduled now; this grid reads nothing before the previous one is done
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -102,9 +120,9 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
                      &bar[slot]);
         }
     };
-    if (b < nfull) issue(b, 0);
+    if (b < nfull && b < bend) issue(b, 0);
     bool ov_any = false;
-    for (uint32_t it = 0; b < nbatch; b += stride, ++it) {
+    for (uint32_t it = 0; b < bend; b += stride, ++it) {
         const int64_t mi = b * Gm::kBatch + lane;
         bool ov = false;
         T v = R::zero();
@@ -119,12 +137,12 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
                 // the refill may only be issued once every load has returned (loaded_dep)
                 const uint32_t dep = loaded_dep(m.v, Gm::kEnt, (uint32_t)((uint64_t)count >> 62));  // count < 2^62
                 __syncwarp();
-                if (b + stride + dep < nfull) issue(b + stride + dep, 0);
+                if (b + stride + dep < nfull && b + stride < bend) issue(b + stride + dep, 0);
                 v = batch_eval<R, N>(m.v, ov);
             }
         } else {
             const int slot = it & 1;
-            if (b + stride < nfull) issue(b + stride, slot ^ 1);  // that buffer was released at the end of it - 1
+            if (b + stride < nfull && b + stride < bend) issue(b + stride, slot ^ 1);  // that buffer was released at the end of it - 1
             if (b < nfull) {
                 mbar_wait(&bar[slot], (it >> 1) & 1u);
                 v = batch_eval<R, N>(buf + slot * Gm::kBatchElems + lane * Gm::kEnt, ov);
