@@ -80,6 +80,14 @@ typedef struct pl_limits {
 #define PL_FLAG_ASYNC 0x4u       /* device pointers only: enqueue on `stream` and return;   */
                                  /* int64 overflow is reported into *status_dev instead     */
 
+#define PL_FLAG_INPUT_READY 0x8u /* device pointers only: the caller states that `a` is not      */
+                                 /* written by work still running on `stream` (it was uploaded   */
+                                 /* or produced earlier and that work has completed, or on       */
+                                 /* another stream the caller has already waited for). The batch */
+                                 /* kernels of orders <= 5 then start loading while the previous */
+                                 /* kernel on the stream drains (programmatic dependent launch); */
+                                 /* their stores still wait for it. Results are identical.       */
+
 /* Bits OR-ed into a caller-owned device status word by PL_FLAG_ASYNC calls. */
 #define PL_STATUS_BIT_OVERFLOW 0x1
 #define PL_STATUS_BIT_ROWS 0x2 /* boson: a malformed output row list (its probability is NaN) */

@@ -21,6 +21,7 @@ PL_I64, PL_F64, PL_C128 = 0, 1, 2
 PL_FLAG_DEVICE_PTRS = 0x1
 PL_FLAG_FMA = 0x2
 PL_FLAG_ASYNC = 0x4
+PL_FLAG_INPUT_READY = 0x8
 PL_STATUS_BIT_OVERFLOW = 0x1
 PL_STATUS_BIT_ROWS = 0x2
 PL_MAX_ORDER = 34

@@ -296,7 +296,7 @@ def _torch_dtype_code(t) -> int:
 
 
 def store_zechin_permanent_batch(a, limits: Optional[Limits] = None, out=None, fma: bool = False,
-                                 stream=None, status=None):
+                                 stream=None, status=None, input_ready: bool = False):
     """Permanents of a batch ``(count, n, n)``.
 
     * numpy array (host): returns a numpy array of ``count`` values; the copy
@@ -306,6 +306,9 @@ def store_zechin_permanent_batch(a, limits: Optional[Limits] = None, out=None, f
       ``torch.cuda.Stream`` (default: the current stream). With ``status`` (a
       CUDA int32 tensor of one element, zeroed by the caller) the call is
       asynchronous and int64 overflow is reported there.
+      ``input_ready=True`` (``PL_FLAG_INPUT_READY``) states that ``a`` is not written by work
+      still running on the stream: consecutive batch kernels of orders <= 5 then overlap their
+      load ramp with the previous kernel's tail (same results).
     * torch tensor on CPU (pinned or not): host path like numpy.
     """
     lim = (limits or Limits()).to_c()
@@ -322,6 +325,8 @@ def store_zechin_permanent_batch(a, limits: Optional[Limits] = None, out=None, f
             if not out.is_cuda:
                 raise DomainError("device input needs a device output")
             flags |= N.PL_FLAG_DEVICE_PTRS
+            if input_ready:
+                flags |= N.PL_FLAG_INPUT_READY
             st = (stream or torch.cuda.current_stream(a.device)).cuda_stream
             status_ptr = None
             if status is not None:

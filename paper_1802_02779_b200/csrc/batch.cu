@@ -145,7 +145,7 @@ pl_status launch_regs_n(const void* a, void* out, int64_t count, int32_t* status
     const int64_t batches = (count + Gm::kBatch - 1) / Gm::kBatch;
     const int64_t blocks = std::min<int64_t>((batches + Gm::kWarps - 1) / Gm::kWarps, (int64_t)num_sms() * per_sm);
     PL_CUDA(launch_pdl(kern, (unsigned)blocks, Gm::kThreads, Gm::kSmem, st, static_cast<const T*>(a),
-                       static_cast<T*>(out), count, status));
+                       static_cast<T*>(out), count, status, plc::input_ready_hint() ? 1 : 0));
     return PL_OK;
 }
 

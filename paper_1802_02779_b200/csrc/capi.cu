@@ -1077,6 +1077,11 @@ pl_status fail_msg(pl_status s, const char* msg) { return fail(s, "%s", msg); }
 pl_status cuda_error(cudaError_t e, const char* what) { return cuda_fail(e, what); }
 pl_status device_ready() { return have_device(); }
 int sm_count() { return num_sms(); }
+namespace {
+thread_local bool tl_input_ready = false;
+}
+bool input_ready_hint() { return tl_input_ready; }
+void set_input_ready_hint(bool on) { tl_input_ready = on; }
 pl_status set_modulus(const pl::ModParams* mp, cudaStream_t st) {
     PL_CUDA(cudaMemcpyToSymbolAsync(pl::c_modp, mp, sizeof(pl::ModParams), 0, cudaMemcpyHostToDevice, st));
     return PL_OK;
@@ -1215,7 +1220,11 @@ pl_status pl_sz_permanent_batch(pl_dtype dtype, int32_t n, int64_t count, const 
     if (limits && limits->num_gpus >= 1) {
         return plc::run_multi(dtype, n, count, a, out, flags, limits, nullptr, static_cast<cudaStream_t>(stream));
     }
-    return run_batch(dtype, n, count, a, out, flags, status_dev, static_cast<cudaStream_t>(stream));
+    // device pointers only: a host batch is uploaded by this call, so its input is never "ready"
+    plc::set_input_ready_hint((flags & PL_FLAG_INPUT_READY) && (flags & PL_FLAG_DEVICE_PTRS));
+    s = run_batch(dtype, n, count, a, out, flags, status_dev, static_cast<cudaStream_t>(stream));
+    plc::set_input_ready_hint(false);
+    return s;
 }
 
 pl_status pl_sz_permanent(pl_dtype dtype, int32_t n, const void* a, void* out, uint32_t flags,

@@ -21,6 +21,11 @@ constexpr pl_dtype kModDtype = static_cast<pl_dtype>(3);
 // stay valid until the stream gets there).
 pl_status set_modulus(const pl::ModParams* mp, cudaStream_t st);
 
+// PL_FLAG_INPUT_READY of the entry point running on this thread (read by the
+// n <= 5 batch launch in batch.cu: loads before griddepcontrol.wait).
+bool input_ready_hint();
+void set_input_ready_hint(bool on);
+
 // Set the thread-local pl_last_error() message and return `s`.
 pl_status fail_msg(pl_status s, const char* msg);
 // Map a CUDA error (allocation failures to PL_ERR_NOMEM).

@@ -72,7 +72,7 @@ template <class R, int N>
 // registers and 3 CTAs (a 128-register cap spills and costs C2 ~5 %)
 __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChecked ? 4 : 3)
     sz_batch_tma_kernel(const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
-                        int32_t* __restrict__ status) {
+                        int32_t* __restrict__ status, int early_loads) {
     using T = typename R::T;
     using Gm = BatchGeom<T, N>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -104,7 +104,11 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
     const int64_t bend = nbatch;
 #endif
     // programmatic dependent launch: the next grid on the stream may be
-    // scheduled now; this grid reads nothing before the previous one is done
+    // scheduled now; this grid reads nothing before the previous one is done --
+    // unless the caller states that the input is not produced by work still
+    // running on the stream (PL_FLAG_INPUT_READY, early_loads): then the loads
+    // start at once, overlapping the previous grid's tail, and only the stores
+    // wait for the previous grid
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (lane == 0) {
         mbar_init(&bar[0], 1);
@@ -112,7 +116,8 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (!early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    bool waited = !early_loads;
     auto issue = [&](int64_t batch, int slot) {
         if (lane == 0) {
             mbar_arrive_expect_tx(&bar[slot], Gm::kBatchBytes);
@@ -153,6 +158,10 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
             load_matrix<T, Gm::kEnt>(a + mi * Gm::kEnt, m);
             v = batch_eval<R, N>(m.v, ov);
         }
+        if (!waited) {  // warp-uniform: before this grid's first store
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            waited = true;
+        }
         if (mi < count) {
             if (ov) v = R::zero();
             out[mi] = v;
@@ -160,6 +169,7 @@ __global__ void __launch_bounds__(BatchGeom<typename R::T, N>::kThreads, R::kChe
         }
         __syncwarp();
     }
+    if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (ov_any) atomicOr(status, 1);
 }
 

@@ -672,3 +672,53 @@ def test_blocked_f32_pack_kernel_opt_in():
         a = configs.int_matrices(n, 203, seed=77 + n, lo=-1, hi=2)
         a[5] *= 3  # its pack leaves the FP32 bound: member-by-member fallback
         assert np.array_equal(np.load("/tmp/_blk_f32_%d.npy" % n), O.sz_batch(a))
+
+
+@pytest.mark.parametrize("dtype,n", [("int64", 5), ("complex128", 5), ("float64", 4), ("complex128", 3), ("int64", 1)])
+def test_input_ready_flag_overlapped_launches_equal_to_oracle(dtype, n):
+    # PL_FLAG_INPUT_READY: the n <= 5 batch kernel loads before griddepcontrol.wait, so back-to-back
+    # launches (plain stream and CUDA graph) overlap; every launch's results are those of the oracle,
+    # also with a ragged tail (count % 32 != 0), a misaligned input and an output the previous launch wrote
+    import torch
+
+    count = 32 * 257 + 19
+    if dtype == "int64":
+        a_np = configs.int_matrices(n, count, seed=8100 + n, lo=-9, hi=9)
+    elif dtype == "float64":
+        a_np = configs.uniform((count, n, n), seed=8200 + n)
+    else:
+        a_np = configs.complex_uniform((count, n, n), seed=8300 + n)
+    want = O.sz_batch(a_np)
+    bufs = [torch.from_numpy(a_np).cuda() for _ in range(3)]
+    outs = [torch.zeros(count, dtype=bufs[0].dtype, device="cuda") for _ in range(3)]
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for rep in range(4):
+        for b, o in zip(bufs, outs):
+            o.zero_()
+            pl.store_zechin_permanent_batch(b, out=o, status=status, input_ready=True)
+        pl.store_zechin_permanent_batch(bufs[0], out=outs[1], status=status, input_ready=True)  # rewrite an output
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    for o in outs:
+        o.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(12):
+            pl.store_zechin_permanent_batch(bufs[i % 3], out=outs[i % 3], status=status, stream=s, input_ready=True)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    assert int(status.item()) == 0
+    if n >= 2:  # a misaligned device view (8-byte entries, odd element offset): the direct-load path
+        flat = torch.zeros(a_np.size + 1, dtype=bufs[0].dtype, device="cuda")
+        flat[1:] = bufs[0].reshape(-1)
+        view = flat[1:].reshape(count, n, n)
+        o = pl.store_zechin_permanent_batch(view, status=status, input_ready=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(o.cpu().numpy().view(np.uint64), want.view(np.uint64))
