@@ -181,6 +181,8 @@ def config_dict(name: str, world: int, fma: bool) -> dict:
     batched = spec["n"] <= 16
     if batched:
         l2 = "inputs from HBM every step: rotating device copies of the batch (>= 320 MiB > L2), K steps in one CUDA graph"
+        if os.environ.get("PL_BENCH_INPUT_READY", "1") != "0" and (spec["n"] <= 5 or name == "c3"):
+            l2 += "; steps launched with PL_FLAG_INPUT_READY (static inputs: a step's loads overlap the previous step's tail)"
         par = f"dp{world} (batch by matrix, no collective)"
     else:
         l2 = "L2 flushed between timed steps (256 MiB write, then 256 MiB read), one event pair per step"
@@ -417,7 +419,7 @@ def measure_config(name, steps, warmup, rank, world, device, flush_buf, fma=Fals
         times = [e0.elapsed_time(e1)]
         timing = f"{reps} rotating device copies of the batch ({reps * in_bytes / 2**20:.0f} MiB > L2), " \
                  f"{steps} steps in one CUDA graph between one event pair" \
-                 + ("; PL_FLAG_INPUT_READY (a step's loads overlap the previous step's tail)" if ready and n <= 5 else "")
+                 + ("; PL_FLAG_INPUT_READY (a step's loads overlap the previous step's tail)" if ready and (n <= 5 or name == "c3") else "")
         del bufs
     else:
         evs = []

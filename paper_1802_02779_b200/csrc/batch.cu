@@ -325,9 +325,22 @@ pl_status launch_f32_pack_n(const void* a, void* out, int64_t count, int32_t* st
     per_sm = std::max(per_sm, 1);
     const int64_t packs = (count + P - 1) / P;
     const int64_t blocks = std::min<int64_t>(packs, (int64_t)num_sms() * per_sm);
+    if (plc::input_ready_hint()) {
+        // PL_FLAG_INPUT_READY: programmatic dependent launch, loads before the previous grid is done
+        // (C3 72 -> 64 us per step in a stream of batches: no launch gap and the next grid's CTAs
+        // fill the slots the last, partial round leaves idle)
+        PL_CUDA(launch_pdl(kern, (unsigned)blocks, (unsigned)pl::kF32Threads, smem, st,
+                           static_cast<const long long*>(a), static_cast<long long*>(out), count, maxc,
+                           (const uint16_t*)pt.tab, (const uint32_t*)pt.off, pt.t32(8), pt.t32(4 * P),
+                           (const uint32_t*)pt.tab2, (const uint32_t*)pt.off2, status, 1));
+        return PL_OK;
+    }
+    // plain launch otherwise: with the attribute but the wait up front the dependent CTAs only sit in
+    // the freed slots (measured 77 against 72 us per step)
     kern<<<(unsigned)blocks, pl::kF32Threads, smem, st>>>(static_cast<const long long*>(a),
                                                          static_cast<long long*>(out), count, maxc, pt.tab,
-                                                               pt.off, pt.t32(8), pt.t32(4 * P), pt.tab2, pt.off2, status);
+                                                         pt.off, pt.t32(8), pt.t32(4 * P), pt.tab2, pt.off2, status,
+                                                         0);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

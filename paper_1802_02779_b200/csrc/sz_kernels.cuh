@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
     const long long* __restrict__ a, long long* __restrict__ out, int64_t count, int maxc,
     const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32_8,
     const uint32_t* __restrict__ ptab32_16, const uint32_t* __restrict__ tab2, const uint32_t* __restrict__ off2,
-    int32_t* __restrict__ status) {
+    int32_t* __restrict__ status, int early_loads) {
     constexpr int n = N, E = N * N;
     using PR = PackRing<RF32X, P>;
     using PT = typename PR::T;
@@ -827,6 +827,11 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
     __shared__ int mode[P], flag;
     const int tid = threadIdx.x;
     const int64_t npacks = (count + P - 1) / P;
+    // programmatic dependent launch (see sz_batch_tma_kernel): the next grid may be scheduled as
+    // CTAs of this one exit; nothing is read before the previous grid is done unless the caller
+    // marked the input ready (PL_FLAG_INPUT_READY) -- then only the stores wait
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (!early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     for (int64_t pb = blockIdx.x; pb < npacks; pb += gridDim.x) {
         const int64_t b0 = P * pb;
         const int have = count - b0 < P ? (int)(count - b0) : P;
@@ -869,10 +874,12 @@ __global__ void __launch_bounds__(kF32Threads) sz_batch_f32_pack_kernel(
             }
             if (tid == 0) {
                 const PT t = smem_top<PR, PT, N>(mat, last, n, ov);
+                if (early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // before this grid's stores
 #pragma unroll
                 for (int i = 0; i < P; ++i) out[b0 + i] = (long long)t.v[i];
             }
         } else {
+            if (early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
             f32_pack_members<N>(g, have, mode, flag, smem_raw, maxc, ptab, poff, ptab32_8, out, b0, status);
         }
         __syncthreads();

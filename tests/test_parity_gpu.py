@@ -722,3 +722,41 @@ def test_input_ready_flag_overlapped_launches_equal_to_oracle(dtype, n):
         o = pl.store_zechin_permanent_batch(view, status=status, input_ready=True)
         torch.cuda.synchronize()
         assert np.array_equal(o.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [10, 12, 14])
+def test_input_ready_flag_f32_packs_equal_to_oracle(n):
+    # the FP32-exact int64 pack kernel (10 <= n <= 14) under programmatic dependent launch, with and
+    # without PL_FLAG_INPUT_READY: back-to-back and graph-replayed launches, ragged last pack, a
+    # member outside the byte range of the packed coefficients
+    import torch
+
+    count = 4 * 301 + 3
+    a_np = configs.int_matrices(n, count, seed=8400 + n, lo=0, hi=1)
+    a_np[5, 0, 0] = 300
+    want = O.sz_batch(a_np)
+    bufs = [torch.from_numpy(a_np).cuda() for _ in range(2)]
+    outs = [torch.zeros(count, dtype=torch.int64, device="cuda") for _ in range(2)]
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for ready in (False, True):
+        for o in outs:
+            o.zero_()
+        for rep in range(6):
+            pl.store_zechin_permanent_batch(bufs[rep % 2], out=outs[rep % 2], status=status, input_ready=ready)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy(), want)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    for o in outs:
+        o.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(8):
+            pl.store_zechin_permanent_batch(bufs[i % 2], out=outs[i % 2], status=status, stream=s, input_ready=True)
+    g.replay()
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), want)
+    assert int(status.item()) == 0
