@@ -540,9 +540,10 @@ def measure_boson(steps, warmup, rank, world, device, flush_buf, fma=False, spec
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream(device)
     cap.wait_stream(stream)
+    ready = os.environ.get("PL_BENCH_INPUT_READY", "1") != "0"  # U is static: steps may overlap (PL_FLAG_INPUT_READY)
     with torch.cuda.graph(graph, stream=cap):
         for _ in range(steps):
-            B.distribution_probabilities(itf, modes, out=out, stream=cap, status=status, fma=fma)
+            B.distribution_probabilities(itf, modes, out=out, stream=cap, status=status, fma=fma, input_ready=ready)
     for _ in range(2):
         graph.replay()
     barrier()

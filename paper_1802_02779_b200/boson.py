@@ -244,12 +244,15 @@ def _distribution_checks(itf: Interferometer, input_modes, limits: Optional[Limi
 
 
 def distribution_probabilities(itf: Interferometer, input_modes: Sequence[int], first: int = 0,
-                               count: Optional[int] = None, fma: bool = False, out=None, stream=None, status=None):
+                               count: Optional[int] = None, fma: bool = False, out=None, stream=None, status=None,
+                               input_ready: bool = False):
     """Probabilities of patterns [first, first + count) of the full
     distribution, enumerated on the device (no enumeration_cap check: the
     pattern range is the caller's). With a CUDA ``out`` tensor the call runs
     on device buffers (``itf``'s cached device unitary) and, given ``status``,
-    is asynchronous on ``stream``."""
+    is asynchronous on ``stream``. ``input_ready=True`` (``PL_FLAG_INPUT_READY``, device path): the
+    unitary is not written by work still running on the stream, so back-to-back calls overlap
+    (the kernel computes before ``griddepcontrol.wait`` and stores after it)."""
     im = _check_input_modes(input_modes, itf.modes())
     total = pattern_count(itf.modes(), len(im))
     if count is None:
@@ -260,6 +263,8 @@ def distribution_probabilities(itf: Interferometer, input_modes: Sequence[int], 
         flags |= N.PL_FLAG_DEVICE_PTRS
         if status is not None:
             flags |= N.PL_FLAG_ASYNC
+        if input_ready:
+            flags |= N.PL_FLAG_INPUT_READY
         st = (stream or torch.cuda.current_stream(out.device)).cuda_stream
         u = itf.device_unitary(out.device)
         _check(N.lib.pl_boson_distribution(itf.modes(), u.data_ptr(), len(im), modes.ctypes.data, first, count,

@@ -63,6 +63,20 @@ pl_status launch_fused(const pl::BosonParams& p, bool enumerate, cudaStream_t st
     per_sm = std::max(per_sm, 1);
     const int64_t want = (p.count + pl::kBosonThreads - 1) / pl::kBosonThreads;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)plc::sm_count() * per_sm));
+    if (p.early) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3(pl::kBosonThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PLC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+        return PL_OK;
+    }
     kern<<<(unsigned)blocks, pl::kBosonThreads, smem, st>>>(p);
     PLC_CUDA(cudaGetLastError());
     return PL_OK;
@@ -283,6 +297,7 @@ pl_status pl_boson_distribution(int32_t m, const void* u, int32_t n, const int32
                         p.rows = nullptr;
                         p.probs = pd;
                         p.status = sd;
+                        p.early = ((flags & PL_FLAG_INPUT_READY) && (flags & PL_FLAG_DEVICE_PTRS)) ? 1 : 0;
                         return launch_fused_any(fma, n, p, true, st);
                     });
 }

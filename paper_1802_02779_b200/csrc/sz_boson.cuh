@@ -47,6 +47,7 @@ struct BosonParams {
     const int32_t* rows;    // given mode: count x n output rows; null = enumerate
     double* probs;          // count probabilities
     int32_t* status;        // PL_STATUS_BIT_ROWS on a malformed row list (may be null)
+    int early;              // PL_FLAG_INPUT_READY: compute before griddepcontrol.wait, store after
 };
 
 constexpr int kBosonBadRows = 0x2;  // = PL_STATUS_BIT_ROWS
@@ -147,6 +148,10 @@ __global__ void __launch_bounds__(kBosonThreads) sz_boson_kernel(BosonParams p) 
     const int stride = m + N;  // binomial table columns a = 0 .. m + N - 1
     uint64_t* cb = reinterpret_cast<uint64_t*>(smem_raw);
     double2* vs = reinterpret_cast<double2*>(smem_raw + (p.rows ? 0 : (size_t)(N + 1) * stride * sizeof(uint64_t)));
+    // programmatic dependent launch (launched with the attribute only when p.early; see
+    // sz_batch_tma_kernel): U and the rows are read at once, the stores wait for the previous grid
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    bool waited = !p.early;
     if (!p.rows) {
         for (int e = threadIdx.x; e < (N + 1) * stride; e += blockDim.x) {
             const int l = e / stride, a = e % stride;
@@ -194,9 +199,15 @@ __global__ void __launch_bounds__(kBosonThreads) sz_boson_kernel(BosonParams p) 
             for (int i = 0; i < N; ++i) rowp[i] = p.u + (size_t)r[i] * m;
             z = perm_accessor<R, N>([&](int i, int j) { return __ldg(rowp[i] + p.in[j]); }, ov);
         }
-        p.probs[t] = bad ? __longlong_as_double(0x7ff8000000000000LL) : boson_prob<R::kFma, N>(z, r);
+        const double pr = bad ? __longlong_as_double(0x7ff8000000000000LL) : boson_prob<R::kFma, N>(z, r);
+        if (!waited) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            waited = true;
+        }
+        p.probs[t] = pr;
         any_bad |= bad;
     }
+    if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (any_bad && p.status) atomicOr(p.status, kBosonBadRows);
 }
 

@@ -100,6 +100,38 @@ def test_distribution_device_buffers_async():
     assert int(st.item()) == 0
 
 
+def test_distribution_input_ready_overlapped_launches():
+    # PL_FLAG_INPUT_READY: the fused kernel computes before griddepcontrol.wait and stores after it;
+    # back-to-back and graph-replayed launches into alternating (and rewritten) outputs are bitwise
+    # the plain results
+    import torch
+
+    itf = B.haar_unitary(25, 2)
+    for modes in ([0, 1, 2, 3, 4], [3, 9, 20]):
+        host = B.distribution_probabilities(itf, modes)
+        outs = [torch.zeros(host.shape[0], dtype=torch.float64, device="cuda") for _ in range(2)]
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for i in range(7):
+            B.distribution_probabilities(itf, modes, out=outs[i % 2], status=st, input_ready=True)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy(), host)
+            o.zero_()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(9):
+                B.distribution_probabilities(itf, modes, out=outs[i % 2], status=st, stream=s, input_ready=True)
+        g.replay()
+        g.replay()
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy(), host)
+        assert int(st.item()) == 0
+
+
 @need_ref
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 8])
 def test_outcome_probabilities_vs_reference(n):
