@@ -734,6 +734,7 @@ def test_input_ready_flag_f32_packs_equal_to_oracle(n):
     count = 4 * 301 + 3
     a_np = configs.int_matrices(n, count, seed=8400 + n, lo=0, hi=1)
     a_np[5, 0, 0] = 300
+    a_np[9, 0, 0] = 10 ** 9  # leaves the FP32-exact range: its pack runs member by member (int64 paths)
     want = O.sz_batch(a_np)
     bufs = [torch.from_numpy(a_np).cuda() for _ in range(2)]
     outs = [torch.zeros(count, dtype=torch.int64, device="cuda") for _ in range(2)]
