@@ -84,9 +84,11 @@ typedef struct pl_limits {
                                  /* written by work still running on `stream` (it was uploaded   */
                                  /* or produced earlier and that work has completed, or on       */
                                  /* another stream the caller has already waited for). The batch */
-                                 /* kernels of orders <= 5 then start loading while the previous */
-                                 /* kernel on the stream drains (programmatic dependent launch); */
-                                 /* their stores still wait for it. Results are identical.       */
+                                 /* kernels of orders <= 5, the int64 pack kernel (10 <= n <= 14)*/
+                                 /* and the fused boson kernel (pl_boson_distribution) then start*/
+                                 /* loading while the previous kernel on the stream drains       */
+                                 /* (programmatic dependent launch); their stores still wait for */
+                                 /* it. Results are identical; other kernels ignore the flag.    */
 
 /* Bits OR-ed into a caller-owned device status word by PL_FLAG_ASYNC calls. */
 #define PL_STATUS_BIT_OVERFLOW 0x1
