@@ -70,7 +70,8 @@ bool is_prime_u32(u64 n) {
 }
 
 // The K largest primes below 2^31, descending from 2^31 - 1 (each > 2^30).
-const std::vector<uint32_t>& primes_desc(size_t k) {
+// (a copy made under the lock: the cache may grow in another thread)
+std::vector<uint32_t> primes_desc(size_t k) {
     static std::mutex mu;
     static std::vector<uint32_t> cache;
     static u64 next = (1ull << 31) - 1;
@@ -80,7 +81,7 @@ const std::vector<uint32_t>& primes_desc(size_t k) {
         cache.push_back((uint32_t)next);
         next -= 2;
     }
-    return cache;
+    return std::vector<uint32_t>(cache.begin(), cache.begin() + (std::ptrdiff_t)k);
 }
 
 // One CTA per prime: X[S] over all column subsets S as bit masks in shared
@@ -409,8 +410,8 @@ pl_status pl_sz_permanent_modp(int32_t n, int32_t nprimes, const uint32_t* prime
 
 int32_t pl_bigint_primes(int32_t count, uint32_t* out) {
     if (count < 1 || !out) return 0;
-    const std::vector<uint32_t>& ps = primes_desc((size_t)count);
-    std::copy(ps.begin(), ps.begin() + count, out);
+    const std::vector<uint32_t> ps = primes_desc((size_t)count);
+    std::copy(ps.begin(), ps.end(), out);
     return count;
 }
 
@@ -437,7 +438,7 @@ pl_status permanent_bigint(bool ryser, int32_t n, const int64_t* a, uint64_t* li
         bits += bit_length(rs);
     }
     const int k = std::max(1, (bits + 2 + 29) / 30);  // every prime > 2^30: prod > 2^(30 k) >= 2^(B + 2)
-    std::vector<uint32_t> ps(primes_desc((size_t)k).begin(), primes_desc((size_t)k).begin() + k);
+    const std::vector<uint32_t> ps = primes_desc((size_t)k);
     std::vector<int64_t> res((size_t)k * n * n);
     for (int i = 0; i < k; ++i) {
         const int64_t p = ps[i];
