@@ -84,8 +84,10 @@ typedef struct pl_limits {
                                  /* written by work still running on `stream` (it was uploaded   */
                                  /* or produced earlier and that work has completed, or on       */
                                  /* another stream the caller has already waited for). The batch */
-                                 /* kernels of orders <= 5, the int64 pack kernel (10 <= n <= 14)*/
-                                 /* and the fused boson kernel (pl_boson_distribution) then start*/
+                                 /* kernels of orders <= 5, the shared-memory kernels of orders  */
+                                 /* 6..14 (warp / CTA per matrix, the int64 FP32 packs; not the  */
+                                 /* two-matrix float packs) and the fused boson kernel           */
+                                 /* (pl_boson_distribution) then start                           */
                                  /* loading while the previous kernel on the stream drains       */
                                  /* (programmatic dependent launch); their stores still wait for */
                                  /* it. Results are identical; other kernels ignore the flag.    */

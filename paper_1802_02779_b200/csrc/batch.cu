@@ -264,8 +264,14 @@ pl_status launch_smem_n(pl_dtype dt, const void* a, void* out, int64_t count, in
     PL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pl::kSmemThreads, smem));
     per_sm = std::max(per_sm, 1);
     const int64_t blocks = std::min<int64_t>(count, (int64_t)num_sms() * per_sm);
+    if (plc::input_ready_hint()) {  // PL_FLAG_INPUT_READY: see launch_f32_pack_n
+        PL_CUDA(launch_pdl(kern, (unsigned)blocks, (unsigned)pl::kSmemThreads, smem, st, static_cast<const T*>(a),
+                           static_cast<T*>(out), count, (int)N, (int)max_layer(N), (const uint16_t*)pt.tab,
+                           (const uint32_t*)pt.off, pt.t32(sizeof(T)), status, 1));
+        return PL_OK;
+    }
     kern<<<(unsigned)blocks, pl::kSmemThreads, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out), count, N,
-                                              (int)max_layer(N), pt.tab, pt.off, pt.t32(sizeof(T)), status);
+                                              (int)max_layer(N), pt.tab, pt.off, pt.t32(sizeof(T)), status, 0);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }
@@ -393,8 +399,15 @@ pl_status launch_warp_n(const void* a, void* out, int64_t count, int32_t* status
     per_sm = std::max(per_sm, 1);
     const int64_t blocks = std::min<int64_t>((count + pl::kWarpKernelWarps - 1) / pl::kWarpKernelWarps,
                                              (int64_t)num_sms() * per_sm);
+    if (plc::input_ready_hint()) {  // PL_FLAG_INPUT_READY: see launch_f32_pack_n
+        PL_CUDA(launch_pdl(kern, (unsigned)blocks, (unsigned)(32 * pl::kWarpKernelWarps), smem, st,
+                           static_cast<const T*>(a), static_cast<T*>(out), count, (const uint16_t*)pt.tab,
+                           (const uint32_t*)pt.off, pt.t32(sizeof(T)), status, 1));
+        return PL_OK;
+    }
     kern<<<(unsigned)blocks, 32 * pl::kWarpKernelWarps, smem, st>>>(static_cast<const T*>(a), static_cast<T*>(out),
-                                                                   count, pt.tab, pt.off, pt.t32(sizeof(T)), status);
+                                                                   count, pt.tab, pt.off, pt.t32(sizeof(T)), status,
+                                                                   0);
     PL_CUDA(cudaGetLastError());
     return PL_OK;
 }

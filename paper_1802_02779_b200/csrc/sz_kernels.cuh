@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
                                                             int n_rt, int maxc, const uint16_t* __restrict__ ptab,
                                                             const uint32_t* __restrict__ poff,
                                                             const uint32_t* __restrict__ ptab32,
-                                                            int32_t* __restrict__ status) {
+                                                            int32_t* __restrict__ status, int early_loads) {
     using T = typename R::T;
     constexpr int n = N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -426,6 +426,9 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
     T* buf0 = mat + ((n * n + 1) & ~1);
     T* buf1 = buf0 + ((maxc + 1) & ~1);
     const int tid = threadIdx.x, nt = blockDim.x;
+    // programmatic dependent launch, as in sz_batch_f32_pack_kernel (no-ops under a plain launch)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (!early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
     for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
         const T* g = a + b * n * n;
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kSmemThreads) sz_batch_smem_kernel(const typen
             if (tid == 0) total = smem_top<R, T, N>(mat, last, n, ov);
         }
         if (tid == 0) {
+            if (early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // before this grid's stores
             if ((flag & 1) || ov) {
                 atomicOr(status, 1);
                 total = R::zero();
@@ -904,9 +908,11 @@ template <class R, int N>
 __global__ void __launch_bounds__(32 * kWarpKernelWarps) sz_batch_warp_kernel(
     const typename R::T* __restrict__ a, typename R::T* __restrict__ out, int64_t count,
     const uint16_t* __restrict__ ptab, const uint32_t* __restrict__ poff, const uint32_t* __restrict__ ptab32,
-    int32_t* __restrict__ status) {
+    int32_t* __restrict__ status, int early_loads) {
     using T = typename R::T;
     static_assert(sizeof(T) == 8, "8-byte rings only");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // see sz_batch_f32_pack_kernel
+    if (!early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     constexpr int E = N * N;
     constexpr int MAXC = (int)binom_u64(N, N / 2);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -947,13 +953,17 @@ __global__ void __launch_bounds__(32 * kWarpKernelWarps) sz_batch_warp_kernel(
         }
         ov = __any_sync(0xffffffffu, ov);
         if (lane == 0) {
+            if (early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // before this grid's stores
             if (ov) total = R::zero();
             out[b] = total;
         }
         ov_any |= ov;
         __syncwarp();
     }
-    if (ov_any && lane == 0) atomicOr(status, 1);
+    if (ov_any && lane == 0) {
+        if (early_loads) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        atomicOr(status, 1);
+    }
 }
 
 // ---------------------------------------------------------------- layer 2

@@ -674,14 +674,15 @@ def test_blocked_f32_pack_kernel_opt_in():
         assert np.array_equal(np.load("/tmp/_blk_f32_%d.npy" % n), O.sz_batch(a))
 
 
-@pytest.mark.parametrize("dtype,n", [("int64", 5), ("complex128", 5), ("float64", 4), ("complex128", 3), ("int64", 1)])
+@pytest.mark.parametrize("dtype,n", [("int64", 5), ("complex128", 5), ("float64", 4), ("complex128", 3), ("int64", 1),
+                                     ("int64", 7), ("float64", 8), ("complex128", 9), ("complex128", 12)])
 def test_input_ready_flag_overlapped_launches_equal_to_oracle(dtype, n):
     # PL_FLAG_INPUT_READY: the n <= 5 batch kernel loads before griddepcontrol.wait, so back-to-back
     # launches (plain stream and CUDA graph) overlap; every launch's results are those of the oracle,
     # also with a ragged tail (count % 32 != 0), a misaligned input and an output the previous launch wrote
     import torch
 
-    count = 32 * 257 + 19
+    count = 32 * 257 + 19 if n <= 5 else 32 * 20 + 19  # n >= 6: the warp / CTA shared-memory kernels
     if dtype == "int64":
         a_np = configs.int_matrices(n, count, seed=8100 + n, lo=-9, hi=9)
     elif dtype == "float64":
